@@ -1,0 +1,1136 @@
+// engine.cu — host orchestration and the C-ABI (include/cqr.h).
+//
+// Restates the reference's execution engine (proj/src/engine.cpp:78-305) for
+// one process per GPU: the tall matrix stays in HBM, every stage is a
+// stream-ordered launch of the sm_100a kernels, failures are a device status
+// word (so an attempt needs ONE host synchronisation, at its end), the retry
+// loop mirrors engine.cpp:137-209 (sizes llround(l*growth^a), seeds
+// derive(seed, a)), and the reference's simulated workers (engine.cpp:12-39,
+// parexec.cpp) become row-block shards on separate GPUs whose s x n sketch and
+// n x n Gram partials are summed with NCCL all-reduce over NVLink.
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/cqr.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using cqr::DevStatus;
+
+namespace {
+
+constexpr double kU = 2.220446049250313e-16;  // types.hpp:31
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct StageEv {
+  int stage;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct cqr_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  DevBuf bufs[24];
+  DevStatus* status = nullptr;   // device
+  DevStatus* status_h = nullptr;  // pinned host
+  double* scal_h = nullptr;       // pinned host scalars
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<StageEv> stage_evs;
+  long long launches = 0;
+  int tiles_key = -1;  // gram tile table currently on the device
+};
+
+namespace {
+
+enum BufId {
+  B_A1 = 0, B_SKPART, B_GPART, B_GTILES, B_G, B_RT, B_RH, B_R, B_RTMP, B_SGN, B_PACK1, B_PACK2, B_WORK,
+  B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X
+};
+
+struct Fail {
+  int code;
+  long long index;
+  std::string msg;
+};
+
+void* buf(cqr_ctx* c, int id, size_t bytes) {
+  DevBuf& b = c->bufs[id];
+  if (bytes == 0) bytes = 8;
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      throw Fail{CQR_OUT_OF_MEMORY, -1, "cudaMalloc of " + std::to_string(bytes) + " bytes failed"};
+    }
+    b.bytes = bytes;
+  }
+  return b.p;
+}
+
+template <typename T>
+T* dbuf(cqr_ctx* c, int id, size_t count) {
+  return static_cast<T*>(buf(c, id, count * sizeof(T)));
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Fail{CQR_CUDA_ERROR, -1, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+void ckn(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Fail{CQR_NCCL_ERROR, -1, std::string(what) + ": " + ncclGetErrorString(r)};
+}
+
+#define LAUNCH(c, expr)          \
+  do {                           \
+    ck((expr), #expr);           \
+    ++(c)->launches;             \
+  } while (0)
+
+void require(bool cond, const char* msg) {
+  if (!cond) throw Fail{CQR_INVALID_ARGUMENT, -1, msg};
+}
+
+bool vec_ok(const void* p, long long ld, int n) {
+  return (ld % 2 == 0) && (n % 2 == 0) && ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+}
+
+// ---- rng on the host (rng.hpp:22-42) -----------------------------------------------
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t derive(uint64_t seed, uint64_t salt) { return mix64(seed ^ mix64(salt + 0x51ED270B8A5EC473ull)); }
+double unit_at(uint64_t seed, uint64_t k) {
+  return static_cast<double>(mix64(seed + (k + 1) * 0x9E3779B97F4A7C15ull) >> 11) * 0x1.0p-53;
+}
+
+long long resolved_size(const cqr_sketch_cfg& cfg, long long m, long long n) {  // sketch.cpp:20-23
+  long long l = cfg.size > 0 ? cfg.size : static_cast<long long>(std::ceil(cfg.rate * static_cast<double>(n)));
+  return std::clamp(l, n, m);
+}
+
+cqr_sketch_cfg default_cfg() {
+  cqr_sketch_cfg c{};
+  c.strategy = CQR_UNIFORM;
+  c.rate = 2.0;
+  c.max_retries = 2;
+  c.retry_growth = 2.0;
+  return c;
+}
+
+cqr_options default_opts() {
+  cqr_options o{};
+  o.shift_kind = CQR_SHIFT_THEORY;
+  o.workers = 1;
+  return o;
+}
+
+// kernels.hpp:272-310 one-sided Jacobi singular values (cond_x diagnostics of
+// the n x n R-hat; engine.cpp:94-100).
+bool svd_values(std::vector<double> w, int rows, int c, std::vector<double>& sv) {
+  // w column-major rows x c
+  const double tol = 10.0 * kU * std::sqrt(static_cast<double>(rows));
+  auto dot = [&](int p, int q) {
+    double s = 0.0;
+    for (int i = 0; i < rows; ++i) s = std::fma(w[(size_t)p * rows + i], w[(size_t)q * rows + i], s);
+    return s;
+  };
+  bool conv = c <= 1;
+  for (int sweep = 0; sweep < 100 && !conv; ++sweep) {
+    conv = true;
+    for (int p = 0; p < c - 1; ++p)
+      for (int q = p + 1; q < c; ++q) {
+        const double al = dot(p, p), be = dot(q, q), ga = dot(p, q);
+        if (std::abs(ga) <= tol * std::sqrt(al * be)) continue;
+        conv = false;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = cs * t;
+        for (int i = 0; i < rows; ++i) {
+          const double a = w[(size_t)p * rows + i], b = w[(size_t)q * rows + i];
+          w[(size_t)p * rows + i] = cs * a - sn * b;
+          w[(size_t)q * rows + i] = sn * a + cs * b;
+        }
+      }
+  }
+  if (!conv) return false;
+  sv.resize(c);
+  for (int j = 0; j < c; ++j) sv[j] = std::sqrt(dot(j, j));
+  std::sort(sv.begin(), sv.end(), std::greater<double>());
+  return true;
+}
+
+// ---- stage timing (StageClock, engine.hpp:14-41, with CUDA events) -----------------
+cudaEvent_t next_event(cqr_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+struct StageScope {
+  cqr_ctx* c;
+  StageEv ev;
+  StageScope(cqr_ctx* c_, int stage) : c(c_) {
+    ev.stage = stage;
+    ev.a = next_event(c);
+    ev.b = next_event(c);
+    ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
+  }
+  ~StageScope() {
+    cudaEventRecord(ev.b, c->stream);
+    c->stage_evs.push_back(ev);
+  }
+};
+
+struct Report {
+  std::vector<cqr_stage_info> stages;
+  long long sketch_rows = 0;
+};
+
+void push_stage(Report& r, int stage, int retries = 0, bool has_shift = false, double shift = 0.0,
+                bool has_cond = false, double cond = 0.0) {
+  cqr_stage_info s{};
+  s.stage = stage;
+  s.retries = retries;
+  s.has_shift = has_shift ? 1 : 0;
+  s.shift = shift;
+  s.has_cond_x = has_cond ? 1 : 0;
+  s.cond_x = cond;
+  r.stages.push_back(s);
+}
+
+// ---- engine ---------------------------------------------------------------------------
+struct Job {
+  cqr_ctx* c;
+  int method;
+  const double* a;  // device, this rank's shard
+  long long m_local, m_global, row0;
+  int n;
+  long long lda;
+  double* q;  // device
+  long long ldq;
+  cqr_sketch_cfg cfg;
+  cqr_options opts;
+  cqr_precond_fn precond = nullptr;
+  void* user = nullptr;
+};
+
+void allreduce(cqr_ctx* c, double* p, size_t count) {
+  if (c->world <= 1) return;
+  ckn(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->comm, c->stream), "ncclAllReduce");
+}
+
+// Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
+void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g) {
+  cqr::GramPlan p = cqr::gram_plan(m, n);
+  double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.partial_doubles, 1));
+  int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
+  const int key = p.np * 100000 + p.parts * 100 + p.maxt;
+  if (c->tiles_key != key) {  // the table depends on (np, parts, maxt) only: upload once
+    std::vector<int32_t> ht(p.tiles_bytes / sizeof(int32_t));
+    cqr::gram_tiles(p, ht.data());
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    ck(cudaMemcpy(tiles, ht.data(), p.tiles_bytes, cudaMemcpyHostToDevice), "tiles H2D");
+    c->tiles_key = key;
+  }
+  if (m > 0) {
+    LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, c->status, c->stream));
+    LAUNCH(c, cqr::launch_gram_combine(p, part, g, c->world <= 1 ? 1 : 0, c->status, c->stream));
+  } else {
+    ck(cudaMemsetAsync(g, 0, sizeof(double) * n * n, c->stream), "memset");
+  }
+  if (c->world > 1) {
+    allreduce(c, g, (size_t)n * n);
+    LAUNCH(c, cqr::launch_mirror_upper(g, n, c->status, c->stream));
+  }
+}
+
+// X R = A on device rows; in may alias out.
+void trisolve_dev(cqr_ctx* c, const double* in, long long ldi, double* out, long long ldo, long long m, int n,
+                  const double* pack, const double* sgn) {
+  if (m <= 0) return;
+  cqr::TrisolveArgs t{};
+  t.in = in;
+  t.ldi = ldi;
+  t.out = out;
+  t.ldo = ldo;
+  t.m = m;
+  t.n = n;
+  t.pack = pack;
+  t.sgn = sgn;
+  t.vec16 = (vec_ok(in, ldi, n) && vec_ok(out, ldo, n)) ? 1 : 0;
+  t.num_sms = c->num_sms;
+  t.status = c->status;
+  LAUNCH(c, cqr::launch_trisolve(t, c->stream));
+}
+
+void reset_status(cqr_ctx* c) { ck(cudaMemsetAsync(c->status, 0, sizeof(DevStatus), c->stream), "status reset"); }
+
+DevStatus read_status(cqr_ctx* c) {
+  ck(cudaMemcpyAsync(c->status_h, c->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream), "status D2H");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  return *c->status_h;
+}
+
+void check_finite(cqr_ctx* c, const double* a, long long m, int n, long long lda);
+
+// One CholeskyQR pass (engine.cpp:78-92): G = X^T X (+shift I), R = chol(G),
+// X <- X R^{-1} (in -> out). shift_mode 0/1/2 as launch_cholesky.
+void cholesky_pass(Job& j, const double* in, long long ldi, Report& rep, double* r_out, int shift_mode,
+                   double shift_value, const double* sgn_for_solve = nullptr, bool defer_solve = false) {
+  cqr_ctx* c = j.c;
+  const int n = j.n;
+  double* g = dbuf<double>(c, B_G, (size_t)n * n);
+  {
+    StageScope t(c, CQR_STAGE_GRAM);
+    gram_dev(c, in, j.m_local, n, ldi, g);
+  }
+  push_stage(rep, CQR_STAGE_GRAM);
+  double* work = dbuf<double>(c, B_WORK, (size_t)n * n);
+  double* shift_d = dbuf<double>(c, B_SCAL, 4);
+  {
+    StageScope t(c, CQR_STAGE_CHOLESKY);
+    const double coef =
+        11.0 * ((double)j.m_global * (double)n + (double)n * (double)(n + 1)) * kU;  // cholqr.cpp:21-26
+    LAUNCH(c, cqr::launch_cholesky(g, n, r_out, work, shift_mode, shift_value, coef, shift_d, c->status, c->stream));
+  }
+  // the theory shift is resolved on the device; its value is patched into the
+  // report after the attempt's single synchronisation
+  push_stage(rep, CQR_STAGE_CHOLESKY, 0, shift_mode != 0, shift_value);
+  if (defer_solve) return;
+  double* pack = dbuf<double>(c, B_PACK2, cqr::trisolve_pack_doubles(n));
+  {
+    StageScope t(c, CQR_STAGE_TRISOLVE);
+    LAUNCH(c, cqr::launch_pack_r(r_out, n, n, pack, 0, c->status, c->stream));
+    trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, n, pack, sgn_for_solve);
+  }
+  push_stage(rep, CQR_STAGE_TRISOLVE);
+}
+
+struct Outcome {
+  Report rep;
+  bool has_r = false;
+  const double* r_dev = nullptr;
+};
+
+// engine.cpp:241-284
+Outcome run_cholqr_family(Job& j) {
+  cqr_ctx* c = j.c;
+  const int n = j.n;
+  Outcome o;
+  reset_status(c);
+  double* r1 = dbuf<double>(c, B_RT, (size_t)n * n);
+  double* r2 = dbuf<double>(c, B_RH, (size_t)n * n);
+  double* r3 = dbuf<double>(c, B_RTMP, (size_t)n * n);
+  double* r = dbuf<double>(c, B_R, (size_t)n * n);
+  const bool r_less = j.opts.r_less != 0;
+  if (j.method == CQR_CHOLQR) {
+    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0);
+    o.has_r = !r_less;
+    o.r_dev = r1;
+  } else if (j.method == CQR_CHOLQR2) {
+    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0);
+    cholesky_pass(j, j.q, j.ldq, o.rep, r2, 0, 0.0);
+    if (!r_less) {
+      StageScope t(c, CQR_STAGE_RECOVER);
+      LAUNCH(c, cqr::launch_triangular_product(r2, r1, n, r, c->status, c->stream));
+    }
+    if (!r_less) push_stage(o.rep, CQR_STAGE_RECOVER);
+    o.has_r = !r_less;
+    o.r_dev = r;
+  } else {  // CQR_SCHOLQR3
+    const int mode = j.opts.shift_kind == CQR_SHIFT_FIXED ? 1 : 2;
+    cholesky_pass(j, j.a, j.lda, o.rep, r1, mode, j.opts.shift_value);
+    cholesky_pass(j, j.q, j.ldq, o.rep, r2, 0, 0.0);
+    double* r3b = dbuf<double>(c, B_X, (size_t)n * n);
+    cholesky_pass(j, j.q, j.ldq, o.rep, r3b, 0, 0.0);
+    if (!r_less) {
+      StageScope t(c, CQR_STAGE_RECOVER);
+      LAUNCH(c, cqr::launch_triangular_product(r2, r1, n, r3, c->status, c->stream));
+      LAUNCH(c, cqr::launch_triangular_product(r3b, r3, n, r, c->status, c->stream));
+    }
+    if (!r_less) push_stage(o.rep, CQR_STAGE_RECOVER);
+    o.has_r = !r_less;
+    o.r_dev = r;
+  }
+  DevStatus s = read_status(c);
+  if (s.code != 0) throw Fail{s.code, s.index, s.code == 1 ? "cholesky breakdown" : "singular triangular factor"};
+  if (j.method == CQR_SCHOLQR3 && j.opts.shift_kind != CQR_SHIFT_FIXED) {
+    ck(cudaMemcpy(c->scal_h, dbuf<double>(c, B_SCAL, 4), sizeof(double), cudaMemcpyDeviceToHost), "shift D2H");
+    for (auto& st : o.rep.stages)
+      if (st.has_shift) {
+        st.shift = c->scal_h[0];
+        break;
+      }
+  }
+  return o;
+}
+
+// engine.cpp:137-209 with the device pipeline.
+Outcome run_precond(Job& j) {
+  cqr_ctx* c = j.c;
+  const int n = j.n;
+  const long long m = j.m_global;
+  const long long base_l = resolved_size(j.cfg, m, n);
+  const bool r_less = j.opts.r_less != 0;
+  if (j.cfg.strategy == CQR_LEVERAGE)
+    throw Fail{CQR_INVALID_ARGUMENT, -1, "leverage sampling needs an oracle Q; call sample_rows_leverage directly"};
+  for (int attempt = 0;; ++attempt) {
+    cqr_sketch_cfg try_cfg = j.cfg;
+    try_cfg.size = std::min<long long>(
+        m, static_cast<long long>(std::llround(static_cast<double>(base_l) * std::pow(j.cfg.retry_growth, attempt))));
+    const uint64_t seed = attempt == 0 ? j.cfg.seed : derive(j.cfg.seed, static_cast<uint64_t>(attempt));
+    const bool last = attempt >= j.cfg.max_retries;
+    const long long l = resolved_size(try_cfg, m, n);
+    Outcome o;
+    reset_status(c);
+    double* a1 = dbuf<double>(c, B_A1, (size_t)l * n);
+    // ---- Sketch (sketch.cpp:94-127)
+    {
+      StageScope t(c, CQR_STAGE_SKETCH);
+      if (try_cfg.strategy == CQR_GAUSSIAN) {
+        cqr::SketchPlan sp = cqr::sketch_plan(j.m_local, n, (int)l, c->num_sms);
+        double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
+        if (j.m_local > 0) {
+          LAUNCH(c, cqr::launch_sketch_gaussian(sp, j.a, j.lda, m, j.row0, seed, part,
+                                                vec_ok(j.a, j.lda, n) ? 1 : 0, c->status, c->stream));
+          LAUNCH(c, cqr::launch_sketch_reduce(sp, part, a1, c->status, c->stream));
+        } else {
+          ck(cudaMemsetAsync(a1, 0, sizeof(double) * l * n, c->stream), "memset");
+        }
+      } else {  // Uniform (sketch.cpp:27-55)
+        long long* idx = nullptr;
+        if (try_cfg.without_replacement) {
+          std::vector<long long> h;
+          std::unordered_set<long long> seen;
+          uint64_t pos = 0;
+          while ((long long)h.size() < l) {
+            const long long i = (long long)(unit_at(seed, pos++) * (double)m);
+            if (seen.insert(i).second) h.push_back(i);
+          }
+          idx = dbuf<long long>(c, B_IDX, (size_t)l);
+          ck(cudaMemcpyAsync(idx, h.data(), sizeof(long long) * l, cudaMemcpyHostToDevice, c->stream), "idx H2D");
+          ck(cudaStreamSynchronize(c->stream), "sync");
+        }
+        LAUNCH(c, cqr::launch_gather_rows(j.a, j.lda, j.m_local, m, j.row0, n, (int)l, seed, idx, a1, nullptr,
+                                          c->status, c->stream));
+      }
+      allreduce(c, a1, (size_t)l * n);
+    }
+    // ---- Precondition: R~ = QR/LU of A1 (kernels.hpp:175-257)
+    double* rt = dbuf<double>(c, B_RT, (size_t)n * n);
+    double* work = dbuf<double>(c, B_WORK, std::max<size_t>((size_t)l * n, (size_t)n * n));
+    double* pack1 = dbuf<double>(c, B_PACK1, cqr::trisolve_pack_doubles(n));
+    {
+      StageScope t(c, CQR_STAGE_PRECONDITION);
+      if (j.precond) {
+        std::vector<double> ha((size_t)l * n), hr((size_t)n * n, 0.0);
+        ck(cudaMemcpyAsync(ha.data(), a1, sizeof(double) * l * n, cudaMemcpyDeviceToHost, c->stream), "a1 D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        int64_t idx = -1;
+        const int st = j.precond(j.user, ha.data(), l, n, hr.data(), &idx);
+        if (st == CQR_SINGULAR_TRIANGULAR) {
+          if (last) throw Fail{CQR_SINGULAR_TRIANGULAR, idx, "preconditioner: singular triangular factor"};
+          continue;
+        }
+        if (st != CQR_OK) throw Fail{st, idx, "preconditioner failed"};
+        ck(cudaMemcpyAsync(rt, hr.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "rt H2D");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+      } else if (j.method == CQR_RLU) {
+        LAUNCH(c, cqr::launch_lu_u(a1, (int)l, n, rt, work, c->status, c->stream));
+      } else {
+        LAUNCH(c, cqr::launch_qr_r(a1, (int)l, n, rt, work, c->status, c->stream));
+      }
+      // degenerate_diagonal (engine.cpp:118-127) + packing for the solve
+      LAUNCH(c, cqr::launch_pack_r(rt, n, n, pack1, 1, c->status, c->stream));
+    }
+    push_stage(o.rep, CQR_STAGE_SKETCH, attempt);
+    // ---- X = A R~^{-1} (A -> Q buffer; A stays intact for a retry)
+    {
+      StageScope t(c, CQR_STAGE_TRISOLVE);
+      trisolve_dev(c, j.a, j.lda, j.q, j.ldq, j.m_local, n, pack1, nullptr);
+    }
+    const bool diag = j.opts.diagnostics != 0;
+    // ---- CholeskyQR on X (Gram, Cholesky; the solve is deferred past Recover so
+    // the sign normalisation of engine.cpp:109-116 can be fused into it)
+    double* rh = dbuf<double>(c, B_RH, (size_t)n * n);
+    Report pass;
+    cholesky_pass(j, j.q, j.ldq, pass, rh, 0, 0.0, nullptr, true);
+    double cond = 0.0;
+    if (diag) {  // cond(X) = cond(R^) (engine.cpp:94-100), NaN/inf when the pass fails
+      DevStatus s = read_status(c);
+      if (s.code == 0) {
+        std::vector<double> hr((size_t)n * n), w((size_t)n * n);
+        ck(cudaMemcpy(hr.data(), rh, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "rh D2H");
+        for (int i = 0; i < n; ++i)
+          for (int k = 0; k < n; ++k) w[(size_t)k * n + i] = hr[(size_t)i * n + k];
+        std::vector<double> sv;
+        if (svd_values(w, n, n, sv))
+          cond = sv.back() > 0.0 ? sv.front() / sv.back() : std::numeric_limits<double>::infinity();
+        else
+          cond = std::numeric_limits<double>::quiet_NaN();
+      } else {
+        cond = std::numeric_limits<double>::infinity();
+      }
+    }
+    push_stage(o.rep, CQR_STAGE_PRECONDITION, 0, false, 0.0, diag, cond);
+    for (auto& s : pass.stages) o.rep.stages.push_back(s);
+    double* r = dbuf<double>(c, B_R, (size_t)n * n);
+    double* sgn = dbuf<double>(c, B_SGN, (size_t)n);
+    if (!r_less) {
+      StageScope t(c, CQR_STAGE_RECOVER);
+      LAUNCH(c, cqr::launch_triangular_product(rh, rt, n, r, c->status, c->stream));
+      LAUNCH(c, cqr::launch_normalize_sign(r, n, sgn, c->status, c->stream));
+    }
+    double* pack2 = dbuf<double>(c, B_PACK2, cqr::trisolve_pack_doubles(n));
+    {
+      StageScope t(c, CQR_STAGE_TRISOLVE);
+      LAUNCH(c, cqr::launch_pack_r(rh, n, n, pack2, 0, c->status, c->stream));
+      trisolve_dev(c, j.q, j.ldq, j.q, j.ldq, j.m_local, n, pack2, r_less ? nullptr : sgn);
+    }
+    push_stage(o.rep, CQR_STAGE_TRISOLVE);
+    if (!r_less) push_stage(o.rep, CQR_STAGE_RECOVER);
+    DevStatus s = read_status(c);
+    if (s.code == 0) {
+      o.has_r = !r_less;
+      o.r_dev = r;
+      o.rep.sketch_rows = l;
+      return o;
+    }
+    if ((s.code == CQR_CHOLESKY_BREAKDOWN || s.code == CQR_SINGULAR_TRIANGULAR) && !last) continue;
+    throw Fail{s.code, s.index, s.code == 1 ? "cholesky breakdown" : "singular triangular factor"};
+  }
+}
+
+void fill_report(cqr_ctx* c, cqr_report* rep, const Outcome* o, int status, long long index, bool r_less,
+                 int method, long long n, long long l) {
+  // stage times from the recorded events (accumulated across attempts)
+  double ms[CQR_STAGE_COUNT] = {0};
+  for (auto& e : c->stage_evs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(e.b) == cudaSuccess && cudaEventElapsedTime(&t, e.a, e.b) == cudaSuccess)
+      ms[e.stage] += t;
+  }
+  cudaGetLastError();
+  c->stage_evs.clear();
+  c->ev_used = 0;
+  if (!rep) return;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->status = status;
+  rep->index = index;
+  rep->r_less = r_less ? 1 : 0;
+  double tot = 0.0;
+  for (int s = 0; s < CQR_STAGE_COUNT; ++s) {
+    rep->stage_ms[s] = ms[s];
+    tot += ms[s];
+  }
+  rep->total_ms = tot;
+  if (o) {
+    rep->n_stages = (int)std::min<size_t>(o->rep.stages.size(), CQR_MAX_STAGE_INFOS);
+    for (int i = 0; i < rep->n_stages; ++i) rep->stages[i] = o->rep.stages[i];
+    rep->sketch_rows = o->rep.sketch_rows;
+  }
+  int rmin, rmax;
+  double vmin, vmax;
+  cqr_comm_model(method, c->world, n, l, &rmin, &rmax, &vmin, &vmax);
+  rep->comm_rounds = rmax;
+  rep->comm_volume = vmax;
+}
+
+template <typename F>
+int guarded(cqr_ctx* c, F&& f) {
+  try {
+    f();
+    return CQR_OK;
+  } catch (const Fail& e) {
+    if (c) c->err = e.msg;
+    return e.code;
+  }
+}
+
+// device-side finiteness check (engine.cpp:222, errors.hpp:89-93)
+__global__ void finite_kernel(const double* __restrict__ a, long long lda, long long m, int n, DevStatus* st) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m * n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / n, j = e - (e / n) * n;
+    if (!isfinite(a[i * lda + j])) {
+      cqr::set_status(st, CQR_INVALID_ARGUMENT, i);
+      return;
+    }
+  }
+}
+
+void check_finite(cqr_ctx* c, const double* a, long long m, int n, long long lda) {
+  if (m <= 0) return;
+  finite_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(a, lda, m, n, c->status);
+  ck(cudaGetLastError(), "finite_kernel");
+  ++c->launches;
+}
+
+int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_report* report) {
+  Outcome o;
+  long long index = -1;
+  const bool r_less = j.opts.r_less != 0;
+  const long long l =
+      (j.m_global >= j.n && j.n >= 1) ? resolved_size(j.cfg, j.m_global, j.n) : 0;
+  c->stage_evs.clear();
+  c->ev_used = 0;
+  int st = CQR_OK;
+  try {
+    require(j.n >= 1 && j.m_global >= j.n, "need m >= n >= 1");
+    require(j.lda >= j.n && j.ldq >= j.n, "leading dimension must be >= n");
+    require(j.m_local >= 0 && j.row0 >= 0 && j.row0 + j.m_local <= j.m_global, "bad shard");
+    require(j.n <= 512, "n > 512 is not supported by the device kernels");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    // non-finite input is rejected up front (engine.cpp:222)
+    reset_status(c);
+    check_finite(c, j.a, j.m_local, j.n, j.lda);
+    {
+      DevStatus s0 = read_status(c);
+      int bad = s0.code != 0;
+      if (c->world > 1) {
+        int* flag = dbuf<int>(c, B_DIAG, 1);
+        ck(cudaMemcpyAsync(flag, &bad, sizeof(int), cudaMemcpyHostToDevice, c->stream), "flag");
+        ckn(ncclAllReduce(flag, flag, 1, ncclInt, ncclMax, c->comm, c->stream), "allreduce flag");
+        ck(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "flag");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+      }
+      if (bad) throw Fail{CQR_INVALID_ARGUMENT, -1, "A has non-finite entries"};
+    }
+    switch (j.method) {
+      case CQR_CHOLQR:
+      case CQR_CHOLQR2:
+      case CQR_SCHOLQR3:
+        o = run_cholqr_family(j);
+        break;
+      case CQR_RQR:
+      case CQR_RLU:
+        o = run_precond(j);
+        break;
+      case CQR_RQR_GAUSSIAN:
+        j.cfg.strategy = CQR_GAUSSIAN;
+        o = run_precond(j);
+        break;
+      case CQR_HOUSEHOLDER:
+        throw Fail{CQR_UNSUPPORTED, -1, "HouseholderQr (dense baseline) is outside the GPU path"};
+      default:
+        throw Fail{CQR_INVALID_ARGUMENT, -1, "unknown method"};
+    }
+    if (o.has_r && r_host) {
+      ck(cudaMemcpy2DAsync(r_host, sizeof(double) * ldr, o.r_dev, sizeof(double) * j.n, sizeof(double) * j.n, j.n,
+                           cudaMemcpyDeviceToHost, c->stream),
+         "R D2H");
+      ck(cudaStreamSynchronize(c->stream), "sync");
+    }
+  } catch (const Fail& e) {
+    st = e.code;
+    index = e.index;
+    c->err = e.msg;
+    cudaStreamSynchronize(c->stream);
+    cudaGetLastError();
+  }
+  fill_report(c, report, st == CQR_OK ? &o : nullptr, st, index, r_less, j.method, j.n, l);
+  return st;
+}
+
+}  // namespace
+
+// =============================== C ABI ===========================================
+extern "C" {
+
+int cqr_abi_version(void) { return CQR_ABI_VERSION; }
+
+void cqr_sketch_cfg_default(cqr_sketch_cfg* cfg) {
+  if (cfg) *cfg = default_cfg();
+}
+
+void cqr_options_default(cqr_options* opts) {
+  if (opts) *opts = default_opts();
+}
+
+int64_t cqr_resolved_size(const cqr_sketch_cfg* cfg, int64_t m, int64_t n) {
+  return resolved_size(cfg ? *cfg : default_cfg(), m, n);
+}
+
+int cqr_create(cqr_ctx** out, int device) {
+  if (!out) return CQR_INVALID_ARGUMENT;
+  *out = nullptr;
+  cqr_ctx* c = new cqr_ctx();
+  c->device = device;
+  const int st = guarded(c, [&] {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaMalloc(&c->status, sizeof(DevStatus)), "status");
+    ck(cudaMallocHost(&c->status_h, sizeof(DevStatus)), "status_h");
+    ck(cudaMallocHost(&c->scal_h, 8 * sizeof(double)), "scal_h");
+  });
+  if (st != CQR_OK) {
+    std::fprintf(stderr, "cqr_create: %s\n", c->err.c_str());
+    delete c;
+    return st;
+  }
+  *out = c;
+  return CQR_OK;
+}
+
+int cqr_destroy(cqr_ctx* c) {
+  if (!c) return CQR_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& b : c->bufs)
+    if (b.p) cudaFree(b.p);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->status) cudaFree(c->status);
+  if (c->status_h) cudaFreeHost(c->status_h);
+  if (c->scal_h) cudaFreeHost(c->scal_h);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return CQR_OK;
+}
+
+const char* cqr_last_error(const cqr_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int cqr_comm_id_size(void) { return (int)sizeof(ncclUniqueId); }
+
+int cqr_comm_make_id(void* id) {
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return CQR_NCCL_ERROR;
+  std::memcpy(id, &u, sizeof(u));
+  return CQR_OK;
+}
+
+int cqr_attach_comm(cqr_ctx* c, int rank, int world, const void* id) {
+  if (!c || world < 1 || rank < 0 || rank >= world) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (c->comm) {
+      ncclCommDestroy(c->comm);
+      c->comm = nullptr;
+    }
+    c->rank = rank;
+    c->world = world;
+    if (world > 1) {
+      ncclUniqueId u;
+      std::memcpy(&u, id, sizeof(u));
+      ckn(ncclCommInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
+    }
+  });
+}
+
+int cqr_stream_handle(cqr_ctx* c, void** stream) {
+  if (!c || !stream) return CQR_INVALID_ARGUMENT;
+  *stream = (void*)c->stream;
+  return CQR_OK;
+}
+
+int64_t cqr_launch_count(const cqr_ctx* c) { return c ? c->launches : 0; }
+
+int cqr_factor_dev(cqr_ctx* c, int method, const double* a, int64_t m_local, int64_t m_global, int64_t row0,
+                   int64_t n, int64_t lda, const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q,
+                   int64_t ldq, double* r, int64_t ldr, cqr_report* report) {
+  if (!c) return CQR_INVALID_ARGUMENT;
+  Job j{};
+  j.c = c;
+  j.method = method;
+  j.a = a;
+  j.m_local = m_local;
+  j.m_global = m_global;
+  j.row0 = row0;
+  j.n = (int)n;
+  j.lda = lda;
+  j.q = q;
+  j.ldq = ldq;
+  j.cfg = cfg ? *cfg : default_cfg();
+  j.opts = opts ? *opts : default_opts();
+  if (c->world <= 1 && (m_local != m_global || row0 != 0)) {
+    c->err = "sharded call without an attached communicator";
+    return CQR_INVALID_ARGUMENT;
+  }
+  return factor_dev_impl(c, j, r, ldr, report);
+}
+
+static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64_t n, int64_t lda,
+                       const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq, double* r,
+                       int64_t ldr, cqr_report* report, cqr_precond_fn fn, void* user) {
+  if (!c) return CQR_INVALID_ARGUMENT;
+  if (m < 1 || n < 1 || lda < n || ldq < n || (r && ldr < n)) {
+    c->err = "bad shape";
+    if (report) {
+      std::memset(report, 0, sizeof(*report));
+      report->status = CQR_INVALID_ARGUMENT;
+      report->index = -1;
+    }
+    return CQR_INVALID_ARGUMENT;
+  }
+  int st = guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* da = dbuf<double>(c, B_HA, (size_t)m * n);
+    double* dq = dbuf<double>(c, B_HQ, (size_t)m * n);
+    ck(cudaMemcpy2DAsync(da, sizeof(double) * n, a, sizeof(double) * lda, sizeof(double) * n, m,
+                         cudaMemcpyHostToDevice, c->stream),
+       "A H2D");
+    Job j{};
+    j.c = c;
+    j.method = method;
+    j.a = da;
+    j.m_local = m;
+    j.m_global = m;
+    j.row0 = 0;
+    j.n = (int)n;
+    j.lda = n;
+    j.q = dq;
+    j.ldq = n;
+    j.cfg = cfg ? *cfg : default_cfg();
+    j.opts = opts ? *opts : default_opts();
+    j.precond = fn;
+    j.user = user;
+    const int s = factor_dev_impl(c, j, r, ldr, report);
+    if (s != CQR_OK) throw Fail{s, report ? report->index : -1, c->err};
+    ck(cudaMemcpy2DAsync(q, sizeof(double) * ldq, dq, sizeof(double) * n, sizeof(double) * n, m,
+                         cudaMemcpyDeviceToHost, c->stream),
+       "Q D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+  return st;
+}
+
+int cqr_factor(cqr_ctx* c, int method, const double* a, int64_t m, int64_t n, int64_t lda,
+               const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq, double* r, int64_t ldr,
+               cqr_report* report) {
+  return factor_host(c, method, a, m, n, lda, cfg, opts, q, ldq, r, ldr, report, nullptr, nullptr);
+}
+
+int cqr_precond_factor(cqr_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, cqr_precond_fn precond,
+                       void* user, const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq,
+                       double* r, int64_t ldr, cqr_report* report) {
+  if (!precond) return CQR_INVALID_ARGUMENT;
+  return factor_host(c, CQR_RQR, a, m, n, lda, cfg, opts, q, ldq, r, ldr, report, precond, user);
+}
+
+// ---- kernel-level entry points -------------------------------------------------------
+int cqr_gram_dev(cqr_ctx* c, const double* x, int64_t m, int64_t n, int64_t ldx, double* g) {
+  if (!c || m < n || n < 1 || ldx < n || n > 512) return CQR_INVALID_ARGUMENT;  // kernels.hpp:65
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    reset_status(c);
+    gram_dev(c, x, m, (int)n, ldx, g);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_gram(cqr_ctx* c, const double* x, int64_t m, int64_t n, int64_t ldx, double* g) {
+  if (!c || m < n || n < 1 || ldx < n || n > 512) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* dx = dbuf<double>(c, B_HA, (size_t)m * n);
+    double* dg = dbuf<double>(c, B_G, (size_t)n * n);
+    ck(cudaMemcpy2DAsync(dx, sizeof(double) * n, x, sizeof(double) * ldx, sizeof(double) * n, m,
+                         cudaMemcpyHostToDevice, c->stream),
+       "X H2D");
+    reset_status(c);
+    gram_dev(c, dx, m, (int)n, n, dg);
+    ck(cudaMemcpyAsync(g, dg, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->stream), "G D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_cholesky_upper(cqr_ctx* c, const double* g, int64_t n, double* r, int64_t* pivot) {
+  if (!c || n < 1 || n > 4096) return CQR_INVALID_ARGUMENT;
+  if (pivot) *pivot = -1;
+  long long idx = -1;
+  int st = guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* dg = dbuf<double>(c, B_G, (size_t)n * n);
+    double* dr = dbuf<double>(c, B_RH, (size_t)n * n);
+    double* work = dbuf<double>(c, B_WORK, (size_t)n * n);
+    ck(cudaMemcpyAsync(dg, g, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "G H2D");
+    reset_status(c);
+    LAUNCH(c, cqr::launch_cholesky(dg, (int)n, dr, work, 0, 0.0, 0.0, nullptr, c->status, c->stream));
+    DevStatus s = read_status(c);
+    if (s.code) {
+      idx = s.index;
+      throw Fail{s.code, s.index, "cholesky breakdown"};
+    }
+    ck(cudaMemcpy(r, dr, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "R D2H");
+  });
+  if (pivot) *pivot = idx;
+  return st;
+}
+
+int cqr_trisolve_inplace_dev(cqr_ctx* c, double* x, int64_t m, int64_t n, int64_t ldx, const double* r_dev,
+                             int64_t* index) {
+  if (!c || n < 1 || n > 512 || ldx < n || m < 0) return CQR_INVALID_ARGUMENT;
+  if (index) *index = -1;
+  long long idx = -1;
+  int st = guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* pack = dbuf<double>(c, B_PACK1, cqr::trisolve_pack_doubles((int)n));
+    reset_status(c);
+    LAUNCH(c, cqr::launch_pack_r(r_dev, (int)n, (int)n, pack, 0, c->status, c->stream));
+    trisolve_dev(c, x, ldx, x, ldx, m, (int)n, pack, nullptr);
+    DevStatus s = read_status(c);
+    if (s.code) {
+      idx = s.index;
+      throw Fail{s.code, s.index, "singular triangular factor"};
+    }
+  });
+  if (index) *index = idx;
+  return st;
+}
+
+int cqr_trisolve_inplace(cqr_ctx* c, double* x, int64_t m, int64_t n, int64_t ldx, const double* r,
+                         int64_t* index) {
+  if (!c || n < 1 || n > 512 || ldx < n || m < 0) return CQR_INVALID_ARGUMENT;
+  if (index) *index = -1;
+  for (int64_t j = 0; j < n; ++j)  // kernels.hpp:106-107: checked before X is touched
+    if (r[j * n + j] == 0.0) {
+      if (index) *index = j;
+      c->err = "singular triangular factor";
+      return CQR_SINGULAR_TRIANGULAR;
+    }
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* dx = dbuf<double>(c, B_HA, (size_t)std::max<int64_t>(m, 1) * n);
+    double* dr = dbuf<double>(c, B_RT, (size_t)n * n);
+    double* pack = dbuf<double>(c, B_PACK1, cqr::trisolve_pack_doubles((int)n));
+    ck(cudaMemcpyAsync(dr, r, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "R H2D");
+    if (m > 0)
+      ck(cudaMemcpy2DAsync(dx, sizeof(double) * n, x, sizeof(double) * ldx, sizeof(double) * n, m,
+                           cudaMemcpyHostToDevice, c->stream),
+         "X H2D");
+    reset_status(c);
+    LAUNCH(c, cqr::launch_pack_r(dr, (int)n, (int)n, pack, 0, c->status, c->stream));
+    trisolve_dev(c, dx, n, dx, n, m, (int)n, pack, nullptr);
+    DevStatus s = read_status(c);
+    if (s.code) throw Fail{s.code, s.index, "singular triangular factor"};
+    if (m > 0)
+      ck(cudaMemcpy2DAsync(x, sizeof(double) * ldx, dx, sizeof(double) * n, sizeof(double) * n, m,
+                           cudaMemcpyDeviceToHost, c->stream),
+         "X D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+static int small_factor(cqr_ctx* c, const double* a1, int64_t l, int64_t n, double* out, int64_t* index, bool lu) {
+  if (!c || n < 1 || l < n || n > 512) return CQR_INVALID_ARGUMENT;  // kernels.hpp:176, 218
+  if (index) *index = -1;
+  long long idx = -1;
+  int st = guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* da = dbuf<double>(c, B_A1, (size_t)l * n);
+    double* dr = dbuf<double>(c, B_RT, (size_t)n * n);
+    double* work = dbuf<double>(c, B_WORK, (size_t)l * n);
+    ck(cudaMemcpyAsync(da, a1, sizeof(double) * l * n, cudaMemcpyHostToDevice, c->stream), "A1 H2D");
+    reset_status(c);
+    if (lu)
+      LAUNCH(c, cqr::launch_lu_u(da, (int)l, (int)n, dr, work, c->status, c->stream));
+    else
+      LAUNCH(c, cqr::launch_qr_r(da, (int)l, (int)n, dr, work, c->status, c->stream));
+    DevStatus s = read_status(c);
+    if (s.code) {
+      idx = s.index;
+      throw Fail{s.code, s.index, "singular triangular factor"};
+    }
+    ck(cudaMemcpy(out, dr, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "R D2H");
+  });
+  if (index) *index = idx;
+  return st;
+}
+
+int cqr_qr_r_factor(cqr_ctx* c, const double* a1, int64_t l, int64_t n, double* r) {
+  return small_factor(c, a1, l, n, r, nullptr, false);
+}
+
+int cqr_lu_u_factor(cqr_ctx* c, const double* a1, int64_t l, int64_t n, double* u, int64_t* index) {
+  return small_factor(c, a1, l, n, u, index, true);
+}
+
+int cqr_sketch_gaussian_dev(cqr_ctx* c, const double* a, int64_t m_local, int64_t m_global, int64_t row0, int64_t n,
+                            int64_t lda, int64_t l, uint64_t seed, double* a1_dev) {
+  if (!c || n < 1 || n > 512 || l < 1 || lda < n || m_local < 0 || row0 + m_local > m_global)
+    return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    reset_status(c);
+    cqr::SketchPlan sp = cqr::sketch_plan(m_local, (int)n, (int)l, c->num_sms);
+    double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
+    if (m_local > 0) {
+      LAUNCH(c, cqr::launch_sketch_gaussian(sp, a, lda, m_global, row0, seed, part, vec_ok(a, lda, (int)n) ? 1 : 0,
+                                            c->status, c->stream));
+      LAUNCH(c, cqr::launch_sketch_reduce(sp, part, a1_dev, c->status, c->stream));
+    } else {
+      ck(cudaMemsetAsync(a1_dev, 0, sizeof(double) * l * n, c->stream), "memset");
+    }
+    allreduce(c, a1_dev, (size_t)l * n);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_sketch_gaussian(cqr_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, int64_t l, uint64_t seed,
+                        double* a1) {
+  if (!c || n < 1 || n > 512 || l < 1 || lda < n || m < 1) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* da = dbuf<double>(c, B_HA, (size_t)m * n);
+    double* d1 = dbuf<double>(c, B_A1, (size_t)l * n);
+    ck(cudaMemcpy2DAsync(da, sizeof(double) * n, a, sizeof(double) * lda, sizeof(double) * n, m,
+                         cudaMemcpyHostToDevice, c->stream),
+       "A H2D");
+    reset_status(c);
+    cqr::SketchPlan sp = cqr::sketch_plan(m, (int)n, (int)l, c->num_sms);
+    double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
+    LAUNCH(c, cqr::launch_sketch_gaussian(sp, da, n, m, 0, seed, part, vec_ok(da, n, (int)n) ? 1 : 0, c->status,
+                                          c->stream));
+    LAUNCH(c, cqr::launch_sketch_reduce(sp, part, d1, c->status, c->stream));
+    ck(cudaMemcpyAsync(a1, d1, sizeof(double) * l * n, cudaMemcpyDeviceToHost, c->stream), "A1 D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_sample_rows_uniform(cqr_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, int64_t l, uint64_t seed,
+                            int without_replacement, double* a1, int64_t* idx) {
+  if (!c || n < 1 || l < 1 || lda < n || m < 1) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* da = dbuf<double>(c, B_HA, (size_t)m * n);
+    double* d1 = dbuf<double>(c, B_A1, (size_t)l * n);
+    long long* didx = dbuf<long long>(c, B_IDX, (size_t)l);
+    long long* dio = dbuf<long long>(c, B_X, (size_t)l);
+    ck(cudaMemcpy2DAsync(da, sizeof(double) * n, a, sizeof(double) * lda, sizeof(double) * n, m,
+                         cudaMemcpyHostToDevice, c->stream),
+       "A H2D");
+    const long long* in = nullptr;
+    std::vector<long long> h;
+    if (without_replacement) {
+      require(l <= m, "without replacement needs l <= m");
+      std::unordered_set<long long> seen;
+      uint64_t pos = 0;
+      while ((long long)h.size() < l) {
+        const long long i = (long long)(unit_at(seed, pos++) * (double)m);
+        if (seen.insert(i).second) h.push_back(i);
+      }
+      ck(cudaMemcpyAsync(didx, h.data(), sizeof(long long) * l, cudaMemcpyHostToDevice, c->stream), "idx H2D");
+      in = didx;
+    }
+    reset_status(c);
+    LAUNCH(c, cqr::launch_gather_rows(da, n, m, m, 0, (int)n, (int)l, seed, in, d1, dio, c->status, c->stream));
+    ck(cudaMemcpyAsync(a1, d1, sizeof(double) * l * n, cudaMemcpyDeviceToHost, c->stream), "A1 D2H");
+    if (idx) ck(cudaMemcpyAsync(idx, dio, sizeof(long long) * l, cudaMemcpyDeviceToHost, c->stream), "idx D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_rng_bits(cqr_ctx* c, uint64_t seed, uint64_t k0, int64_t count, uint64_t* out) {
+  if (!c || count < 0) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    uint64_t* d = dbuf<uint64_t>(c, B_X, (size_t)std::max<int64_t>(count, 1));
+    LAUNCH(c, cqr::launch_rng_bits(seed, k0, count, d, c->stream));
+    ck(cudaMemcpyAsync(out, d, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_rng_gaussian(cqr_ctx* c, uint64_t seed, uint64_t k0, int64_t count, double* out) {
+  if (!c || count < 0) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* d = dbuf<double>(c, B_X, (size_t)std::max<int64_t>(count, 1));
+    LAUNCH(c, cqr::launch_rng_gaussian(seed, k0, count, d, c->stream));
+    ck(cudaMemcpyAsync(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_orthogonality_error_dev(cqr_ctx* c, const double* q, int64_t m, int64_t n, int64_t ldq, double* out) {
+  if (!c || m < n || n < 1 || n > 512) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    reset_status(c);
+    double* g = dbuf<double>(c, B_DIAG, (size_t)n * n + 2);
+    gram_dev(c, q, m, (int)n, ldq, g);
+    double* o = g + (size_t)n * n;
+    LAUNCH(c, cqr::launch_orth_from_gram(g, (int)n, o, c->stream));
+    ck(cudaMemcpyAsync(c->scal_h, o, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *out = c->scal_h[0];
+  });
+}
+
+int cqr_residual_error_dev(cqr_ctx* c, const double* a, int64_t lda, const double* q, int64_t ldq,
+                           const double* r_host, int64_t m, int64_t n, double* out) {
+  if (!c || m < 1 || n < 1) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const int nb = c->num_sms * 4;
+    double* dr = dbuf<double>(c, B_DIAG, (size_t)n * n + 2 * nb + 2);
+    double* part = dr + (size_t)n * n;
+    double* o = part + 2 * nb;
+    ck(cudaMemcpyAsync(dr, r_host, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "R H2D");
+    LAUNCH(c, cqr::launch_residual(a, lda, q, ldq, dr, m, (int)n, part, nb, o, c->stream));
+    ++c->launches;
+    if (c->world > 1) allreduce(c, o, 2);
+    ck(cudaMemcpyAsync(c->scal_h, o, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *out = std::sqrt(c->scal_h[0]) / std::sqrt(c->scal_h[1]);
+  });
+}
+
+int64_t cqr_block_offset(int64_t m, int p, int b) {  // parexec.cpp:13-15
+  if (b <= 0) return 0;
+  if (b >= p) return m;
+  return (static_cast<int64_t>(b) * m + p - 1) / p;
+}
+
+int cqr_comm_model(int method, int p, int64_t n, int64_t l, int* rounds_min, int* rounds_max, double* volume_min,
+                   double* volume_max) {  // parexec.cpp:44-62
+  const double pn2 = (double)p * (double)n * (double)n;
+  const double nl = (double)n * (double)l;
+  int a = 0, b = 0;
+  double x = 0, y = 0;
+  switch (method) {
+    case CQR_CHOLQR: a = b = 2; x = y = pn2; break;
+    case CQR_CHOLQR2: a = b = 4; x = y = 2 * pn2; break;
+    case CQR_SCHOLQR3: a = b = 6; x = y = 3 * pn2; break;
+    case CQR_RLU:
+    case CQR_RQR:
+    case CQR_RQR_GAUSSIAN: a = 3; b = 4; x = 1.5 * pn2; y = 1.5 * pn2 + nl; break;
+    case CQR_HOUSEHOLDER: break;
+    default: return CQR_INVALID_ARGUMENT;
+  }
+  if (rounds_min) *rounds_min = a;
+  if (rounds_max) *rounds_max = b;
+  if (volume_min) *volume_min = x;
+  if (volume_max) *volume_max = y;
+  return CQR_OK;
+}
+
+}  // extern "C"

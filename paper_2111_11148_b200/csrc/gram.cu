@@ -1,0 +1,239 @@
+// gram.cu — G = X^T X over fixed 1024-row leaves combined by the pairwise tree
+// (kernels.hpp:17-71, engine.cpp:24-39).
+//
+// Per leaf, every upper element is an fma chain over the leaf's rows in
+// ascending order from +0 (the oracle's pinned order). One CTA owns a leaf (or
+// a part of its output when n is large); each warp owns up to MAXT 16x16
+// macro tiles of the upper triangle and marches over the leaf's rows with
+// DMMA m8n8k4 (k = 4 rows per step; DMMA's internal order is the sequential
+// chain), so each leaf partial is bit-identical to the oracle's. Rows are
+// streamed through a cp.async double buffer. The leaf partials are then
+// combined per element with the streaming form of the pairwise tree
+// (binary counter + right fold, proven equal to the level-by-level tree in
+// tests/test_oracle.py::test_gram_tree_equals_stack_fold) and mirrored.
+//
+// HBM bytes per row: 8n; flops: n(n+1) per row (upper triangle incl. diagonal).
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cqr {
+
+namespace {
+
+constexpr int kLeafRows = 1024;  // kernels.hpp:20
+constexpr int kWpc = 8;
+
+int gram_np(int n) {
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  if (n <= 64) return 64;
+  if (n <= 128) return 128;
+  if (n <= 256) return 256;
+  return 512;
+}
+
+template <int NP, int MAXT, int CH>
+__global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __restrict__ x, long long ldx,
+                                                               long long m, int n, int parts,
+                                                               const int32_t* __restrict__ tiles,
+                                                               double* __restrict__ partial, int vec16,
+                                                               const DevStatus* st) {
+  constexpr int LDX = NP + 4;
+  extern __shared__ __align__(16) double smem[];
+  if (failed(st)) return;
+  const int leaf = blockIdx.x / parts, part = blockIdx.x - (blockIdx.x / parts) * parts;
+  const long long r0 = (long long)leaf * kLeafRows;
+  const int rows = (int)min((long long)kLeafRows, m - r0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, gr = lane >> 2;
+  int mt[MAXT];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) mt[t] = tiles[(part * kWpc + warp) * MAXT + t];
+  double acc[MAXT][4][2];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+
+  const double* xg = x + r0 * ldx;
+  const int nch = (rows + CH - 1) / CH;
+  double* buf[2] = {smem, smem + CH * LDX};
+  stage_rows(buf[0], LDX, xg, ldx, min(CH, rows), CH, n, NP, tid, kWpc * 32, vec16 != 0);
+  cp_async_commit();
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      const int rr = min(CH, rows - (c + 1) * CH);
+      stage_rows(buf[(c + 1) & 1], LDX, xg + (long long)(c + 1) * CH * ldx, ldx, rr, CH, n, NP, tid, kWpc * 32,
+                 vec16 != 0);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* b = buf[c & 1];
+#pragma unroll 2
+    for (int k4 = 0; k4 < CH / 4; ++k4) {
+      const double* xr = b + (4 * k4 + q) * LDX + gr;
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        if (mt[t] < 0) continue;
+        const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
+        const double a0 = xr[16 * I2], a1 = xr[16 * I2 + 8];
+        const double b0 = xr[16 * J2], b1 = xr[16 * J2 + 8];
+        dmma(acc[t][0][0], acc[t][0][1], a0, b0);
+        dmma(acc[t][1][0], acc[t][1][1], a0, b1);
+        if (I2 != J2) dmma(acc[t][2][0], acc[t][2][1], a1, b0);
+        dmma(acc[t][3][0], acc[t][3][1], a1, b1);
+      }
+    }
+    __syncthreads();
+  }
+  double* out = partial + (long long)leaf * NP * NP;
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    if (mt[t] < 0) continue;
+    const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int si = u >> 1, sj = u & 1;
+      if (I2 == J2 && si == 1 && sj == 0) continue;
+      const int i = 16 * I2 + 8 * si + gr, j = 16 * J2 + 8 * sj + 2 * q;
+      *reinterpret_cast<double2*>(out + i * NP + j) = make_double2(acc[t][u][0], acc[t][u][1]);
+    }
+  }
+}
+
+// Streaming pairwise tree: after pushing leaf i, merge (top-1) + top once per
+// trailing zero of (i+1); finally fold the stack right to left.
+__global__ void gram_combine_kernel(const double* __restrict__ partial, int leaves, int np, int n,
+                                    double* __restrict__ g, int mirror, const DevStatus* st) {
+  if (failed(st)) return;
+  const int i = blockIdx.y;
+  const int j = i + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double* p = partial + (long long)i * np + j;
+  const long long stride = (long long)np * np;
+  double stk[40];
+  int top = 0;
+  int leaf = 0;
+  for (; leaf + 8 <= leaves; leaf += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (long long)(leaf + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      double cur = v[u];
+      unsigned t = (unsigned)(leaf + u + 1);
+      while ((t & 1u) == 0u) {
+        cur = stk[--top] + cur;
+        t >>= 1;
+      }
+      stk[top++] = cur;
+    }
+  }
+  for (; leaf < leaves; ++leaf) {
+    double cur = __ldg(p + (long long)leaf * stride);
+    unsigned t = (unsigned)(leaf + 1);
+    while ((t & 1u) == 0u) {
+      cur = stk[--top] + cur;
+      t >>= 1;
+    }
+    stk[top++] = cur;
+  }
+  double acc = stk[top - 1];
+  for (int k = top - 2; k >= 0; --k) acc = stk[k] + acc;
+  g[(long long)i * n + j] = acc;
+  if (mirror) g[(long long)j * n + i] = acc;
+}
+
+__global__ void mirror_kernel(double* g, int n, const DevStatus* st) {
+  if (failed(st)) return;
+  const int i = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < i) g[(long long)i * n + j] = g[(long long)j * n + i];
+}
+
+template <int NP, int MAXT, int CH>
+cudaError_t launch_leaves_t(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
+                            double* partial, int vec16, const DevStatus* st, cudaStream_t s) {
+  const size_t smem = (size_t)2 * CH * (NP + 4) * sizeof(double);
+  auto k = gram_leaf_kernel<NP, MAXT, CH>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)(p.leaves * p.parts), kWpc * 32, smem, s>>>(x, ldx, p.m, p.n, p.parts, tiles, partial, vec16, st);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+GramPlan gram_plan(long long m, int n) {
+  GramPlan p;
+  p.n = n;
+  p.m = m;
+  p.np = gram_np(n);
+  p.leaves = (int)((m + kLeafRows - 1) / kLeafRows);
+  p.wpc = kWpc;
+  const int nm = p.np / 16;
+  const int macros = nm * (nm + 1) / 2;
+  const int cap = 9;
+  p.parts = (macros + kWpc * cap - 1) / (kWpc * cap);
+  int maxt = (macros + kWpc * p.parts - 1) / (kWpc * p.parts);
+  p.maxt = maxt <= 1 ? 1 : maxt <= 2 ? 2 : maxt <= 5 ? 5 : 9;
+  p.ch = p.np <= 128 ? 32 : 16;
+  p.partial_doubles = (size_t)p.leaves * p.np * p.np;
+  p.tiles_bytes = (size_t)p.parts * kWpc * p.maxt * sizeof(int32_t);
+  return p;
+}
+
+void gram_tiles(const GramPlan& p, int32_t* out) {
+  const int nm = p.np / 16;
+  const int slots = p.parts * kWpc;
+  for (int e = 0; e < slots * p.maxt; ++e) out[e] = -1;
+  // round-robin the upper macro tiles over (part, warp) slots, filling each slot's list
+  int idx = 0;
+  for (int I = 0; I < nm; ++I)
+    for (int J = I; J < nm; ++J) {
+      const int slot = idx % slots, t = idx / slots;
+      out[slot * p.maxt + t] = I | (J << 16);
+      ++idx;
+    }
+}
+
+cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
+                               double* partial, int vec16, const DevStatus* st, cudaStream_t s) {
+#define CQR_GRAM_CASE(NP_, CH_)                                                                     \
+  case NP_:                                                                                          \
+    switch (p.maxt) {                                                                                \
+      case 1: return launch_leaves_t<NP_, 1, CH_>(p, x, ldx, tiles, partial, vec16, st, s);         \
+      case 2: return launch_leaves_t<NP_, 2, CH_>(p, x, ldx, tiles, partial, vec16, st, s);         \
+      case 5: return launch_leaves_t<NP_, 5, CH_>(p, x, ldx, tiles, partial, vec16, st, s);         \
+      default: return launch_leaves_t<NP_, 9, CH_>(p, x, ldx, tiles, partial, vec16, st, s);        \
+    }
+  switch (p.np) {
+    CQR_GRAM_CASE(16, 32)
+    CQR_GRAM_CASE(32, 32)
+    CQR_GRAM_CASE(64, 32)
+    CQR_GRAM_CASE(128, 32)
+    CQR_GRAM_CASE(256, 16)
+    CQR_GRAM_CASE(512, 16)
+  }
+#undef CQR_GRAM_CASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gram_combine(const GramPlan& p, const double* partial, double* g, int mirror,
+                                const DevStatus* st, cudaStream_t s) {
+  dim3 grid((unsigned)((p.n + 127) / 128), (unsigned)p.n);
+  gram_combine_kernel<<<grid, 128, 0, s>>>(partial, p.leaves, p.np, p.n, g, mirror, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mirror_upper(double* g, int n, const DevStatus* st, cudaStream_t s) {
+  dim3 grid((unsigned)((n + 127) / 128), (unsigned)n);
+  mirror_kernel<<<grid, 128, 0, s>>>(g, n, st);
+  return cudaGetLastError();
+}
+
+}  // namespace cqr

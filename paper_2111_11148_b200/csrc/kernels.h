@@ -1,0 +1,100 @@
+// kernels.h — internal launch interface between the host engine and the
+// sm_100a kernels (not part of the C-ABI; see include/cqr.h for that).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cqr {
+
+struct DevStatus;
+
+// ---- trisolve.cu --------------------------------------------------------------
+int trisolve_np(int n);                 // padded width bucket of the trisolve kernel
+size_t trisolve_pack_doubles(int n);    // workspace for the packed R
+cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int degenerate, DevStatus* st,
+                          cudaStream_t s);
+struct TrisolveArgs {
+  const double* in;
+  long long ldi;
+  double* out;  // may alias in
+  long long ldo;
+  long long m;
+  int n;
+  const double* pack;  // from launch_pack_r
+  const double* bpack;
+  const double* dpack;
+  const double* sgn;  // optional column signs applied to the stored result (normalize_sign)
+  int vec16;
+  int num_sms;
+  const DevStatus* status;
+};
+cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s);
+
+// ---- gram.cu ---------------------------------------------------------------------
+struct GramPlan {
+  int n = 0, np = 0, leaves = 0, parts = 0, maxt = 0, wpc = 0, ch = 0;
+  long long m = 0;
+  size_t partial_doubles = 0;  // leaves * np * np
+  size_t tiles_bytes = 0;
+};
+GramPlan gram_plan(long long m, int n);
+// Host-side tile table for the plan (parts * wpc * maxt entries, packed I2 | J2<<16, -1 = none).
+void gram_tiles(const GramPlan& p, int32_t* out);
+// Leaf partials (1024-row leaves, kernels.hpp:20-38) -> partial[leaf][np*np] (upper tiles).
+cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles_dev,
+                               double* partial, int vec16, const DevStatus* st, cudaStream_t s);
+// Pairwise tree over leaves (kernels.hpp:42-57, streaming form) -> g upper (ld = n);
+// mirror=1 also writes the lower triangle (kernels.hpp:69).
+cudaError_t launch_gram_combine(const GramPlan& p, const double* partial, double* g, int mirror,
+                                const DevStatus* st, cudaStream_t s);
+cudaError_t launch_mirror_upper(double* g, int n, const DevStatus* st, cudaStream_t s);
+
+// ---- sketch.cu ---------------------------------------------------------------------
+struct SketchPlan {
+  int n = 0, np = 0, l = 0, lp = 0, s_tiles = 0, kchunks = 0;
+  long long m_local = 0, rows_per_chunk = 0;
+  size_t partial_doubles = 0;
+};
+SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms);
+cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,
+                                   long long row0, uint64_t seed, double* partial, int vec16,
+                                   const DevStatus* st, cudaStream_t s);
+// a1[i][c] = sum over k-chunks (ascending) of partial -> l x n (ld = n)
+cudaError_t launch_sketch_reduce(const SketchPlan& p, const double* partial, double* a1, const DevStatus* st,
+                                 cudaStream_t s);
+// Uniform row extraction (sketch.cpp:45-55). idx_host == nullptr: indices
+// drawn on the device as floor(unit_at(seed, k) * m_global) (rng.hpp:69-71);
+// rows outside [row0, row0+m_local) are written as zeros (the caller sums
+// the shards). idx_out (device, optional) receives the indices.
+cudaError_t launch_gather_rows(const double* a, long long lda, long long m_local, long long m_global,
+                               long long row0, int n, int l, uint64_t seed, const long long* idx_dev,
+                               double* a1, long long* idx_out, const DevStatus* st, cudaStream_t s);
+cudaError_t launch_rng_bits(uint64_t seed, uint64_t k0, long long count, uint64_t* out, cudaStream_t s);
+cudaError_t launch_rng_gaussian(uint64_t seed, uint64_t k0, long long count, double* out, cudaStream_t s);
+
+// ---- small.cu (single-CTA factorizations, all on device) ------------------------------
+// kernels.hpp:76-90 (+ G += shift*I, engine.cpp:85; theory shift from trace(G)).
+// shift_mode 0 none, 1 fixed (value), 2 theory (coef * trace(G)); shift_out optional.
+size_t small_work_doubles(int rows, int n);
+cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int shift_mode, double shift_value,
+                            double theory_coef, double* shift_out, DevStatus* st, cudaStream_t s);
+// kernels.hpp:211-257 (U only; status SingularTriangular(j) on a zero pivot).
+cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s);
+// kernels.hpp:165-184 (sign-normalised R of a Householder QR).
+cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work, DevStatus* st, cudaStream_t s);
+// engine.cpp:103-107 dense L*R with the strict lower part zeroed.
+cudaError_t launch_triangular_product(const double* left, const double* right, int n, double* out,
+                                      const DevStatus* st, cudaStream_t s);
+// engine.cpp:109-116 on R (rows with a negative diagonal flipped); sgn[i] = +-1
+// is then applied to Q's columns by the final trisolve.
+cudaError_t launch_normalize_sign(double* r, int n, double* sgn, const DevStatus* st, cudaStream_t s);
+
+// ---- diag.cu ------------------------------------------------------------------------------
+// sum over rows of ||a_i - q_i R||^2 and ||a_i||^2 into out[0], out[1] (fixed order).
+cudaError_t launch_residual(const double* a, long long lda, const double* q, long long ldq, const double* r,
+                            long long m, int n, double* partial, int nblocks, double* out, cudaStream_t s);
+cudaError_t launch_orth_from_gram(const double* g, int n, double* out, cudaStream_t s);
+
+}  // namespace cqr

@@ -1,0 +1,277 @@
+// sketch.cu — Gaussian sketch A1 = Omega A with Omega generated in-kernel
+// (sketch.cpp:94-116), uniform row extraction (sketch.cpp:27-55) and the
+// device RNG fills used by the parity tests (rng.hpp:22-92).
+//
+// Omega(i, j) = gaussian_at(seed, i*m + j) with the GLOBAL row index j, so a
+// row-sharded A (one GPU per block, parexec.cpp:9-18) sketches to partials that
+// sum to the single-GPU sketch. Omega never touches HBM: each CTA owns an
+// (ST rows of Omega) x (a contiguous range of A's rows) block, generates the
+// Omega tile for each 32-row step into shared memory exactly once (both
+// Box-Muller outputs of a pair are used, rng.hpp:47-55), and multiplies it
+// with the staged A rows on DMMA m8n8k4. Per-CTA partials are summed in a
+// fixed k-chunk order by a second kernel (deterministic run to run).
+//
+// Algorithmic work: 2*l*m*n flops + l*m Gaussian draws; HBM: 8*m*n bytes of A
+// (each A row is read by l/ST CTAs that run together, the repeats hit L2).
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cqr {
+
+namespace {
+
+constexpr int kST = 64;  // Omega rows per CTA
+constexpr int kKS = 32;  // A rows per step
+constexpr int kThreads = 256;
+
+int sketch_np(int n) {
+  if (n <= 8) return 8;
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  if (n <= 64) return 64;
+  if (n <= 128) return 128;
+  if (n <= 256) return 256;
+  return 512;
+}
+
+// Generate Omega[s0 .. s0+ST) x [kb .. kb+KS) (kb = global row index) into
+// sOm (row stride KS+4). Rows of Omega at or beyond l are zero.
+__device__ __forceinline__ void gen_omega(double* sOm, int s0, int l, long long m_global, long long kb,
+                                          uint64_t seed, int tid) {
+  constexpr int PPR = kKS / 2 + 1;  // pair slots per Omega row
+  for (int e = tid; e < kST * PPR; e += kThreads) {
+    const int i = e / PPR, pp = e - i * PPR;
+    double* row = sOm + i * (kKS + 4);
+    if (s0 + i >= l) {
+      if (pp < kKS / 2) {
+        row[2 * pp] = 0.0;
+        row[2 * pp + 1] = 0.0;
+      }
+      continue;
+    }
+    const unsigned long long c_lo = (unsigned long long)(s0 + i) * (unsigned long long)m_global + kb;
+    const unsigned long long p = (c_lo >> 1) + pp;
+    if (p > ((c_lo + kKS - 1) >> 1)) continue;
+    double ge, go;
+    gaussian_pair(seed, p, ge, go);
+    const long long ce = (long long)(2 * p - c_lo);
+    if (ce >= 0 && ce < kKS) row[ce] = ge;
+    if (ce + 1 >= 0 && ce + 1 < kKS) row[ce + 1] = go;
+  }
+}
+
+// NP = columns handled by one CTA (<= 128); wider A is split over gridDim.z
+// column parts of NP, each regenerating the same Omega tile.
+template <int NP>
+__global__ void __launch_bounds__(kThreads) sketch_kernel(const double* __restrict__ a, long long lda,
+                                                          long long m_local, long long m_global, long long row0,
+                                                          int n, int l, uint64_t seed, long long rows_per_chunk,
+                                                          double* __restrict__ partial, int lp, int np_total,
+                                                          int vec16, const DevStatus* st) {
+  constexpr int NT = NP / 8;
+  constexpr int WN = NT < 8 ? NT : 8;  // warps along n
+  constexpr int WM = 8 / WN;           // warps along Omega rows
+  constexpr int MG = kST / 8 / WM;     // 8-row groups per warp
+  constexpr int NG = NT / WN;          // 8-col groups per warp
+  constexpr int LDA = NP + 4;
+  constexpr int LDO = kKS + 4;
+  extern __shared__ __align__(16) double smem[];
+  if (failed(st)) return;
+  double* sOm = smem;
+  double* sA[2] = {smem + kST * LDO, smem + kST * LDO + kKS * LDA};
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, gr = lane >> 2;
+  const int wm = warp / WN, wn = warp - (warp / WN) * WN;
+  const int s0 = blockIdx.x * kST;
+  const int col0 = blockIdx.z * NP;
+  a += col0;
+  n = min(NP, n - col0);
+  const long long k_begin = (long long)blockIdx.y * rows_per_chunk;
+  const long long k_end = min(m_local, k_begin + rows_per_chunk);
+
+  double acc[MG][NG][2];
+#pragma unroll
+  for (int g = 0; g < MG; ++g)
+#pragma unroll
+    for (int h = 0; h < NG; ++h) acc[g][h][0] = acc[g][h][1] = 0.0;
+
+  const int nsteps = k_end > k_begin ? (int)((k_end - k_begin + kKS - 1) / kKS) : 0;
+  if (nsteps > 0) {
+    stage_rows(sA[0], LDA, a + k_begin * lda, lda, (int)min((long long)kKS, k_end - k_begin), kKS, n, NP, tid,
+               kThreads, vec16 != 0);
+    cp_async_commit();
+  }
+  for (int st_i = 0; st_i < nsteps; ++st_i) {
+    const long long kb = k_begin + (long long)st_i * kKS;
+    if (st_i + 1 < nsteps) {
+      const long long kn = kb + kKS;
+      stage_rows(sA[(st_i + 1) & 1], LDA, a + kn * lda, lda, (int)min((long long)kKS, k_end - kn), kKS, n, NP,
+                 tid, kThreads, vec16 != 0);
+      cp_async_commit();
+    }
+    gen_omega(sOm, s0, l, m_global, row0 + kb, seed, tid);
+    if (st_i + 1 < nsteps)
+      cp_async_wait<1>();
+    else
+      cp_async_wait<0>();
+    __syncthreads();
+    const double* A = sA[st_i & 1];
+    const double* O = sOm + (wm * MG * 8 + gr) * LDO + q;
+#pragma unroll 2
+    for (int k4 = 0; k4 < kKS / 4; ++k4) {
+      double af[MG], bf[NG];
+#pragma unroll
+      for (int g = 0; g < MG; ++g) af[g] = O[g * 8 * LDO + 4 * k4];
+#pragma unroll
+      for (int h = 0; h < NG; ++h) bf[h] = A[(4 * k4 + q) * LDA + (wn * NG + h) * 8 + gr];
+#pragma unroll
+      for (int g = 0; g < MG; ++g)
+#pragma unroll
+        for (int h = 0; h < NG; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
+    }
+    __syncthreads();
+  }
+  // partial[chunk][s0 + i][col0 + col], lp rows per chunk, np_total columns
+  double* out = partial + (long long)blockIdx.y * lp * np_total + col0;
+#pragma unroll
+  for (int g = 0; g < MG; ++g) {
+    const int i = s0 + (wm * MG + g) * 8 + gr;
+#pragma unroll
+    for (int h = 0; h < NG; ++h) {
+      const int j = (wn * NG + h) * 8 + 2 * q;
+      *reinterpret_cast<double2*>(out + (long long)i * np_total + j) = make_double2(acc[g][h][0], acc[g][h][1]);
+    }
+  }
+}
+
+__global__ void sketch_reduce_kernel(const double* __restrict__ partial, int kchunks, int lp, int np, int l,
+                                     int n, double* __restrict__ a1, const DevStatus* st) {
+  if (failed(st)) return;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)l * n) return;
+  const int i = (int)(e / n), c = (int)(e - (long long)i * n);
+  const double* p = partial + (long long)i * np + c;
+  const long long stride = (long long)lp * np;
+  double s = 0.0;
+  for (int k = 0; k < kchunks; ++k) s += __ldg(p + k * stride);
+  a1[e] = s;
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ a, long long lda, long long m_local,
+                                   long long m_global, long long row0, int n, int l, uint64_t seed,
+                                   const long long* __restrict__ idx_in, double* __restrict__ a1,
+                                   long long* __restrict__ idx_out, const DevStatus* st) {
+  if (failed(st)) return;
+  const int k = blockIdx.x;
+  long long idx;
+  if (idx_in) {
+    idx = idx_in[k];
+  } else {
+    const double u = (double)(bits_at(seed, (uint64_t)k) >> 11) * 0x1.0p-53;  // Stream(seed).next_index, rng.hpp:69-71
+    idx = (long long)(u * (double)m_global);
+  }
+  if (idx_out && threadIdx.x == 0) idx_out[k] = idx;
+  const long long loc = idx - row0;
+  const bool mine = loc >= 0 && loc < m_local;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) a1[(long long)k * n + c] = mine ? a[loc * lda + c] : 0.0;
+}
+
+__global__ void rng_bits_kernel(uint64_t seed, uint64_t k0, long long count, uint64_t* out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = bits_at(seed, k0 + (uint64_t)e);
+}
+
+__global__ void rng_gauss_kernel(uint64_t seed, uint64_t k0, long long count, double* out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count;
+       e += (long long)gridDim.x * blockDim.x) {
+    const uint64_t k = k0 + (uint64_t)e;
+    double ge, go;
+    gaussian_pair(seed, k >> 1, ge, go);
+    out[e] = (k & 1) ? go : ge;
+  }
+}
+
+template <int NP>
+cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
+                            uint64_t seed, double* partial, int vec16, const DevStatus* st, cudaStream_t s) {
+  const size_t smem = (size_t)(kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
+  auto k = sketch_kernel<NP>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)p.s_tiles, (unsigned)p.kchunks, (unsigned)(p.np / NP));
+  k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial, p.lp,
+                                 p.np, vec16, st);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms) {
+  SketchPlan p;
+  p.n = n;
+  p.l = l;
+  p.np = sketch_np(n);
+  p.m_local = m_local;
+  p.s_tiles = (l + kST - 1) / kST;
+  p.lp = p.s_tiles * kST;
+  // about 2 resident CTAs per SM over a few waves; chunks are multiples of KS rows
+  const long long target = (long long)num_sms * 4;
+  const int zparts = p.np > 128 ? p.np / 128 : 1;
+  long long kc = (target + (long long)p.s_tiles * zparts - 1) / ((long long)p.s_tiles * zparts);
+  const long long max_kc = (m_local + kKS - 1) / kKS;
+  if (kc > max_kc) kc = max_kc;
+  if (kc < 1) kc = 1;
+  long long rpc = (m_local + kc - 1) / kc;
+  rpc = (rpc + kKS - 1) / kKS * kKS;
+  if (rpc < kKS) rpc = kKS;
+  p.rows_per_chunk = rpc;
+  p.kchunks = (int)((m_local + rpc - 1) / rpc);
+  if (p.kchunks < 1) p.kchunks = 1;
+  p.partial_doubles = (size_t)p.kchunks * p.lp * p.np;
+  return p;
+}
+
+cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,
+                                   long long row0, uint64_t seed, double* partial, int vec16, const DevStatus* st,
+                                   cudaStream_t s) {
+  switch (p.np) {
+    case 8: return launch_sketch_t<8>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+    case 16: return launch_sketch_t<16>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+    case 32: return launch_sketch_t<32>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+    case 64: return launch_sketch_t<64>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+    case 128: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+    case 256:
+    case 512: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sketch_reduce(const SketchPlan& p, const double* partial, double* a1, const DevStatus* st,
+                                 cudaStream_t s) {
+  const long long total = (long long)p.l * p.n;
+  sketch_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(partial, p.kchunks, p.lp, p.np, p.l, p.n,
+                                                                       a1, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(const double* a, long long lda, long long m_local, long long m_global, long long row0,
+                               int n, int l, uint64_t seed, const long long* idx_dev, double* a1, long long* idx_out,
+                               const DevStatus* st, cudaStream_t s) {
+  gather_rows_kernel<<<(unsigned)l, 128, 0, s>>>(a, lda, m_local, m_global, row0, n, l, seed, idx_dev, a1, idx_out,
+                                                 st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rng_bits(uint64_t seed, uint64_t k0, long long count, uint64_t* out, cudaStream_t s) {
+  rng_bits_kernel<<<256, 256, 0, s>>>(seed, k0, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rng_gaussian(uint64_t seed, uint64_t k0, long long count, double* out, cudaStream_t s) {
+  rng_gauss_kernel<<<256, 256, 0, s>>>(seed, k0, count, out);
+  return cudaGetLastError();
+}
+
+}  // namespace cqr

@@ -1,0 +1,335 @@
+// small.cu — the small s x n and n x n factorizations, on device, one CTA each
+// (latency-bound: n <= 512 steps of O(n) parallel work). The working matrix
+// lives in shared memory when it fits (<= ~200 KB) and otherwise in an
+// L2-resident global workspace; the same kernel body serves both through a
+// generic pointer.
+//
+//  cholesky_kernel  kernels.hpp:76-90 (+ G += shift*I, engine.cpp:85): right-looking,
+//                   every element an fma chain in k order from g(i,j) (the
+//                   oracle's pinned order) -> bitwise equal to the oracle.
+//  lu_kernel        kernels.hpp:211-257: partial pivoting with the first maximum,
+//                   fma trailing update skipped for zero multipliers -> bitwise.
+//  qr_kernel        kernels.hpp:165-184: Householder (beta = -sign(c0)*norm),
+//                   sign-normalised R; reductions in a fixed tree order
+//                   (deterministic; tolerance parity with the oracle).
+//  triangular_product_kernel  engine.cpp:103-107 (fma chain over all k) -> bitwise.
+//  normalize_sign_kernel      engine.cpp:109-116 (R rows; Q columns via sgn).
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cqr {
+
+namespace {
+
+constexpr int kT = 1024;
+constexpr size_t kSmemCap = 200 * 1024;
+
+// Deterministic block sum (fixed xor tree in each warp, then warp 0 over the
+// warp sums in index order through the same tree). All threads get the result.
+__device__ double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double w = lane < nw ? scratch[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (lane == 0) scratch[32] = w;
+  }
+  __syncthreads();
+  return scratch[32];
+}
+
+__global__ void __launch_bounds__(kT) cholesky_kernel(const double* __restrict__ g, int n, double* __restrict__ r,
+                                                      double* work, int use_smem, int shift_mode, double shift_value,
+                                                      double theory_coef, double* shift_out, DevStatus* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double s_d;
+  __shared__ int s_bad;
+  if (failed(st)) return;
+  double* S = use_smem ? smem : work;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < n * n; e += nt) S[e] = g[e];
+  __syncthreads();
+  if (shift_mode != 0 && tid == 0) {
+    double sh = shift_value;
+    if (shift_mode == 2) {  // theory shift from trace(G) == ||A||_F^2 (cholqr.cpp:21-26)
+      double tr = 0.0;
+      for (int j = 0; j < n; ++j) tr += g[(long long)j * n + j];
+      sh = theory_coef * tr;
+    }
+    for (int j = 0; j < n; ++j) S[(long long)j * n + j] += sh;
+    if (shift_out) *shift_out = sh;
+  }
+  __syncthreads();
+  for (int i = 0; i < n; ++i) {
+    if (tid == 0) {
+      const double sii = S[(long long)i * n + i];
+      if (!(sii > 0.0)) {
+        s_bad = 1;
+        set_status(st, 1 /*CQR_CHOLESKY_BREAKDOWN*/, i);
+      } else {
+        s_bad = 0;
+        s_d = sqrt(sii);
+        S[(long long)i * n + i] = s_d;
+      }
+    }
+    __syncthreads();
+    if (s_bad) return;
+    const double d = s_d;
+    double* Si = S + (long long)i * n;
+    for (int j = i + 1 + tid; j < n; j += nt) Si[j] = Si[j] / d;
+    __syncthreads();
+    const int w = n - i - 1;
+    for (int e = tid; e < w * w; e += nt) {
+      const int a = i + 1 + e / w, b = i + 1 + e % w;
+      if (b >= a) S[(long long)a * n + b] = fma(-Si[a], Si[b], S[(long long)a * n + b]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e / n, j = e % n;
+    r[e] = j >= i ? S[e] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kT) lu_kernel(const double* __restrict__ a1, int l, int n, double* __restrict__ u,
+                                                double* work, int use_smem, DevStatus* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double wb[32];
+  __shared__ int wi[32];
+  __shared__ int s_piv;
+  if (failed(st)) return;
+  double* W = use_smem ? smem : work;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (long long e = tid; e < (long long)l * n; e += nt) W[e] = a1[e];
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    // first maximum of |W(i, j)| over i >= j (kernels.hpp:226-234)
+    double best = -1.0;
+    int idx = 0x7fffffff;
+    for (int i = j + tid; i < l; i += nt) {
+      const double v = fabs(W[(long long)i * n + j]);
+      if (v > best) {
+        best = v;
+        idx = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ob > best || (ob == best && oi < idx)) {
+        best = ob;
+        idx = oi;
+      }
+    }
+    if (lane == 0) {
+      wb[warp] = best;
+      wi[warp] = idx;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      best = lane < nw ? wb[lane] : -1.0;
+      idx = lane < nw ? wi[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ob > best || (ob == best && oi < idx)) {
+          best = ob;
+          idx = oi;
+        }
+      }
+      if (lane == 0) s_piv = idx;
+    }
+    __syncthreads();
+    const int piv = s_piv;
+    if (piv >= l || W[(long long)piv * n + j] == 0.0) {
+      if (tid == 0) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, j);
+      return;
+    }
+    if (piv != j) {
+      for (int c = tid; c < n; c += nt) {
+        const double t = W[(long long)j * n + c];
+        W[(long long)j * n + c] = W[(long long)piv * n + c];
+        W[(long long)piv * n + c] = t;
+      }
+      __syncthreads();
+    }
+    const double d = W[(long long)j * n + j];
+    for (int i = j + 1 + tid; i < l; i += nt) W[(long long)i * n + j] = W[(long long)i * n + j] / d;
+    __syncthreads();
+    const int w = n - j - 1;
+    if (w > 0) {
+      const double* pr = W + (long long)j * n;
+      for (long long e = tid; e < (long long)(l - j - 1) * w; e += nt) {
+        const int i = j + 1 + (int)(e / w), c = j + 1 + (int)(e % w);
+        const double mult = W[(long long)i * n + j];
+        if (mult != 0.0) W[(long long)i * n + c] = fma(-mult, pr[c], W[(long long)i * n + c]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e / n, c = e % n;
+    u[e] = c >= i ? W[e] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kT) qr_kernel(const double* __restrict__ a1, int l, int n, double* __restrict__ r,
+                                                double* work, int use_smem, DevStatus* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double scratch[33];
+  __shared__ double ts[512];
+  __shared__ double s_tau, s_beta, s_denom;
+  __shared__ int s_zero;
+  if (failed(st)) return;
+  double* W = use_smem ? smem : work;  // column-major l x n
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (long long e = tid; e < (long long)l * n; e += nt) {
+    const int i = (int)(e / n), c = (int)(e % n);
+    W[(long long)c * l + i] = a1[e];
+  }
+  __syncthreads();
+  const double tol = 2.2250738585072014e-308 * 2.2250738585072014e-308;  // (smallest normal)^2
+  for (int j = 0; j < n; ++j) {
+    double* col = W + (long long)j * l;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < l; i += nt) part = fma(col[i], col[i], part);
+    const double tail = block_sum(part, scratch);
+    if (tid == 0) {
+      const double c0 = col[j];
+      if (tail <= tol) {
+        s_zero = 1;
+        s_tau = 0.0;
+        s_beta = c0;
+        s_denom = 1.0;
+      } else {
+        s_zero = 0;
+        double beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        s_beta = beta;
+        s_denom = c0 - beta;
+        s_tau = (beta - c0) / beta;
+      }
+    }
+    __syncthreads();
+    const double denom = s_denom, tau = s_tau;
+    const int zero = s_zero;
+    for (int i = j + 1 + tid; i < l; i += nt) col[i] = zero ? 0.0 : col[i] / denom;
+    __syncthreads();
+    if (tid == 0) col[j] = s_beta;
+    if (tau != 0.0) {
+      for (int c = j + 1 + warp; c < n; c += nw) {
+        const double* cc = W + (long long)c * l;
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < l; i += 32) s = fma(col[i], cc[i], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) ts[c] = tau * (cc[j] + s);
+      }
+      __syncthreads();
+      const int w = n - j - 1, h = l - j;
+      for (long long e = tid; e < (long long)w * h; e += nt) {
+        const int c = j + 1 + (int)(e / h), i = j + (int)(e % h);
+        double* cc = W + (long long)c * l;
+        if (i == j)
+          cc[j] -= ts[c];
+        else
+          cc[i] = fma(-ts[c], col[i], cc[i]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e / n, c = e % n;
+    r[e] = c >= i ? W[(long long)c * l + i] : 0.0;
+  }
+  __syncthreads();
+  // normalize_r_sign (kernels.hpp:165-168)
+  for (int i = tid; i < n; i += nt)
+    if (r[(long long)i * n + i] < 0.0)
+      for (int c = i; c < n; ++c) r[(long long)i * n + c] = -r[(long long)i * n + c];
+}
+
+__global__ void triangular_product_kernel(const double* __restrict__ left, const double* __restrict__ right, int n,
+                                          double* __restrict__ out, const DevStatus* st) {
+  if (failed(st)) return;
+  const int i = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  if (j >= i) {
+    const double* li = left + (long long)i * n;
+    for (int k = 0; k < n; ++k) s = fma(li[k], right[(long long)k * n + j], s);
+  }
+  out[(long long)i * n + j] = s;
+}
+
+__global__ void normalize_sign_kernel(double* r, int n, double* sgn, const DevStatus* st) {
+  if (failed(st)) return;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double* ri = r + (long long)i * n;
+    if (ri[i] < 0.0) {
+      for (int c = i; c < n; ++c) ri[c] = -ri[c];
+      sgn[i] = -1.0;
+    } else {
+      sgn[i] = 1.0;
+    }
+  }
+}
+
+template <typename K, typename... Args>
+cudaError_t launch_small(K kernel, size_t bytes, cudaStream_t s, Args... args) {
+  const int use_smem = bytes <= kSmemCap ? 1 : 0;
+  const size_t smem = use_smem ? bytes : 0;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+  if (e != cudaSuccess) return e;
+  (void)use_smem;
+  kernel<<<1, kT, smem, s>>>(args...);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t small_work_doubles(int rows, int n) { return (size_t)rows * n; }
+
+cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int shift_mode, double shift_value,
+                            double theory_coef, double* shift_out, DevStatus* st, cudaStream_t s) {
+  const size_t bytes = (size_t)n * n * sizeof(double);
+  const int use_smem = bytes <= kSmemCap;
+  return launch_small(cholesky_kernel, bytes, s, g, n, r, work, use_smem, shift_mode, shift_value, theory_coef,
+                      shift_out, st);
+}
+
+cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
+  const size_t bytes = (size_t)l * n * sizeof(double);
+  const int use_smem = bytes <= kSmemCap;
+  return launch_small(lu_kernel, bytes, s, a1, l, n, u, work, use_smem, st);
+}
+
+cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work, DevStatus* st, cudaStream_t s) {
+  if (n > 512) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)l * n * sizeof(double);
+  const int use_smem = bytes <= kSmemCap;
+  return launch_small(qr_kernel, bytes, s, a1, l, n, r, work, use_smem, st);
+}
+
+cudaError_t launch_triangular_product(const double* left, const double* right, int n, double* out,
+                                      const DevStatus* st, cudaStream_t s) {
+  dim3 grid((unsigned)((n + 127) / 128), (unsigned)n);
+  triangular_product_kernel<<<grid, 128, 0, s>>>(left, right, n, out, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normalize_sign(double* r, int n, double* sgn, const DevStatus* st, cudaStream_t s) {
+  normalize_sign_kernel<<<1, 256, 0, s>>>(r, n, sgn, st);
+  return cudaGetLastError();
+}
+
+}  // namespace cqr

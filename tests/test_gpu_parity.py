@@ -1,0 +1,320 @@
+"""Parity of the B200 path (through the C-ABI, libcqr.so) against the CPU oracle.
+
+Bitwise where the oracle pins the operation order and the device follows it:
+RNG integers, uniform row extraction, Gram (leaf tree), Cholesky, trisolve,
+LU, triangular product -> CholeskyQR/CholeskyQR2/sCholeskyQR3 and rLU with the
+uniform sketch are bit-identical to the oracle end to end (up to the sign of
+zero, which numpy's == ignores). Tolerance where it cannot be: the Box-Muller
+transcendentals (CUDA libm vs glibc, <= a few ulp), and therefore the Gaussian
+sketch and everything downstream of it, and the Householder R of rQR (tree
+reductions). Tolerances are written next to each assertion.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+from paper_2111_11148_b200 import _abi
+from paper_2111_11148_b200 import cholqr as G
+
+pytestmark = pytest.mark.gpu
+U = np.finfo(np.float64).eps
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "rng_golden.json")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    assert os.path.exists(G.LIB_PATH), "libcqr.so not built"
+    yield
+
+
+def uni(l, seed):
+    return G.SketchConfig(size=l, seed=seed)
+
+
+def relf(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------- rng ---------------------------------------------------------------
+def test_rng_bits_bitwise_golden():
+    g = json.load(open(GOLDEN))
+    for s in g["seeds"]:
+        seed = int(s)
+        ks = [int(k) for k, _ in g["bits"][s]]
+        for k, v in g["bits"][s]:
+            assert int(G.rng_bits(seed, int(k), 1)[0]) == int(v)
+        b = G.rng_bits(seed, 0, 4096)
+        assert np.array_equal(b, o.bits_fill(seed, 0, 4096))
+        del ks
+
+
+def test_rng_gaussian_within_ulps():
+    for seed in (0, 1, 42, o.derive(1, 0x5E7C)):
+        n = 200000
+        gd = G.rng_gaussian(seed, 12345, n)
+        go = o.gaussian_fill(seed, 12345, n)
+        # CUDA log/sincos vs glibc: |diff| <= 8 ulp of max(|g|, 1)
+        tol = 8 * U * np.maximum(np.abs(go), 1.0)
+        assert np.all(np.abs(gd - go) <= tol)
+        assert np.mean(gd == go) > 0.5  # most draws are bit-identical
+
+
+# ---------------- kernels -------------------------------------------------------------
+@pytest.mark.parametrize("m,n,seed", [(3, 3, 0), (50, 10, 7), (2500, 6, 11), (3000, 12, 2), (5000, 64, 3),
+                                      (4113, 128, 4), (2048, 1, 5), (20000, 33, 6), (9000, 200, 7),
+                                      (3000, 300, 8)])
+def test_gram_bitwise(m, n, seed):
+    a = o.gaussian_matrix(m, n, seed)
+    g = G.gram(a)
+    assert np.array_equal(g, o.gram(a))
+    assert np.array_equal(g, g.T)
+
+
+def test_gram_known_answers():
+    assert np.array_equal(G.gram(np.eye(3)), np.eye(3))
+    assert G.gram(np.array([[1.0], [2.0], [2.0]]))[0, 0] == 9.0
+
+
+@pytest.mark.parametrize("n,seed", [(1, 1), (2, 2), (30, 3), (64, 4), (128, 5), (129, 6), (256, 7)])
+def test_cholesky_bitwise(n, seed):
+    a = o.gaussian_matrix(3 * n + 5, n, seed)
+    g = o.gram(a)
+    assert np.array_equal(G.cholesky_upper(g), o.cholesky_upper(g))
+
+
+def test_cholesky_known_and_breakdown():
+    assert np.array_equal(G.cholesky_upper(np.array([[4.0, 2.0], [2.0, 2.0]])), np.array([[2.0, 1.0], [0.0, 1.0]]))
+    g = o.gram(o.synthesize(1000, 20, 1e10, 42))
+    with pytest.raises(o.OracleError) as eo:
+        o.cholesky_upper(g)
+    with pytest.raises(G.CholeskyBreakdown) as eg:
+        G.cholesky_upper(g)
+    assert eg.value.pivot_index == eo.value.index
+
+
+@pytest.mark.parametrize("m,n,seed", [(1, 2, 1), (30, 5, 2), (100, 8, 3), (2000, 9, 4), (3001, 24, 5),
+                                      (10000, 64, 6), (4099, 128, 7), (1000, 100, 8), (700, 256, 9),
+                                      (300, 300, 10), (200, 512, 11)])
+def test_trisolve_bitwise(m, n, seed):
+    a = o.gaussian_matrix(m, n, seed)
+    r = o.qr_r_factor(o.gaussian_matrix(2 * n + 3, n, seed + 100))
+    assert np.array_equal(G.right_trisolve(a, r), o.right_trisolve(a, r))
+
+
+def test_trisolve_identity_and_singular():
+    a = o.gaussian_matrix(30, 5, 1)
+    assert np.array_equal(G.right_trisolve(a, np.eye(5)), a)
+    r = np.eye(3)
+    r[1, 1] = 0.0
+    with pytest.raises(G.SingularTriangular) as e:
+        G.right_trisolve(o.gaussian_matrix(4, 3, 2), r)
+    assert e.value.index == 1
+
+
+@pytest.mark.parametrize("l,n,seed", [(2, 2, 1), (30, 10, 2), (128, 64, 3), (256, 128, 4), (300, 150, 5)])
+def test_lu_bitwise(l, n, seed):
+    a1 = o.gaussian_matrix(l, n, seed)
+    assert np.array_equal(G.lu_u_factor(a1), o.lu_u_factor(a1))
+
+
+def test_lu_known_and_singular():
+    assert np.array_equal(G.lu_u_factor(np.array([[2.0, 1.0], [4.0, 3.0]])), np.array([[4.0, 3.0], [0.0, -0.5]]))
+    z = np.zeros((4, 2))
+    z[:, 0] = 1.0
+    with pytest.raises(G.SingularTriangular):
+        G.lu_u_factor(z)
+
+
+@pytest.mark.parametrize("l,n,seed", [(2, 1, 1), (40, 10, 2), (128, 64, 3), (256, 128, 4), (512, 256, 5)])
+def test_qr_r_tolerance(l, n, seed):
+    a1 = o.gaussian_matrix(l, n, seed)
+    # different reduction trees: R agrees to a small multiple of u*cond
+    assert relf(G.qr_r_factor(a1), o.qr_r_factor(a1)) <= 1e-13
+    assert abs(G.qr_r_factor(np.array([[3.0], [4.0]]))[0, 0] - 5.0) <= 5e-15
+
+
+@pytest.mark.parametrize("m,n,l,seed", [(60, 4, 8, 21), (5000, 7, 9, 1234), (20001, 64, 128, 5),
+                                        (30000, 128, 256, 6), (4000, 200, 300, 7)])
+def test_sketch_gaussian_tolerance(m, n, l, seed):
+    a = o.gaussian_matrix(m, n, seed + 1)
+    ref = o.sketch_gaussian(a, l, seed)
+    got = G.sketch_gaussian(a, G.SketchConfig(strategy=G.Strategy.Gaussian, size=l), seed).a1
+    # Omega within a few ulp and a different summation tree: relative 1e-13
+    assert relf(got, ref) <= 1e-13
+    assert np.array_equal(got, G.sketch_gaussian(a, G.SketchConfig(strategy=G.Strategy.Gaussian, size=l),
+                                                 seed).a1)  # deterministic
+
+
+def test_uniform_gather_bitwise():
+    a = o.gaussian_matrix(1000, 10, 2)
+    for wr in (False, True):
+        s = G.sample_rows_uniform(a, G.SketchConfig(size=20, without_replacement=wr), 7)
+        a1, idx = o.sample_rows_uniform(a, 20, 7, wr)
+        assert np.array_equal(s.indices, idx) and np.array_equal(s.a1, a1)
+
+
+# ---------------- algorithms: bitwise families -----------------------------------------
+FIXED = _abi.options(shift_kind=_abi.SHIFT_FIXED, shift_value=1e-15)
+
+
+@pytest.mark.parametrize("method", [_abi.CHOLQR, _abi.CHOLQR2, _abi.SCHOLQR3])
+@pytest.mark.parametrize("m,n,kappa,seed", [(400, 10, 1e2, 12), (5000, 24, 1e5, 9), (20000, 50, 1e6, 5),
+                                            (10000, 128, 1e4, 3)])
+def test_cholqr_family_bitwise(method, m, n, kappa, seed):
+    a = o.synthesize(m, n, kappa, seed)
+    ref = o.factor(method, a, opts=FIXED)
+    f, _, rep = G._factor(method, a, None, FIXED)
+    assert np.array_equal(f.q, ref.q) and np.array_equal(f.r, ref.r)
+    assert [s.stage for s in f.report.stages] == [_abi.STAGE_NAMES[s.stage] for s in ref.stages]
+
+
+def test_scholqr3_theory_shift_bitwise():
+    a = o.synthesize(10000, 50, 1e5, 9)
+    th = _abi.options()
+    ref = o.factor(_abi.SCHOLQR3, a, opts=th)
+    f, _, _ = G._factor(_abi.SCHOLQR3, a, None, th)
+    assert np.array_equal(f.q, ref.q) and np.array_equal(f.r, ref.r)
+    sh = [s.shift for s in f.report.stages if s.shift is not None]
+    assert sh and sh[0] == [s.shift for s in ref.stages if s.has_shift][0]
+
+
+def test_breakdowns_match():
+    for method, kappa, seed in ((_abi.CHOLQR, 1e10, 3), (_abi.CHOLQR2, 1e12, 6)):
+        a = o.synthesize(2000, 20, kappa, seed)
+        with pytest.raises(o.OracleError) as eo:
+            o.factor(method, a)
+        with pytest.raises(G.CholeskyBreakdown) as eg:
+            G._factor(method, a, None, _abi.options())
+        assert eg.value.pivot_index == eo.value.index
+
+
+@pytest.mark.parametrize("m,n,kappa,l,seed", [(400, 16, 1.0, 32, 17), (500, 15, 1e8, 30, 26),
+                                              (20000, 50, 1e12, 100, 20), (20000, 50, 1e15, 100, 21),
+                                              (100000, 64, 1e10, 128, 1)])
+def test_rlu_uniform_bitwise(m, n, kappa, l, seed):
+    a = o.synthesize(m, n, kappa, seed) if kappa > 1 else o.random_orthogonal(m, n, seed)
+    ref = o.factor(_abi.RLU, a, _abi.sketch_cfg(size=l, seed=seed + 1))
+    f = G.rlu_cholesky_qr(a, uni(l, seed + 1))
+    assert np.array_equal(f.q, ref.q) and np.array_equal(f.r, ref.r)
+
+
+def test_identity_preconditioner_is_cholesky_qr():  # test_cholqr.cpp:113-121
+    a = o.synthesize(400, 10, 1e2, 12)
+    base = G.cholesky_qr(a)
+    f = G.precond_cholesky_qr(a, lambda a1: np.eye(a1.shape[1]), uni(20, 13))
+    assert np.array_equal(f.q, base.q) and np.array_equal(f.r, base.r)
+
+
+# ---------------- algorithms: tolerance families -----------------------------------------
+def q_tol(kappa):
+    # Q is determined to O(kappa*u): 10x the oracle's seed-to-seed spread, floor 1e-10
+    return max(1e-10, 0.5 * kappa * U)
+
+
+@pytest.mark.parametrize("m,n,kappa,l,seed", [(400, 16, 1.0, 32, 14), (20000, 50, 1e12, 100, 18),
+                                              (20000, 50, 1e15, 100, 21), (100000, 64, 1e10, 128, 2)])
+def test_rqr_uniform_tolerance(m, n, kappa, l, seed):
+    a = o.synthesize(m, n, kappa, seed) if kappa > 1 else o.random_orthogonal(m, n, seed)
+    ref = o.factor(_abi.RQR, a, _abi.sketch_cfg(size=l, seed=seed + 1))
+    f = G.rqr_cholesky_qr(a, uni(l, seed + 1))
+    assert relf(f.r, ref.r) <= 1e-13
+    assert np.linalg.norm(f.q - ref.q) / math.sqrt(n) <= q_tol(kappa)
+    assert o.orthogonality_error(f.q) <= max(2 * o.orthogonality_error(ref.q), 1e-11)
+    assert o.residual_error(a, f.q, f.r) <= max(2 * o.residual_error(a, ref.q, ref.r), 1e-12)
+
+
+@pytest.mark.parametrize("method", [_abi.RQR_GAUSSIAN, _abi.RLU])
+@pytest.mark.parametrize("m,n,kappa,seed", [(800, 16, 1e10, 29), (100000, 64, 1e10, 1), (50000, 128, 1e14, 2)])
+def test_gaussian_sketch_methods_tolerance(method, m, n, kappa, seed):
+    a = o.synthesize(m, n, kappa, seed)
+    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, rate=2.0, seed=o.derive(seed, 0x5E7C))
+    ref = o.factor(method, a, cfg)
+    f, _, _ = G._factor(method, a, G.SketchConfig(strategy=G.Strategy.Gaussian, seed=o.derive(seed, 0x5E7C)),
+                        _abi.options())
+    assert relf(f.r, ref.r) <= 1e-12
+    assert np.linalg.norm(f.q - ref.q) / math.sqrt(n) <= q_tol(kappa)
+    assert o.orthogonality_error(f.q) <= max(2 * o.orthogonality_error(ref.q), 1e-11)
+    assert o.residual_error(a, f.q, f.r) <= max(2 * o.residual_error(a, ref.q, ref.r), 1e-12)
+
+
+# ---------------- behaviour -------------------------------------------------------------------
+def test_retry_on_degenerate_draw():  # test_cholqr.cpp:211-234
+    a = np.eye(2)
+    exercised = False
+    for seed in range(256):
+        _, idx = o.sample_rows_uniform(a, 2, seed)
+        if idx[0] != idx[1]:
+            continue
+        try:
+            ref = o.factor(_abi.RQR, a, _abi.sketch_cfg(size=2, seed=seed))
+        except o.OracleError:
+            with pytest.raises(G.Error):
+                G.rqr_cholesky_qr(a, uni(2, seed))
+            continue
+        f = G.rqr_cholesky_qr(a, uni(2, seed))
+        assert f.report.stages[0].retries == ref.stages[0].retries >= 1
+        assert np.allclose(f.q, ref.q, atol=1e-15)
+        exercised = True
+        break
+    assert exercised
+
+
+def test_r_less_and_non_finite():
+    a = o.synthesize(300, 10, 1e4, 27)
+    f = G.rqr_cholesky_qr(a, uni(20, 28), G.Options(r_less=True))
+    assert f.r is None and f.report.r_less
+    assert o.orthogonality_error(f.q) <= 1e-12
+    b = np.ones((8, 2))
+    b[3, 1] = np.nan
+    with pytest.raises(ValueError):
+        G.cholesky_qr(b)
+
+
+def test_diagnostics_cond_x():  # test_cholqr.cpp:154-171 (20 of the 100 trials)
+    small = 0
+    for t in range(20):
+        a = o.synthesize(2000, 40, 1e5, 3000 + t)
+        f = G.rqr_cholesky_qr(a, uni(80, 4000 + t), G.Options(diagnostics=True))
+        ref = o.factor(_abi.RQR, a, _abi.sketch_cfg(size=80, seed=4000 + t), _abi.options(diagnostics=True))
+        c = [s.cond_x for s in f.report.stages if s.cond_x is not None][0]
+        cr = [s.cond_x for s in ref.stages if s.has_cond_x][0]
+        assert abs(c - cr) <= 1e-8 * cr
+        small += c <= 100.0
+    assert small >= 19
+
+
+def test_device_tensors_match_host():
+    import torch
+
+    a = o.synthesize(20000, 64, 1e12, 3)
+    cfg = G.SketchConfig(strategy=G.Strategy.Gaussian, seed=77)
+    fh = G.rqr_cholesky_qr(a, cfg)
+    ad = torch.as_tensor(a, device="cuda")
+    fd = G.rqr_cholesky_qr(ad, cfg)
+    assert np.array_equal(fd.q.cpu().numpy(), fh.q) and np.array_equal(fd.r, fh.r)
+    assert G.orthogonality_error_dev(fd.q) <= 1e-12
+    assert G.residual_error_dev(ad, fd.q, fd.r) <= 1e-14
+
+
+def test_run_parallel_counters():
+    a = o.synthesize(1000, 10, 1e3, 13)
+    run = G.run_parallel(G.Method.CholeskyQr, a, 4)
+    assert run.timing.comm_rounds == 2 and run.timing.comm_volume == 4.0 * 10 * 10
+    assert run.timing.total_ms > 0.0
+
+
+def test_launch_count_and_determinism():
+    a = o.synthesize(50000, 64, 1e8, 25)
+    ctx = G.context()
+    before = ctx.launches
+    f1 = G.rlu_cholesky_qr(a, G.SketchConfig(strategy=G.Strategy.Gaussian, seed=5))
+    f2 = G.rlu_cholesky_qr(a, G.SketchConfig(strategy=G.Strategy.Gaussian, seed=5))
+    assert ctx.launches - before >= 2 * 8
+    assert np.array_equal(f1.q, f2.q) and np.array_equal(f1.r, f2.r)
