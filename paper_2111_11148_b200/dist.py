@@ -1,0 +1,59 @@
+"""One process per GPU: the row-block data parallelism of the reference's
+parexec (parexec.hpp:11-57, simulated there with threads) on real GPUs.
+
+Rank b owns rows [ceil(b*m/p), ceil((b+1)*m/p)) of the global m x n matrix
+(parexec.cpp:13-15). The library sums the s x n sketch partials and the n x n
+Gram partials with NCCL all-reduce (its own communicator, created from a
+unique id that rank 0 broadcasts through torch.distributed), runs the small
+factorizations redundantly on every rank (identical inputs give identical R,
+so no broadcast and no collective for the retry decision), and leaves Q
+row-sharded. torch.distributed is only the plumbing (id exchange, barriers).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from . import cholqr as cq
+
+
+def shard_rows(m: int, p: int, b: int):
+    """(row0, rows) of block b (parexec.cpp:9-18)."""
+    lo, hi = cq.block_offset(m, p, b), cq.block_offset(m, p, b + 1)
+    return lo, hi - lo
+
+
+def make_context(device: int, rank: int | None = None, world: int | None = None):
+    """Context on `device` with an NCCL communicator over the torch.distributed group."""
+    import torch.distributed as td
+
+    ctx = cq.Context(device)
+    if world is None:
+        world = td.get_world_size() if td.is_initialized() else 1
+        rank = td.get_rank() if td.is_initialized() else 0
+    if world > 1:
+        obj = [cq.make_comm_id() if rank == 0 else None]
+        td.broadcast_object_list(obj, src=0)
+        ctx.attach_comm(rank, world, obj[0])
+    return ctx
+
+
+def factor_sharded(ctx, method, a_local, m_global: int, row0: int, cfg: cq.SketchConfig | None = None,
+                   opts=None, q_out=None):
+    """cqr_factor_dev on this rank's CUDA shard; returns (Q_local, R, report)."""
+    import torch
+
+    if opts is None:
+        opts = _abi.options()
+    cfg_c = (cfg or cq.SketchConfig())._c()
+    m_local, n = a_local.shape
+    q = q_out if q_out is not None else torch.empty_like(a_local)
+    r = np.zeros((n, n))
+    rep = _abi.Report()
+    st = cq._lib().cqr_factor_dev(ctx.h, method, C.c_void_p(a_local.data_ptr()), m_local, m_global, row0, n,
+                                  a_local.stride(0), C.byref(cfg_c), C.byref(opts), C.c_void_p(q.data_ptr()),
+                                  q.stride(0), cq._ptr(r), n, C.byref(rep))
+    ctx._check(st, rep.index)
+    return q, (None if opts.r_less else r), rep
