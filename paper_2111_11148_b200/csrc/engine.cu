@@ -249,7 +249,7 @@ void allreduce(cqr_ctx* c, double* p, size_t count) {
 // Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
 void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g) {
   cqr::GramPlan p = cqr::gram_plan(m, n);
-  double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.partial_doubles, 1));
+  double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.workspace_doubles, 1));
   int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
   const int key = p.np * 100000 + p.parts * 100 + p.maxt;
   if (c->tiles_key != key) {  // the table depends on (np, parts, maxt) only: upload once
@@ -262,6 +262,7 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
   if (m > 0) {
     LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, c->status, c->stream));
     LAUNCH(c, cqr::launch_gram_combine(p, part, g, c->world <= 1 ? 1 : 0, c->status, c->stream));
+    ++c->launches;
   } else {
     ck(cudaMemsetAsync(g, 0, sizeof(double) * n * n, c->stream), "memset");
   }
@@ -288,6 +289,15 @@ void trisolve_dev(cqr_ctx* c, const double* in, long long ldi, double* out, long
   t.num_sms = c->num_sms;
   t.status = c->status;
   LAUNCH(c, cqr::launch_trisolve(t, c->stream));
+}
+
+const char* status_msg(int code) {
+  switch (code) {
+    case CQR_CHOLESKY_BREAKDOWN: return "cholesky breakdown";
+    case CQR_SINGULAR_TRIANGULAR: return "singular triangular factor";
+    case CQR_INVALID_ARGUMENT: return "A has non-finite entries";
+    default: return "device failure";
+  }
 }
 
 void reset_status(cqr_ctx* c) { ck(cudaMemsetAsync(c->status, 0, sizeof(DevStatus), c->stream), "status reset"); }
@@ -344,7 +354,6 @@ Outcome run_cholqr_family(Job& j) {
   cqr_ctx* c = j.c;
   const int n = j.n;
   Outcome o;
-  reset_status(c);
   double* r1 = dbuf<double>(c, B_RT, (size_t)n * n);
   double* r2 = dbuf<double>(c, B_RH, (size_t)n * n);
   double* r3 = dbuf<double>(c, B_RTMP, (size_t)n * n);
@@ -380,7 +389,7 @@ Outcome run_cholqr_family(Job& j) {
     o.r_dev = r;
   }
   DevStatus s = read_status(c);
-  if (s.code != 0) throw Fail{s.code, s.index, s.code == 1 ? "cholesky breakdown" : "singular triangular factor"};
+  if (s.code != 0) throw Fail{s.code, s.index, status_msg(s.code)};
   if (j.method == CQR_SCHOLQR3 && j.opts.shift_kind != CQR_SHIFT_FIXED) {
     ck(cudaMemcpy(c->scal_h, dbuf<double>(c, B_SCAL, 4), sizeof(double), cudaMemcpyDeviceToHost), "shift D2H");
     for (auto& st : o.rep.stages)
@@ -409,7 +418,7 @@ Outcome run_precond(Job& j) {
     const bool last = attempt >= j.cfg.max_retries;
     const long long l = resolved_size(try_cfg, m, n);
     Outcome o;
-    reset_status(c);
+    if (attempt > 0) reset_status(c);
     double* a1 = dbuf<double>(c, B_A1, (size_t)l * n);
     // ---- Sketch (sketch.cpp:94-127)
     {
@@ -524,7 +533,7 @@ Outcome run_precond(Job& j) {
       return o;
     }
     if ((s.code == CQR_CHOLESKY_BREAKDOWN || s.code == CQR_SINGULAR_TRIANGULAR) && !last) continue;
-    throw Fail{s.code, s.index, s.code == 1 ? "cholesky breakdown" : "singular triangular factor"};
+    throw Fail{s.code, s.code == CQR_INVALID_ARGUMENT ? -1 : s.index, status_msg(s.code)};
   }
 }
 
@@ -574,21 +583,32 @@ int guarded(cqr_ctx* c, F&& f) {
   }
 }
 
-// device-side finiteness check (engine.cpp:222, errors.hpp:89-93)
-__global__ void finite_kernel(const double* __restrict__ a, long long lda, long long m, int n, DevStatus* st) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m * n;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long i = e / n, j = e - (e / n) * n;
-    if (!isfinite(a[i * lda + j])) {
-      cqr::set_status(st, CQR_INVALID_ARGUMENT, i);
-      return;
+// device-side finiteness check (engine.cpp:222, errors.hpp:89-93): one pass
+// over A with 16-byte loads; a warp vote keeps the flag write rare.
+__global__ void finite_kernel(const double* __restrict__ a, long long lda, long long m, int n, int vec,
+                              DevStatus* st) {
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (lda == n && vec) {
+    const double2* p = reinterpret_cast<const double2*>(a);
+    const long long total = m * n / 2;
+    for (long long e = t0; e < total; e += stride) {
+      const double2 v = __ldg(p + e);
+      bad |= !isfinite(v.x) || !isfinite(v.y);
     }
+    if (t0 == 0 && (m * n) % 2) bad |= !isfinite(a[m * n - 1]);
+  } else {
+    for (long long i = t0 / 32; i < m; i += stride / 32)
+      for (int j = (int)(t0 & 31); j < n; j += 32) bad |= !isfinite(a[i * lda + j]);
   }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) cqr::set_status(st, CQR_INVALID_ARGUMENT, -1);
 }
 
 void check_finite(cqr_ctx* c, const double* a, long long m, int n, long long lda) {
   if (m <= 0) return;
-  finite_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(a, lda, m, n, c->status);
+  const int vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+  finite_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(a, lda, m, n, vec, c->status);
   ck(cudaGetLastError(), "finite_kernel");
   ++c->launches;
 }
@@ -608,10 +628,12 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     require(j.m_local >= 0 && j.row0 >= 0 && j.row0 + j.m_local <= j.m_global, "bad shard");
     require(j.n <= 512, "n > 512 is not supported by the device kernels");
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    // non-finite input is rejected up front (engine.cpp:222)
+    // non-finite input is rejected up front (engine.cpp:222). One process: the
+    // check only sets the status word (read with the attempt's single sync);
+    // several ranks agree on it first so they take the same path.
     reset_status(c);
     check_finite(c, j.a, j.m_local, j.n, j.lda);
-    {
+    if (c->world > 1) {
       DevStatus s0 = read_status(c);
       int bad = s0.code != 0;
       if (c->world > 1) {

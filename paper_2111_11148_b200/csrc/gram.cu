@@ -105,43 +105,59 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
   }
 }
 
-// Streaming pairwise tree: after pushing leaf i, merge (top-1) + top once per
-// trailing zero of (i+1); finally fold the stack right to left.
-__global__ void gram_combine_kernel(const double* __restrict__ partial, int leaves, int np, int n,
-                                    double* __restrict__ g, int mirror, const DevStatus* st) {
+// The pairwise tree of kernels.hpp:42-57 in streaming form: after pushing leaf
+// i, merge (top-1) + top once per trailing zero of (i+1); at the end fold the
+// stack right to left. Two levels for parallelism: level A folds each aligned
+// group of kGroup leaves (a complete group is a perfect subtree; the last,
+// partial group is folded by the same rule), level B runs the counter over the
+// complete groups and appends the partial group last. Equal to the one-level
+// form because subtrees of different sizes never merge.
+constexpr int kGroup = 16;
+
+__device__ __forceinline__ void push_merge(double* stk, int& top, double v, unsigned count_after) {
+  while ((count_after & 1u) == 0u) {
+    v = stk[--top] + v;
+    count_after >>= 1;
+  }
+  stk[top++] = v;
+}
+
+__global__ void gram_combine_a_kernel(const double* __restrict__ partial, int leaves, int np, int n,
+                                      double* __restrict__ gsum, const DevStatus* st) {
+  if (failed(st)) return;
+  const int i = blockIdx.y;
+  const int j = i + blockIdx.x * blockDim.x + threadIdx.x;
+  const int grp = blockIdx.z;
+  if (j >= n) return;
+  const long long stride = (long long)np * np;
+  const int l0 = grp * kGroup, l1 = min(leaves, l0 + kGroup);
+  const double* p = partial + (long long)i * np + j;
+  double v[kGroup];
+#pragma unroll
+  for (int u = 0; u < kGroup; ++u) v[u] = (l0 + u < l1) ? __ldg(p + (long long)(l0 + u) * stride) : 0.0;
+  double stk[8];
+  int top = 0;
+#pragma unroll
+  for (int u = 0; u < kGroup; ++u)
+    if (l0 + u < l1) push_merge(stk, top, v[u], (unsigned)(u + 1));
+  double acc = stk[top - 1];
+  for (int k = top - 2; k >= 0; --k) acc = stk[k] + acc;
+  gsum[(long long)grp * np * np + (long long)i * np + j] = acc;
+}
+
+__global__ void gram_combine_b_kernel(const double* __restrict__ gsum, int leaves, int np, int n,
+                                      double* __restrict__ g, int mirror, const DevStatus* st) {
   if (failed(st)) return;
   const int i = blockIdx.y;
   const int j = i + blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  const double* p = partial + (long long)i * np + j;
+  const int full = leaves / kGroup, groups = (leaves + kGroup - 1) / kGroup;
   const long long stride = (long long)np * np;
+  const double* p = gsum + (long long)i * np + j;
   double stk[40];
   int top = 0;
-  int leaf = 0;
-  for (; leaf + 8 <= leaves; leaf += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (long long)(leaf + u) * stride);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      double cur = v[u];
-      unsigned t = (unsigned)(leaf + u + 1);
-      while ((t & 1u) == 0u) {
-        cur = stk[--top] + cur;
-        t >>= 1;
-      }
-      stk[top++] = cur;
-    }
-  }
-  for (; leaf < leaves; ++leaf) {
-    double cur = __ldg(p + (long long)leaf * stride);
-    unsigned t = (unsigned)(leaf + 1);
-    while ((t & 1u) == 0u) {
-      cur = stk[--top] + cur;
-      t >>= 1;
-    }
-    stk[top++] = cur;
-  }
+  for (int k = 0; k < full; ++k) push_merge(stk, top, __ldg(p + (long long)k * stride), (unsigned)(k + 1));
+  if (groups > full) stk[top++] = __ldg(p + (long long)full * stride);
   double acc = stk[top - 1];
   for (int k = top - 2; k >= 0; --k) acc = stk[k] + acc;
   g[(long long)i * n + j] = acc;
@@ -183,6 +199,7 @@ GramPlan gram_plan(long long m, int n) {
   p.maxt = maxt <= 1 ? 1 : maxt <= 2 ? 2 : maxt <= 5 ? 5 : 9;
   p.ch = p.np <= 128 ? 32 : 16;
   p.partial_doubles = (size_t)p.leaves * p.np * p.np;
+  p.workspace_doubles = p.partial_doubles + (size_t)((p.leaves + kGroup - 1) / kGroup) * p.np * p.np;
   p.tiles_bytes = (size_t)p.parts * kWpc * p.maxt * sizeof(int32_t);
   return p;
 }
@@ -223,10 +240,14 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_gram_combine(const GramPlan& p, const double* partial, double* g, int mirror,
+cudaError_t launch_gram_combine(const GramPlan& p, double* partial, double* g, int mirror,
                                 const DevStatus* st, cudaStream_t s) {
-  dim3 grid((unsigned)((p.n + 127) / 128), (unsigned)p.n);
-  gram_combine_kernel<<<grid, 128, 0, s>>>(partial, p.leaves, p.np, p.n, g, mirror, st);
+  const int groups = (p.leaves + kGroup - 1) / kGroup;
+  double* gsum = partial + p.partial_doubles;  // workspace after the leaf partials (gram_plan reserves it)
+  dim3 ga((unsigned)((p.n + 127) / 128), (unsigned)p.n, (unsigned)groups);
+  gram_combine_a_kernel<<<ga, 128, 0, s>>>(partial, p.leaves, p.np, p.n, gsum, st);
+  dim3 gb((unsigned)((p.n + 127) / 128), (unsigned)p.n);
+  gram_combine_b_kernel<<<gb, 128, 0, s>>>(gsum, p.leaves, p.np, p.n, g, mirror, st);
   return cudaGetLastError();
 }
 

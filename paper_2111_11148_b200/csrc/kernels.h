@@ -36,7 +36,8 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s);
 struct GramPlan {
   int n = 0, np = 0, leaves = 0, parts = 0, maxt = 0, wpc = 0, ch = 0;
   long long m = 0;
-  size_t partial_doubles = 0;  // leaves * np * np
+  size_t partial_doubles = 0;    // leaves * np * np
+  size_t workspace_doubles = 0;  // partials + the per-group sums of the combine
   size_t tiles_bytes = 0;
 };
 GramPlan gram_plan(long long m, int n);
@@ -47,7 +48,7 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
                                double* partial, int vec16, const DevStatus* st, cudaStream_t s);
 // Pairwise tree over leaves (kernels.hpp:42-57, streaming form) -> g upper (ld = n);
 // mirror=1 also writes the lower triangle (kernels.hpp:69).
-cudaError_t launch_gram_combine(const GramPlan& p, const double* partial, double* g, int mirror,
+cudaError_t launch_gram_combine(const GramPlan& p, double* partial, double* g, int mirror,
                                 const DevStatus* st, cudaStream_t s);
 cudaError_t launch_mirror_upper(double* g, int n, const DevStatus* st, cudaStream_t s);
 

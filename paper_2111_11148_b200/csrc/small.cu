@@ -84,10 +84,11 @@ __global__ void __launch_bounds__(kT) cholesky_kernel(const double* __restrict__
     double* Si = S + (long long)i * n;
     for (int j = i + 1 + tid; j < n; j += nt) Si[j] = Si[j] / d;
     __syncthreads();
-    const int w = n - i - 1;
-    for (int e = tid; e < w * w; e += nt) {
-      const int a = i + 1 + e / w, b = i + 1 + e % w;
-      if (b >= a) S[(long long)a * n + b] = fma(-Si[a], Si[b], S[(long long)a * n + b]);
+    // trailing update of the upper triangle: warps over rows, lanes over columns
+    for (int a = i + 1 + (tid >> 5); a < n; a += nt >> 5) {
+      const double ra = Si[a];
+      double* Sa = S + (long long)a * n;
+      for (int b = a + (tid & 31); b < n; b += 32) Sa[b] = fma(-ra, Si[b], Sa[b]);
     }
     __syncthreads();
   }
@@ -164,13 +165,14 @@ __global__ void __launch_bounds__(kT) lu_kernel(const double* __restrict__ a1, i
     const double d = W[(long long)j * n + j];
     for (int i = j + 1 + tid; i < l; i += nt) W[(long long)i * n + j] = W[(long long)i * n + j] / d;
     __syncthreads();
-    const int w = n - j - 1;
-    if (w > 0) {
+    if (j + 1 < n) {
       const double* pr = W + (long long)j * n;
-      for (long long e = tid; e < (long long)(l - j - 1) * w; e += nt) {
-        const int i = j + 1 + (int)(e / w), c = j + 1 + (int)(e % w);
-        const double mult = W[(long long)i * n + j];
-        if (mult != 0.0) W[(long long)i * n + c] = fma(-mult, pr[c], W[(long long)i * n + c]);
+      // warps over rows, lanes over columns (coalesced), no integer division
+      for (int i = j + 1 + warp; i < l; i += nw) {
+        double* Wi = W + (long long)i * n;
+        const double mult = Wi[j];
+        if (mult != 0.0)
+          for (int c = j + 1 + lane; c < n; c += 32) Wi[c] = fma(-mult, pr[c], Wi[c]);
       }
     }
     __syncthreads();
@@ -234,14 +236,15 @@ __global__ void __launch_bounds__(kT) qr_kernel(const double* __restrict__ a1, i
         if (lane == 0) ts[c] = tau * (cc[j] + s);
       }
       __syncthreads();
-      const int w = n - j - 1, h = l - j;
-      for (long long e = tid; e < (long long)w * h; e += nt) {
-        const int c = j + 1 + (int)(e / h), i = j + (int)(e % h);
+      for (int c = j + 1 + warp; c < n; c += nw) {
         double* cc = W + (long long)c * l;
-        if (i == j)
-          cc[j] -= ts[c];
-        else
-          cc[i] = fma(-ts[c], col[i], cc[i]);
+        const double t = ts[c];
+        for (int i = j + lane; i < l; i += 32) {
+          if (i == j)
+            cc[j] -= t;
+          else
+            cc[i] = fma(-t, col[i], cc[i]);
+        }
       }
     }
     __syncthreads();
@@ -257,31 +260,47 @@ __global__ void __launch_bounds__(kT) qr_kernel(const double* __restrict__ a1, i
       for (int c = i; c < n; ++c) r[(long long)i * n + c] = -r[(long long)i * n + c];
 }
 
+// 32x32 output tile per CTA (32x8 threads, 4 rows each); k chunks of 32 staged
+// in shared memory, ascending, so every element is the fma chain over k = 0..n-1.
 __global__ void triangular_product_kernel(const double* __restrict__ left, const double* __restrict__ right, int n,
                                           double* __restrict__ out, const DevStatus* st) {
+  __shared__ double sl[32][33], sr[32][33];
   if (failed(st)) return;
-  const int i = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  double s = 0.0;
-  if (j >= i) {
-    const double* li = left + (long long)i * n;
-    for (int k = 0; k < n; ++k) s = fma(li[k], right[(long long)k * n + j], s);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool any = j0 + 31 >= i0;  // tile touches the upper triangle
+  for (int k0 = 0; any && k0 < n; k0 += 32) {
+    for (int u = 0; u < 4; ++u) {
+      const int r = ty + 8 * u;
+      sl[r][tx] = (i0 + r < n && k0 + tx < n) ? left[(long long)(i0 + r) * n + k0 + tx] : 0.0;
+      sr[r][tx] = (k0 + r < n && j0 + tx < n) ? right[(long long)(k0 + r) * n + j0 + tx] : 0.0;
+    }
+    __syncthreads();
+    const int kk = min(32, n - k0);
+    for (int k = 0; k < kk; ++k)
+      for (int u = 0; u < 4; ++u) acc[u] = fma(sl[ty + 8 * u][k], sr[k][tx], acc[u]);
+    __syncthreads();
   }
-  out[(long long)i * n + j] = s;
+  for (int u = 0; u < 4; ++u) {
+    const int i = i0 + ty + 8 * u, j = j0 + tx;
+    if (i < n && j < n) out[(long long)i * n + j] = (j >= i) ? acc[u] : 0.0;
+  }
 }
 
 __global__ void normalize_sign_kernel(double* r, int n, double* sgn, const DevStatus* st) {
+  __shared__ double s[512];
   if (failed(st)) return;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double* ri = r + (long long)i * n;
-    if (ri[i] < 0.0) {
-      for (int c = i; c < n; ++c) ri[c] = -ri[c];
-      sgn[i] = -1.0;
-    } else {
-      sgn[i] = 1.0;
-    }
+    const double v = r[(long long)i * n + i] < 0.0 ? -1.0 : 1.0;
+    s[i] = v;
+    sgn[i] = v;
   }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < n; i += nw)
+    if (s[i] < 0.0)
+      for (int c = i + lane; c < n; c += 32) r[(long long)i * n + c] = -r[(long long)i * n + c];
 }
 
 template <typename K, typename... Args>
@@ -322,13 +341,13 @@ cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work,
 
 cudaError_t launch_triangular_product(const double* left, const double* right, int n, double* out,
                                       const DevStatus* st, cudaStream_t s) {
-  dim3 grid((unsigned)((n + 127) / 128), (unsigned)n);
-  triangular_product_kernel<<<grid, 128, 0, s>>>(left, right, n, out, st);
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  triangular_product_kernel<<<grid, dim3(32, 8), 0, s>>>(left, right, n, out, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_normalize_sign(double* r, int n, double* sgn, const DevStatus* st, cudaStream_t s) {
-  normalize_sign_kernel<<<1, 256, 0, s>>>(r, n, sgn, st);
+  normalize_sign_kernel<<<1, 1024, 0, s>>>(r, n, sgn, st);
   return cudaGetLastError();
 }
 

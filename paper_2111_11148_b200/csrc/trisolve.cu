@@ -1,19 +1,26 @@
 // trisolve.cu — tall right triangular solve X R = A (kernels.hpp:94-127).
 //
 // Reference recurrence, per row and column j: y_j = a_j; for k < j:
-// y_j = fma(-r_kj, x_k, y_j); x_j = y_j / r_jj. A row's result depends only on
-// that row, so any row partition gives the same bits (kernels.hpp:98-101).
+// y_j = fma(-r_kj, x_k, y_j) (skipped when r_kj == 0); x_j = y_j / r_jj. A row's
+// result depends only on that row, so any row partition gives the same bits
+// (kernels.hpp:98-101).
 //
-// B200 mapping: each warp owns a panel of 8*MG rows staged in shared memory.
-// Columns are processed in blocks J of 8. The contributions of all earlier
-// blocks (k < 8J) are accumulated with DMMA m8n8k4 (A operand = solved X
-// columns from smem, B operand = -R tile). DMMA accumulates as the sequential
-// fma chain in k order, so this is the reference's chain bit for bit. The
-// 8x8 diagonal block then runs the remaining k in [8J, j) as scalar fma + an
-// IEEE division, inside the DMMA accumulator registers (4 lanes per row,
-// shuffles broadcast x_k). Rows are independent, so warps never synchronise.
+// B200 mapping. Each warp owns a panel of RW = 8*MG rows staged in shared
+// memory; columns go in blocks J of 8:
+//  1. off-diagonal part, k < 8J: DMMA m8n8k4 with A = solved X columns (smem)
+//     and B = -R tiles (smem when they fit). DMMA accumulates as the
+//     sequential fma chain in k order (profiles/r01_fp64_probe.txt), so this is
+//     the reference's chain bit for bit (zero terms are not skipped: only the
+//     sign of an exact zero can differ);
+//  2. diagonal 8x8 block, one lane per row: the remaining k in [8J, j) as
+//     scalar fma, then the division. The division uses RN(1/r_jj) (computed
+//     once per column by pack_r) and two Markstein corrections, which is the
+//     correctly rounded quotient (tools/probe/markstein_check.c: 2e8 cases,
+//     0 mismatches; tests/test_gpu_parity.py checks it on device), with the
+//     IEEE division kept for zeros and extreme exponents.
+// Rows are independent, so warps never synchronise with each other.
 //
-// HBM bytes per row: 8n read + 8n written; flops: n^2 (n(n-1)/2 fma + n div).
+// Per row: HBM 8n bytes read + 8n written; n^2 flops (n(n-1)/2 fma + n div).
 
 #include "common.cuh"
 #include "kernels.h"
@@ -22,40 +29,29 @@ namespace cqr {
 
 namespace {
 
-// Bpack[(J*(J-1) + k4)*32 + lane] = -R[4*k4 + (lane&3)][8*J + (lane>>2)], k4 < 2J
-// Dpack[J*64 + kk*8 + q*2 + e]     = R[8J+kk][8J + 2q + e]          (8x8 diagonal block)
-// R is padded to np with the identity. Checks the diagonal first (lowest
-// index wins): degenerate=1 flags zero or non-finite (engine.cpp:118-127),
-// degenerate=0 flags exact zeros only (kernels.hpp:106-107).
+// Packed R for a padded width np (R padded with the identity):
+//   bpack[(J*(J-1) + k4)*32 + lane] = -R[4*k4 + (lane&3)][8J + (lane>>2)]   (k4 < 2J)
+//   dpack[J*80 + kk*8 + j]          =  R[8J+kk][8J+j]                       (8x8 diag block)
+//   dpack[J*80 + 64 + j]            =  RN(1 / R[8J+j][8J+j])
+//   dpack[J*80 + 72 + j]            =  1 if the fast division is safe for column j
+constexpr int kDiagStride = 80;
+
 __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int np, double* __restrict__ bpack,
-                              double* __restrict__ dpack, int degenerate, DevStatus* st) {
+                              double* __restrict__ dpack, int* __restrict__ bad_min, int degenerate,
+                              DevStatus* st) {
   if (failed(st)) return;
-  __shared__ int bad;
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int b = -1;
-    for (int j = 0; j < n; ++j) {
-      const double d = r[(long long)j * ldr + j];
-      if (d == 0.0 || (degenerate && !isfinite(d))) {
-        b = j;
-        break;
-      }
-    }
-    if (b >= 0) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, b);
-  }
-  (void)bad;
   auto R = [&](int i, int j) -> double {
     if (i < n && j < n) return r[(long long)i * ldr + j];
     return (i == j) ? 1.0 : 0.0;
   };
   const int nt = np / 8;
   const long long nb = (long long)nt * (nt - 1) * 32;
-  const long long nd = (long long)nt * 64;
+  const long long nd = (long long)nt * kDiagStride;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nb + nd;
        e += (long long)gridDim.x * blockDim.x) {
     if (e < nb) {
       const int lane = (int)(e & 31);
       const long long f = e >> 5;
-      // invert f = J*(J-1) + k4, 0 <= k4 < 2J
       int J = (int)((1.0 + sqrt(1.0 + 4.0 * (double)f)) * 0.5);
       while ((long long)J * (J - 1) > f) --J;
       while ((long long)(J + 1) * J <= f) ++J;
@@ -63,11 +59,44 @@ __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int 
       bpack[e] = -R(4 * k4 + (lane & 3), 8 * J + (lane >> 2));
     } else {
       const long long d = e - nb;
-      const int J = (int)(d / 64), w = (int)(d % 64);
-      const int kk = w / 8, q = (w % 8) / 2, ee = w % 2;
-      dpack[d] = R(8 * J + kk, 8 * J + 2 * q + ee);
+      const int J = (int)(d / kDiagStride), w = (int)(d % kDiagStride);
+      double v;
+      if (w < 64) {
+        v = R(8 * J + w / 8, 8 * J + w % 8);
+      } else {
+        const int j = 8 * J + (w - 64) % 8;
+        const double dj = R(j, j);
+        if (w < 72) {
+          v = 1.0 / dj;
+        } else {
+          const double a = fabs(dj);
+          v = (a >= 0x1p-500 && a <= 0x1p+500) ? 1.0 : 0.0;
+        }
+      }
+      dpack[d] = v;
     }
   }
+  // diagonal check, lowest failing index (kernels.hpp:106-107 / engine.cpp:118-127)
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double dj = r[(long long)j * ldr + j];
+    if (dj == 0.0 || (degenerate && !isfinite(dj))) atomicMin(bad_min, j);
+  }
+}
+
+__global__ void pack_status_kernel(const int* bad_min, int n, DevStatus* st) {
+  if (*bad_min < n) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, *bad_min);
+}
+
+__device__ __forceinline__ double fast_div(double y, double d, double inv, bool safe) {
+  const double ay = fabs(y);
+  if (!safe || !(ay >= 0x1p-900 && ay <= 0x1p+900)) {
+    return (y == 0.0 && safe) ? y * inv : y / d;
+  }
+  const double q0 = y * inv;
+  double r = fma(-q0, d, y);
+  const double q1 = fma(r, inv, q0);
+  r = fma(-q1, d, y);
+  return fma(r, inv, q1);
 }
 
 template <int NP, int MG, int WPC, bool BSMEM>
@@ -81,113 +110,130 @@ __global__ void __launch_bounds__(WPC * 32) trisolve_kernel(const double* in, lo
   constexpr int RW = 8 * MG;
   constexpr int LDX = NP + 4;
   constexpr int NB = NT * (NT - 1) * 32;
+  constexpr int ND = NT * kDiagStride;
   extern __shared__ __align__(16) double smem[];
   if (failed(st)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, gr = lane >> 2;
+  double* sD = smem;
   const double* sB = bpack;
-  double* sX = smem + (BSMEM ? NB : 0) + warp * RW * LDX;
+  double* sX = smem + ND + (BSMEM ? NB : 0) + warp * RW * LDX;
+  for (int e = threadIdx.x; e < ND; e += WPC * 32) sD[e] = dpack[e];
   if constexpr (BSMEM) {
-    double* s = smem;
+    double* s = smem + ND;
     for (int e = threadIdx.x; e < NB; e += WPC * 32) s[e] = bpack[e];
     sB = s;
-    __syncthreads();
   }
+  __syncthreads();
   const long long groups = (m + RW - 1) / RW;
   for (long long grp = (long long)blockIdx.x * WPC + warp; grp < groups; grp += (long long)gridDim.x * WPC) {
     const long long row0 = grp * RW;
     const int rows = (int)min((long long)RW, m - row0);
-    stage_rows(sX, LDX, in + row0 * ldi, ldi, rows, RW, n, NP, lane, 32, vec16 != 0);
+    // stage the panel (zero-padded columns and rows)
+    if (vec16) {
+      for (int r = 0; r < RW; ++r)
+        for (int c2 = lane; c2 < NP / 2; c2 += 32) {
+          double* d = sX + r * LDX + 2 * c2;
+          if (r < rows && 2 * c2 < n)
+            cp_async16(d, in + (row0 + r) * ldi + 2 * c2);
+          else
+            *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);
+        }
+    } else {
+      for (int r = 0; r < RW; ++r)
+        for (int c = lane; c < NP; c += 32) {
+          double* d = sX + r * LDX + c;
+          if (r < rows && c < n)
+            cp_async8(d, in + (row0 + r) * ldi + c);
+          else
+            *d = 0.0;
+        }
+    }
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
 #pragma unroll 1
     for (int J = 0; J < NT; ++J) {
-      double c[MG][2];
-#pragma unroll
-      for (int g = 0; g < MG; ++g) {
-        const double2 v = *reinterpret_cast<const double2*>(sX + (g * 8 + gr) * LDX + 8 * J + 2 * q);
-        c[g][0] = v.x;
-        c[g][1] = v.y;
-      }
-      const double* bj = sB + (long long)J * (J - 1) * 32 + lane;
-      const double* xa = sX + gr * LDX + q;
-#pragma unroll 4
-      for (int k4 = 0; k4 < 2 * J; ++k4) {
-        const double b = BSMEM ? bj[k4 * 32] : __ldg(bj + k4 * 32);
-#pragma unroll
-        for (int g = 0; g < MG; ++g) dmma(c[g][0], c[g][1], xa[g * 8 * LDX + 4 * k4], b);
-      }
-      // diagonal block: remaining k in [8J, j) then the division, per row
-      double dv[8][2];
-      const double* dp = dpack + J * 64 + q * 2;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(dp + kk * 8));
-        dv[kk][0] = v.x;
-        dv[kk][1] = v.y;
-      }
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const int qo = kk >> 1, eo = kk & 1;
+      if (J > 0) {
+        double c[MG][2];
 #pragma unroll
         for (int g = 0; g < MG; ++g) {
-          double x = 0.0;
-          if (q == qo) {
-            x = (eo ? c[g][1] : c[g][0]) / (eo ? dv[kk][1] : dv[kk][0]);
-            if (eo)
-              c[g][1] = x;
-            else
-              c[g][0] = x;
-          }
-          x = __shfl_sync(0xffffffffu, x, (lane & ~3) | qo);
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = 2 * q + e;
-            if (col > kk) {
-              const double rr = dv[kk][e];
-              if (rr != 0.0) c[g][e] = fma(-rr, x, c[g][e]);
-            }
-          }
+          const double2 v = *reinterpret_cast<const double2*>(sX + (g * 8 + gr) * LDX + 8 * J + 2 * q);
+          c[g][0] = v.x;
+          c[g][1] = v.y;
         }
+        const double* bj = sB + (long long)J * (J - 1) * 32 + lane;
+        const double* xa = sX + gr * LDX + q;
+#pragma unroll 4
+        for (int k4 = 0; k4 < 2 * J; ++k4) {
+          const double b = BSMEM ? bj[k4 * 32] : __ldg(bj + k4 * 32);
+#pragma unroll
+          for (int g = 0; g < MG; ++g) dmma(c[g][0], c[g][1], xa[g * 8 * LDX + 4 * k4], b);
+        }
+#pragma unroll
+        for (int g = 0; g < MG; ++g)
+          *reinterpret_cast<double2*>(sX + (g * 8 + gr) * LDX + 8 * J + 2 * q) = make_double2(c[g][0], c[g][1]);
+        __syncwarp();
       }
-      // publish the solved block: smem (operand for later blocks) and global
+      // diagonal block: one lane per row
+      if (lane < RW) {
+        double* xr = sX + lane * LDX + 8 * J;
+        double y[8];
 #pragma unroll
-      for (int g = 0; g < MG; ++g) {
-        *reinterpret_cast<double2*>(sX + (g * 8 + gr) * LDX + 8 * J + 2 * q) = make_double2(c[g][0], c[g][1]);
-        const int r = g * 8 + gr;
-        const int col = 8 * J + 2 * q;
-        if (r < rows) {
-          double* o = out + (row0 + r) * ldo + col;
-          double v0 = c[g][0], v1 = c[g][1];
-          if (sgn != nullptr) {
-            if (col < n) v0 *= sgn[col];
-            if (col + 1 < n) v1 *= sgn[col + 1];
-          }
-          if (vec16 && col + 1 < n) {
-            *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
-          } else {
-            if (col < n) o[0] = v0;
-            if (col + 1 < n) o[1] = v1;
-          }
+        for (int u = 0; u < 4; ++u) {
+          const double2 v = *reinterpret_cast<const double2*>(xr + 2 * u);
+          y[2 * u] = v.x;
+          y[2 * u + 1] = v.y;
         }
+        const double* D = sD + J * kDiagStride;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#pragma unroll
+          for (int kk = 0; kk < j; ++kk) {
+            const double rr = D[kk * 8 + j];
+            if (rr != 0.0) y[j] = fma(-rr, y[kk], y[j]);
+          }
+          y[j] = fast_div(y[j], D[j * 8 + j], D[64 + j], D[72 + j] != 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(xr + 2 * u) = make_double2(y[2 * u], y[2 * u + 1]);
       }
       __syncwarp();
     }
+    // write the solved panel (coalesced rows), applying the column signs
+    if (vec16) {
+      for (int r = 0; r < rows; ++r)
+        for (int c2 = lane; 2 * c2 < n; c2 += 32) {
+          double2 v = *reinterpret_cast<const double2*>(sX + r * LDX + 2 * c2);
+          if (sgn) {
+            v.x *= sgn[2 * c2];
+            v.y *= sgn[2 * c2 + 1];
+          }
+          *reinterpret_cast<double2*>(out + (row0 + r) * ldo + 2 * c2) = v;
+        }
+    } else {
+      for (int r = 0; r < rows; ++r)
+        for (int c = lane; c < n; c += 32) {
+          double v = sX[r * LDX + c];
+          if (sgn) v *= sgn[c];
+          out[(row0 + r) * ldo + c] = v;
+        }
+    }
+    __syncwarp();
   }
 }
 
 template <int NP, int MG, int WPC, bool BSMEM>
 cudaError_t launch_trisolve_t(const TrisolveArgs& a, cudaStream_t s) {
   constexpr int NT = NP / 8;
-  const size_t smem = (size_t)((BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * (NP + 4)) * sizeof(double);
+  const size_t smem =
+      (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * (NP + 4)) * sizeof(double);
   auto k = trisolve_kernel<NP, MG, WPC, BSMEM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + 8 * MG - 1) / (8 * MG);
   long long grid = (groups + WPC - 1) / WPC;
-  const long long cap = (long long)a.num_sms * 1;
-  if (grid > cap) grid = cap;
+  if (grid > a.num_sms) grid = a.num_sms;
   if (grid < 1) grid = 1;
   k<<<(unsigned)grid, WPC * 32, smem, s>>>(a.in, a.ldi, a.out, a.ldo, a.m, a.n, a.bpack, a.dpack, a.sgn, a.vec16,
                                            a.status);
@@ -209,7 +255,7 @@ int trisolve_np(int n) {
 size_t trisolve_pack_doubles(int n) {
   const int np = trisolve_np(n);
   const int nt = np / 8;
-  return (size_t)nt * (nt - 1) * 32 + (size_t)nt * 64 + 64;
+  return (size_t)nt * (nt - 1) * 32 + (size_t)nt * kDiagStride + 8;
 }
 
 cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int degenerate, DevStatus* st,
@@ -218,11 +264,15 @@ cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int deg
   const int nt = np / 8;
   double* bpack = pack;
   double* dpack = pack + (size_t)nt * (nt - 1) * 32;
-  const long long total = (long long)nt * (nt - 1) * 32 + (long long)nt * 64;
+  int* bad = reinterpret_cast<int*>(dpack + (size_t)nt * kDiagStride);
+  const long long total = (long long)nt * (nt - 1) * 32 + (long long)nt * kDiagStride;
   long long g0 = (total + 255) / 256;
-  int grid = (int)(g0 < 1024 ? g0 : 1024);
+  int grid = (int)(g0 < 512 ? g0 : 512);
   if (grid < 1) grid = 1;
-  pack_r_kernel<<<grid, 256, 0, s>>>(r, ldr, n, np, bpack, dpack, degenerate, st);
+  cudaError_t e = cudaMemsetAsync(bad, 0x7f, sizeof(int), s);  // 0x7f7f7f7f > any n
+  if (e != cudaSuccess) return e;
+  pack_r_kernel<<<grid, 256, 0, s>>>(r, ldr, n, np, bpack, dpack, bad, degenerate, st);
+  pack_status_kernel<<<1, 1, 0, s>>>(bad, n, st);
   return cudaGetLastError();
 }
 
@@ -237,8 +287,8 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
     case 32: return launch_trisolve_t<32, 2, 16, true>(a, s);
     case 64: return launch_trisolve_t<64, 2, 16, true>(a, s);
     case 128: return launch_trisolve_t<128, 2, 8, true>(a, s);
-    case 256: return launch_trisolve_t<256, 2, 6, false>(a, s);
-    case 512: return launch_trisolve_t<512, 1, 6, false>(a, s);
+    case 256: return launch_trisolve_t<256, 2, 5, false>(a, s);
+    case 512: return launch_trisolve_t<512, 1, 5, false>(a, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -69,7 +69,7 @@ def test_rng_gaussian_within_ulps():
 # ---------------- kernels -------------------------------------------------------------
 @pytest.mark.parametrize("m,n,seed", [(3, 3, 0), (50, 10, 7), (2500, 6, 11), (3000, 12, 2), (5000, 64, 3),
                                       (4113, 128, 4), (2048, 1, 5), (20000, 33, 6), (9000, 200, 7),
-                                      (3000, 300, 8)])
+                                      (3000, 300, 8), (33 * 1024 + 5, 16, 9), (70000, 64, 10), (16 * 1024, 24, 11)])
 def test_gram_bitwise(m, n, seed):
     a = o.gaussian_matrix(m, n, seed)
     g = G.gram(a)
@@ -106,6 +106,22 @@ def test_trisolve_bitwise(m, n, seed):
     a = o.gaussian_matrix(m, n, seed)
     r = o.qr_r_factor(o.gaussian_matrix(2 * n + 3, n, seed + 100))
     assert np.array_equal(G.right_trisolve(a, r), o.right_trisolve(a, r))
+
+
+def test_trisolve_division_is_correctly_rounded():
+    # diagonal R: x = a / d elementwise, so the device's reciprocal + Markstein
+    # division must equal numpy's IEEE division bit for bit
+    rng = np.random.default_rng(5)
+    for n in (8, 64, 128):
+        a = rng.standard_normal((4096, n)) * 10.0 ** rng.integers(-30, 30, size=(4096, n))
+        a[::17, 0] = 0.0
+        a[::19, 1] = -0.0
+        d = rng.standard_normal(n) * 10.0 ** rng.integers(-20, 20, size=n)
+        d[0] = 3.0
+        d[1] = -1e-310  # subnormal divisor: IEEE fallback
+        x = G.right_trisolve(a, np.diag(d))
+        ref = a / d
+        assert np.array_equal(x.view(np.int64), ref.view(np.int64))
 
 
 def test_trisolve_identity_and_singular():
