@@ -154,8 +154,11 @@ Mat sample_rows_uniform(const Mat& a, Index l, bool without, Stream& s, std::vec
 // sketch.cpp:94-116. Omega(i, j) = gaussian_at(seed, i*m + j), generated in
 // 2048-column chunks; fixed order: for each chunk, t(i,c) = fma-chain over the
 // chunk's rows in ascending order starting from 0, then a1(i,c) += t(i,c).
-Mat sketch_gaussian(const Mat& a, Index l, uint64_t seed) {
+Mat sketch_gaussian(const Mat& a, Index l, uint64_t seed, Index m_global = -1, Index row0 = 0) {
+  // m_global/row0: a row block of a larger matrix (counters use global rows,
+  // the decomposition the multi-GPU path relies on)
   const Index m = a.rows, n = a.cols;
+  const Index mg = m_global < 0 ? m : m_global;
   Mat a1(l, n);
   constexpr Index kChunk = 2048;
   std::vector<double> omega(static_cast<size_t>(l * std::min(m, kChunk)));
@@ -164,7 +167,7 @@ Mat sketch_gaussian(const Mat& a, Index l, uint64_t seed) {
     const Index len = std::min(m - j0, kChunk);
     for (Index i = 0; i < l; ++i)
       for (Index jj = 0; jj < len; ++jj)
-        omega[static_cast<size_t>(i * len + jj)] = gaussian_at(seed, static_cast<uint64_t>(i * m + j0 + jj));
+        omega[static_cast<size_t>(i * len + jj)] = gaussian_at(seed, static_cast<uint64_t>(i * mg + row0 + j0 + jj));
     for (Index i = 0; i < l; ++i) {
       std::fill(t.begin(), t.end(), 0.0);
       const double* om = omega.data() + i * len;
@@ -993,6 +996,11 @@ int orc_sample_rows_uniform(const double* a, int64_t m, int64_t n, int64_t lda, 
 int orc_sketch_gaussian(const double* a, int64_t m, int64_t n, int64_t lda, int64_t l, uint64_t seed,
                         double* a1) {
   return guarded([&] { store(sketch_gaussian(from_strided(a, m, n, lda), l, seed), a1); });
+}
+
+int orc_sketch_gaussian_shard(const double* a, int64_t m_local, int64_t m_global, int64_t row0, int64_t n,
+                              int64_t l, uint64_t seed, double* a1) {
+  return guarded([&] { store(sketch_gaussian(from_strided(a, m_local, n, n), l, seed, m_global, row0), a1); });
 }
 
 int orc_gram(const double* x, int64_t m, int64_t n, int64_t ldx, int workers, double* g) {

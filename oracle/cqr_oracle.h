@@ -49,6 +49,9 @@ int orc_sample_rows_uniform(const double* a, int64_t m, int64_t n, int64_t lda, 
                             uint64_t seed, int without_replacement, double* a1, int64_t* idx);
 int orc_sketch_gaussian(const double* a, int64_t m, int64_t n, int64_t lda, int64_t l,
                         uint64_t seed, double* a1);
+/* the same for rows [row0, row0+m_local) of an m_global-row matrix (global counters) */
+int orc_sketch_gaussian_shard(const double* a, int64_t m_local, int64_t m_global, int64_t row0, int64_t n,
+                              int64_t l, uint64_t seed, double* a1);
 
 /* kernels.hpp (status codes as cqr_status) */
 int orc_gram(const double* x, int64_t m, int64_t n, int64_t ldx, int workers, double* g);

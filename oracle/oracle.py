@@ -43,6 +43,7 @@ def lib():
             "orc_resolved_size": (i64, [P(_abi.SketchCfg), i64, i64]),
             "orc_sample_rows_uniform": (i32, [pd, i64, i64, i64, i64, u64, i32, pd, pi64]),
             "orc_sketch_gaussian": (i32, [pd, i64, i64, i64, i64, u64, pd]),
+            "orc_sketch_gaussian_shard": (i32, [pd, i64, i64, i64, i64, i64, u64, pd]),
             "orc_gram": (i32, [pd, i64, i64, i64, i32, pd]),
             "orc_gram_tree_combine": (None, [pd, i64, i64, pd]),
             "orc_gram_stack_combine": (None, [pd, i64, i64, pd]),
@@ -163,6 +164,14 @@ def sketch_gaussian(a, l, seed):
     m, n = a.shape
     a1 = np.empty((l, n))
     _check(lib().orc_sketch_gaussian(_pd(a), m, n, n, l, seed, _pd(a1)))
+    return a1
+
+
+def sketch_gaussian_shard(a_local, m_global, row0, l, seed):
+    a = _f64(a_local)
+    m, n = a.shape
+    a1 = np.empty((l, n))
+    _check(lib().orc_sketch_gaussian_shard(_pd(a), m, m_global, row0, n, l, seed, _pd(a1)))
     return a1
 
 
