@@ -29,6 +29,7 @@ struct TrisolveArgs {
   int vec16;
   int num_sms;
   const DevStatus* status;
+  int variant = 0;  // 0: right-looking register kernel (n <= 256), 1: left-looking smem panel
 };
 cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s);
 

@@ -34,7 +34,10 @@ namespace {
 //   dpack[J*80 + kk*8 + j]          =  R[8J+kk][8J+j]                       (8x8 diag block)
 //   dpack[J*80 + 64 + j]            =  RN(1 / R[8J+j][8J+j])
 //   dpack[J*80 + 72 + j]            =  1 if the fast division is safe for column j
-constexpr int kDiagStride = 80;
+//   dpack[J*80 + 80]                =  1 if the block's strict upper part has no zero and
+//                                      all its divisions are safe (uniform fast path)
+// (per-block stride kDiagStride = 88)
+constexpr int kDiagStride = 88;
 
 __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int np, double* __restrict__ bpack,
                               double* __restrict__ dpack, int* __restrict__ bad_min, int degenerate,
@@ -63,6 +66,17 @@ __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int 
       double v;
       if (w < 64) {
         v = R(8 * J + w / 8, 8 * J + w % 8);
+      } else if (w >= 80) {
+        v = 0.0;
+        if (w == 80) {
+          bool ok = true;
+          for (int a = 0; a < 8; ++a) {
+            const double da = fabs(R(8 * J + a, 8 * J + a));
+            ok = ok && da >= 0x1p-500 && da <= 0x1p+500;
+            for (int b = a + 1; b < 8; ++b) ok = ok && R(8 * J + a, 8 * J + b) != 0.0;
+          }
+          v = ok ? 1.0 : 0.0;
+        }
       } else {
         const int j = 8 * J + (w - 64) % 8;
         const double dj = R(j, j);
@@ -223,6 +237,210 @@ __global__ void __launch_bounds__(WPC * 32) trisolve_kernel(const double* in, lo
   }
 }
 
+// Super-block kernel (the default). A warp owns 32 rows (4 DMMA row groups;
+// one lane per row in the scalar part, so all 32 lanes work). Columns go in
+// passes of 64 (8 blocks of 8), the pass held in DMMA accumulator registers:
+//  1. left-looking: contributions of all columns solved in earlier passes,
+//     k ascending, A fragments re-read from the output (this warp's own rows,
+//     L2-resident; column signs, when fused, are undone exactly by a second
+//     multiplication by +-1), 32 independent accumulator chains per step;
+//  2. right-looking inside the pass: block J solved one lane per row (scalar fma
+//     + correctly rounded division), then its 8 columns update the pass's later
+//     blocks with DMMA; the 8-block window rotates so the loop is not unrolled.
+// Every element therefore receives k = 0, 1, ..., j-1 in ascending order, the
+// in-block terms last, then the division: the reference recurrence exactly.
+__device__ __forceinline__ bool div_exponent_ok(double y) {
+  const unsigned e = ((unsigned)__double2hiint(y) >> 20) & 0x7ffu;  // |y| in [2^-899, 2^900]
+  return e - 124u < 1800u;
+}
+
+template <int NP, int WPC, bool BSMEM>
+__global__ void __launch_bounds__(WPC * 32, 1)
+    trisolve_sb_kernel(const double* in, long long ldi, double* out, long long ldo, long long m, int n,
+                       const double* __restrict__ bpack, const double* __restrict__ dpack,
+                       const double* __restrict__ sgn, int vec16, const DevStatus* st) {
+  constexpr int NT = NP / 8;
+  constexpr int MG = 4, RW = 32, W = NT < 8 ? NT : 8;  // window (blocks per pass)
+  constexpr int NPASS = NT / W;
+  constexpr int NB = BSMEM ? NT * (NT - 1) * 32 : 0;
+  constexpr int ND = NT * kDiagStride;
+  constexpr int LDS_ = 8 + 2;
+  extern __shared__ __align__(16) double smem[];
+  if (failed(st)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 3, gr = lane >> 2;
+  double* sD = smem;
+  const double* sB = bpack;
+  double* sS = smem + ND + NB + warp * RW * LDS_;
+  for (int e = threadIdx.x; e < ND; e += WPC * 32) sD[e] = dpack[e];
+  if constexpr (BSMEM) {
+    for (int e = threadIdx.x; e < NB; e += WPC * 32) smem[ND + e] = bpack[e];
+    sB = smem + ND;
+  }
+  __syncthreads();
+  const long long groups = (m + RW - 1) / RW;
+  for (long long grp = (long long)blockIdx.x * WPC + warp; grp < groups; grp += (long long)gridDim.x * WPC) {
+    const long long row0 = grp * RW;
+    const int rows = (int)min((long long)RW, m - row0);
+#pragma unroll 1
+    for (int P = 0; P < NPASS; ++P) {
+      const int c0 = 8 * W * P;
+      double acc[MG][W][2];
+#pragma unroll
+      for (int g = 0; g < MG; ++g) {
+        const int r = g * 8 + gr;
+        const double* src = in + (row0 + r) * ldi + c0 + 2 * q;
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+          const int c = c0 + 8 * t + 2 * q;
+          if (r < rows && vec16 && c + 1 < n) {
+            const double2 v = *reinterpret_cast<const double2*>(src + 8 * t);
+            acc[g][t][0] = v.x;
+            acc[g][t][1] = v.y;
+          } else {
+            acc[g][t][0] = (r < rows && c < n) ? src[8 * t] : 0.0;
+            acc[g][t][1] = (r < rows && c + 1 < n) ? src[8 * t + 1] : 0.0;
+          }
+        }
+      }
+      // 1. left-looking: k in [0, c0), ascending
+      if (P > 0) {
+        const double* xrow[MG];
+#pragma unroll
+        for (int g = 0; g < MG; ++g) {
+          const int r = min(g * 8 + gr, rows - 1);
+          xrow[g] = out + (row0 + r) * ldo + q;
+        }
+#pragma unroll 2
+        for (int k4 = 0; k4 < c0 / 4; ++k4) {
+          double af[MG];
+          const double s = sgn ? sgn[4 * k4 + q] : 1.0;
+#pragma unroll
+          for (int g = 0; g < MG; ++g) af[g] = xrow[g][4 * k4] * s;
+#pragma unroll
+          for (int t = 0; t < W; ++t) {
+            const int JJ = 8 * P + t;
+            const int bi = (JJ * (JJ - 1) + k4) * 32 + lane;
+            const double b = BSMEM ? sB[bi] : __ldg(sB + bi);
+#pragma unroll
+            for (int g = 0; g < MG; ++g) dmma(acc[g][t][0], acc[g][t][1], af[g], b);
+          }
+        }
+      }
+      // 2. right-looking inside the pass
+#pragma unroll 1
+      for (int Jl = 0; Jl < W; ++Jl) {
+        const int J = W * P + Jl;
+#pragma unroll
+        for (int g = 0; g < MG; ++g)
+          *reinterpret_cast<double2*>(sS + (g * 8 + gr) * LDS_ + 2 * q) = make_double2(acc[g][0][0], acc[g][0][1]);
+        __syncwarp();
+        {
+          double* xr = sS + lane * LDS_;
+          double y[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double2 v = *reinterpret_cast<const double2*>(xr + 2 * u);
+            y[2 * u] = v.x;
+            y[2 * u + 1] = v.y;
+          }
+          const double* D = sD + J * kDiagStride;
+          if (D[80] != 0.0) {  // no zero in the block's strict upper part, divisors safe (uniform)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+#pragma unroll
+              for (int kk = 0; kk < j; ++kk) y[j] = fma(-D[kk * 8 + j], y[kk], y[j]);
+              const double d = D[j * 8 + j], inv = D[64 + j];
+              const double yy = y[j];
+              if (div_exponent_ok(yy)) {
+                const double q0 = yy * inv;
+                double rr = fma(-q0, d, yy);
+                const double q1 = fma(rr, inv, q0);
+                rr = fma(-q1, d, yy);
+                y[j] = fma(rr, inv, q1);
+              } else {
+                y[j] = (yy == 0.0) ? yy * inv : yy / d;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+#pragma unroll
+              for (int kk = 0; kk < j; ++kk) {
+                const double rr = D[kk * 8 + j];
+                if (rr != 0.0) y[j] = fma(-rr, y[kk], y[j]);
+              }
+              y[j] = fast_div(y[j], D[j * 8 + j], D[64 + j], D[72 + j] != 0.0);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(xr + 2 * u) = make_double2(y[2 * u], y[2 * u + 1]);
+          if (lane < rows) {
+            double* o = out + (row0 + lane) * ldo + 8 * J;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int c = 8 * J + 2 * u;
+              double v0 = y[2 * u], v1 = y[2 * u + 1];
+              if (sgn) {
+                if (c < n) v0 *= sgn[c];
+                if (c + 1 < n) v1 *= sgn[c + 1];
+              }
+              if (vec16 && c + 1 < n) {
+                *reinterpret_cast<double2*>(o + 2 * u) = make_double2(v0, v1);
+              } else {
+                if (c < n) o[2 * u] = v0;
+                if (c + 1 < n) o[2 * u + 1] = v1;
+              }
+            }
+          }
+        }
+        __syncwarp();
+        double af[MG][2];
+#pragma unroll
+        for (int g = 0; g < MG; ++g)
+#pragma unroll
+          for (int kk4 = 0; kk4 < 2; ++kk4) af[g][kk4] = sS[(g * 8 + gr) * LDS_ + 4 * kk4 + q];
+        const double* bcol = sB + (2 * J) * 32 + lane;
+#pragma unroll
+        for (int t = 1; t < W; ++t) {
+          if (Jl + t < W) {
+            const int JJ = J + t;
+            const double* bp = bcol + (JJ * (JJ - 1)) * 32;
+#pragma unroll
+            for (int kk4 = 0; kk4 < 2; ++kk4) {
+              const double b = BSMEM ? bp[kk4 * 32] : __ldg(bp + kk4 * 32);
+#pragma unroll
+              for (int g = 0; g < MG; ++g) dmma(acc[g][t][0], acc[g][t][1], af[g][kk4], b);
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < MG; ++g) {
+            acc[g][t - 1][0] = acc[g][t][0];
+            acc[g][t - 1][1] = acc[g][t][1];
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+template <int NP, int WPC, bool BSMEM>
+cudaError_t launch_trisolve_sb_t(const TrisolveArgs& a, cudaStream_t s) {
+  constexpr int NT = NP / 8;
+  const size_t smem = (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 32 * 10) * sizeof(double);
+  auto k = trisolve_sb_kernel<NP, WPC, BSMEM>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long groups = (a.m + 31) / 32;
+  long long grid = (groups + WPC - 1) / WPC;
+  if (grid > (long long)a.num_sms) grid = a.num_sms;
+  if (grid < 1) grid = 1;
+  k<<<(unsigned)grid, WPC * 32, smem, s>>>(a.in, a.ldi, a.out, a.ldo, a.m, a.n, a.bpack, a.dpack, a.sgn, a.vec16,
+                                           a.status);
+  return cudaGetLastError();
+}
+
 template <int NP, int MG, int WPC, bool BSMEM>
 cudaError_t launch_trisolve_t(const TrisolveArgs& a, cudaStream_t s) {
   constexpr int NT = NP / 8;
@@ -281,14 +499,24 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   const int nt = np / 8;
   a.bpack = a.pack;
   a.dpack = a.pack + (size_t)nt * (nt - 1) * 32;
+  if (a.variant == 1) {  // left-looking (smem panel), kept for comparison and n = 512
+    switch (np) {
+      case 8: return launch_trisolve_t<8, 2, 16, true>(a, s);
+      case 16: return launch_trisolve_t<16, 2, 16, true>(a, s);
+      case 32: return launch_trisolve_t<32, 2, 16, true>(a, s);
+      case 64: return launch_trisolve_t<64, 2, 16, true>(a, s);
+      case 128: return launch_trisolve_t<128, 2, 8, true>(a, s);
+      case 256: return launch_trisolve_t<256, 2, 5, false>(a, s);
+    }
+  }
   switch (np) {
-    case 8: return launch_trisolve_t<8, 2, 16, true>(a, s);
-    case 16: return launch_trisolve_t<16, 2, 16, true>(a, s);
-    case 32: return launch_trisolve_t<32, 2, 16, true>(a, s);
-    case 64: return launch_trisolve_t<64, 2, 16, true>(a, s);
-    case 128: return launch_trisolve_t<128, 2, 8, true>(a, s);
-    case 256: return launch_trisolve_t<256, 2, 5, false>(a, s);
-    case 512: return launch_trisolve_t<512, 1, 5, false>(a, s);
+    case 8: return launch_trisolve_sb_t<8, 12, true>(a, s);
+    case 16: return launch_trisolve_sb_t<16, 12, true>(a, s);
+    case 32: return launch_trisolve_sb_t<32, 12, true>(a, s);
+    case 64: return launch_trisolve_sb_t<64, 12, true>(a, s);
+    case 128: return launch_trisolve_sb_t<128, 12, true>(a, s);
+    case 256: return launch_trisolve_sb_t<256, 8, false>(a, s);
+    case 512: return launch_trisolve_sb_t<512, 8, false>(a, s);
   }
   return cudaErrorInvalidValue;
 }
