@@ -14,7 +14,11 @@
 // Algorithmic work: 2*l*m*n flops + l*m Gaussian draws; HBM: 8*m*n bytes of A
 // (each A row is read by l/ST CTAs that run together, the repeats hit L2).
 
+#include <cmath>
+#include <mutex>
+
 #include "common.cuh"
+#include "boxmuller.cuh"
 #include "kernels.h"
 
 namespace cqr {
@@ -35,40 +39,52 @@ int sketch_np(int n) {
   return 512;
 }
 
-// Generate Omega[s0 .. s0+ST) x [kb .. kb+KS) (kb = global row index) into
-// sOm (row stride KS+4). Rows of Omega at or beyond l are zero.
-__device__ __forceinline__ void gen_omega(double* sOm, int s0, int l, long long m_global, long long kb,
-                                          uint64_t seed, int tid) {
-  constexpr int PPR = kKS / 2 + 1;  // pair slots per Omega row
-  for (int e = tid; e < kST * PPR; e += kThreads) {
-    const int i = e / PPR, pp = e - i * PPR;
-    double* row = sOm + i * (kKS + 4);
-    if (s0 + i >= l) {
-      if (pp < kKS / 2) {
-        row[2 * pp] = 0.0;
-        row[2 * pp + 1] = 0.0;
-      }
-      continue;
-    }
+__constant__ BmTables c_bm;
+
+// Generate the Box-Muller pairs of Omega[s0 .. s0+ST) x [kb .. kb+KS) (kb =
+// global row index of A) into sOm (row stride KS+4). Straight-line code:
+// invalid slots compute a clamped pair and skip the (predicated) stores; Omega
+// rows at or beyond l are zero. ALIGNED: every row's counter range starts
+// even (m_global and kb even), so a row is exactly KS/2 pairs.
+template <bool ALIGNED>
+__device__ __forceinline__ void gen_pair_slot(const BmTables& T, double* sOm, int s0, int l, long long m_global,
+                                              long long kb, uint64_t seed, int e) {
+  constexpr int LDO = kKS + 4;
+  if (ALIGNED) {
+    const int i = e >> 4, pp = e & 15;
+    const unsigned long long c_lo = (unsigned long long)(s0 + i) * (unsigned long long)m_global + kb;
+    double ge, go;
+    gaussian_pair_fast(T, seed, (c_lo >> 1) + pp, ge, go);
+    const bool live = s0 + i < l;
+    *reinterpret_cast<double2*>(sOm + i * LDO + 2 * pp) = make_double2(live ? ge : 0.0, live ? go : 0.0);
+  } else {
+    constexpr int PPR = kKS / 2 + 1;
+    const bool valid = e < kST * PPR;
+    const int ee = valid ? e : 0;
+    const int i = ee / PPR, pp = ee - i * PPR;
     const unsigned long long c_lo = (unsigned long long)(s0 + i) * (unsigned long long)m_global + kb;
     const unsigned long long p = (c_lo >> 1) + pp;
-    if (p > ((c_lo + kKS - 1) >> 1)) continue;
     double ge, go;
-    gaussian_pair(seed, p, ge, go);
+    gaussian_pair_fast(T, seed, p, ge, go);
+    const bool live = s0 + i < l;
     const long long ce = (long long)(2 * p - c_lo);
-    if (ce >= 0 && ce < kKS) row[ce] = ge;
-    if (ce + 1 >= 0 && ce + 1 < kKS) row[ce + 1] = go;
+    double* row = sOm + i * LDO;
+    if (valid && ce >= 0 && ce < kKS) row[ce] = live ? ge : 0.0;
+    if (valid && ce + 1 >= 0 && ce + 1 < kKS) row[ce + 1] = live ? go : 0.0;
   }
 }
 
 // NP = columns handled by one CTA (<= 128); wider A is split over gridDim.z
-// column parts of NP, each regenerating the same Omega tile.
-template <int NP>
-__global__ void __launch_bounds__(kThreads) sketch_kernel(const double* __restrict__ a, long long lda,
-                                                          long long m_local, long long m_global, long long row0,
-                                                          int n, int l, uint64_t seed, long long rows_per_chunk,
-                                                          double* __restrict__ partial, int lp, int np_total,
-                                                          int vec16, const DevStatus* st) {
+// column parts of NP, each regenerating the same Omega tile. Per 32-row step:
+// one barrier; the DMMAs of step i are interleaved (same basic block) with the
+// Box-Muller draws of step i+1 into the other Omega buffer, and the A rows of
+// step i+1 stream in by cp.async meanwhile.
+template <int NP, bool ALIGNED>
+__global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __restrict__ a, long long lda,
+                                                             long long m_local, long long m_global, long long row0,
+                                                             int n, int l, uint64_t seed, long long rows_per_chunk,
+                                                             double* __restrict__ partial, int lp, int np_total,
+                                                             int vec16, const DevStatus* st) {
   constexpr int NT = NP / 8;
   constexpr int WN = NT < 8 ? NT : 8;  // warps along n
   constexpr int WM = 8 / WN;           // warps along Omega rows
@@ -76,10 +92,15 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const double* __restri
   constexpr int NG = NT / WN;          // 8-col groups per warp
   constexpr int LDA = NP + 4;
   constexpr int LDO = kKS + 4;
+  constexpr int SLOTS = ALIGNED ? kST * kKS / 2 : kST * (kKS / 2 + 1);
+  constexpr int PER = (SLOTS + kThreads - 1) / kThreads;  // pair slots per thread per step
+  constexpr int K4 = kKS / 4;
   extern __shared__ __align__(16) double smem[];
   if (failed(st)) return;
-  double* sOm = smem;
-  double* sA[2] = {smem + kST * LDO, smem + kST * LDO + kKS * LDA};
+  BmTables& T = *reinterpret_cast<BmTables*>(smem);
+  double* base = smem + sizeof(BmTables) / sizeof(double);
+  double* sOm[2] = {base, base + kST * LDO};
+  double* sA[2] = {base + 2 * kST * LDO, base + 2 * kST * LDO + kKS * LDA};
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = lane & 3, gr = lane >> 2;
   const int wm = warp / WN, wn = warp - (warp / WN) * WN;
@@ -89,48 +110,56 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const double* __restri
   n = min(NP, n - col0);
   const long long k_begin = (long long)blockIdx.y * rows_per_chunk;
   const long long k_end = min(m_local, k_begin + rows_per_chunk);
-
+  {
+    const double* src = reinterpret_cast<const double*>(&c_bm);
+    double* dst = reinterpret_cast<double*>(&T);
+    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += kThreads) dst[e] = src[e];
+  }
   double acc[MG][NG][2];
 #pragma unroll
   for (int g = 0; g < MG; ++g)
 #pragma unroll
     for (int h = 0; h < NG; ++h) acc[g][h][0] = acc[g][h][1] = 0.0;
-
   const int nsteps = k_end > k_begin ? (int)((k_end - k_begin + kKS - 1) / kKS) : 0;
   if (nsteps > 0) {
     stage_rows(sA[0], LDA, a + k_begin * lda, lda, (int)min((long long)kKS, k_end - k_begin), kKS, n, NP, tid,
                kThreads, vec16 != 0);
     cp_async_commit();
+    __syncthreads();  // tables
+#pragma unroll
+    for (int u = 0; u < PER; ++u)
+      gen_pair_slot<ALIGNED>(T, sOm[0], s0, l, m_global, row0 + k_begin, seed, tid + kThreads * u);
   }
   for (int st_i = 0; st_i < nsteps; ++st_i) {
     const long long kb = k_begin + (long long)st_i * kKS;
+    cp_async_wait<0>();
+    __syncthreads();
     if (st_i + 1 < nsteps) {
       const long long kn = kb + kKS;
-      stage_rows(sA[(st_i + 1) & 1], LDA, a + kn * lda, lda, (int)min((long long)kKS, k_end - kn), kKS, n, NP,
-                 tid, kThreads, vec16 != 0);
+      stage_rows(sA[(st_i + 1) & 1], LDA, a + kn * lda, lda, (int)min((long long)kKS, k_end - kn), kKS, n, NP, tid,
+                 kThreads, vec16 != 0);
       cp_async_commit();
     }
-    gen_omega(sOm, s0, l, m_global, row0 + kb, seed, tid);
-    if (st_i + 1 < nsteps)
-      cp_async_wait<1>();
-    else
-      cp_async_wait<0>();
-    __syncthreads();
     const double* A = sA[st_i & 1];
-    const double* O = sOm + (wm * MG * 8 + gr) * LDO + q;
-#pragma unroll 2
-    for (int k4 = 0; k4 < kKS / 4; ++k4) {
-      double af[MG], bf[NG];
+    const double* O = sOm[st_i & 1] + (wm * MG * 8 + gr) * LDO + q;
+    double* On = sOm[(st_i + 1) & 1];
+    const long long kbn = row0 + kb + kKS;
 #pragma unroll
-      for (int g = 0; g < MG; ++g) af[g] = O[g * 8 * LDO + 4 * k4];
+    for (int u = 0; u < PER; ++u) {
+      gen_pair_slot<ALIGNED>(T, On, s0, l, m_global, kbn, seed, tid + kThreads * u);
 #pragma unroll
-      for (int h = 0; h < NG; ++h) bf[h] = A[(4 * k4 + q) * LDA + (wn * NG + h) * 8 + gr];
+      for (int k4 = u * K4 / PER; k4 < (u + 1) * K4 / PER; ++k4) {
+        double af[MG], bf[NG];
 #pragma unroll
-      for (int g = 0; g < MG; ++g)
+        for (int g = 0; g < MG; ++g) af[g] = O[g * 8 * LDO + 4 * k4];
 #pragma unroll
-        for (int h = 0; h < NG; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
+        for (int h = 0; h < NG; ++h) bf[h] = A[(4 * k4 + q) * LDA + (wn * NG + h) * 8 + gr];
+#pragma unroll
+        for (int g = 0; g < MG; ++g)
+#pragma unroll
+          for (int h = 0; h < NG; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
+      }
     }
-    __syncthreads();
   }
   // partial[chunk][s0 + i][col0 + col], lp rows per chunk, np_total columns
   double* out = partial + (long long)blockIdx.y * lp * np_total + col0;
@@ -183,21 +212,56 @@ __global__ void rng_bits_kernel(uint64_t seed, uint64_t k0, long long count, uin
     out[e] = bits_at(seed, k0 + (uint64_t)e);
 }
 
+// The same Box-Muller code as the sketch kernel (the parity tests compare it to glibc).
 __global__ void rng_gauss_kernel(uint64_t seed, uint64_t k0, long long count, double* out) {
+  __shared__ BmTables T;
+  {
+    const double* src = reinterpret_cast<const double*>(&c_bm);
+    double* dst = reinterpret_cast<double*>(&T);
+    for (int e = threadIdx.x; e < (int)(sizeof(BmTables) / sizeof(double)); e += blockDim.x) dst[e] = src[e];
+  }
+  __syncthreads();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count;
        e += (long long)gridDim.x * blockDim.x) {
     const uint64_t k = k0 + (uint64_t)e;
     double ge, go;
-    gaussian_pair(seed, k >> 1, ge, go);
+    gaussian_pair_fast(T, seed, k >> 1, ge, go);
     out[e] = (k & 1) ? go : ge;
   }
+}
+
+cudaError_t ensure_tables() {
+  static std::mutex mu;
+  static unsigned long long done = 0;  // bit per device
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (dev < 64 && (done >> dev) & 1ull) return cudaSuccess;
+  BmTables t;
+  bm_tables_host(&t);
+  e = cudaMemcpyToSymbol(c_bm, &t, sizeof(t));
+  if (e == cudaSuccess && dev < 64) done |= 1ull << dev;
+  return e;
 }
 
 template <int NP>
 cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
                             uint64_t seed, double* partial, int vec16, const DevStatus* st, cudaStream_t s) {
-  const size_t smem = (size_t)(kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
-  auto k = sketch_kernel<NP>;
+  cudaError_t e0 = ensure_tables();
+  if (e0 != cudaSuccess) return e0;
+  const size_t smem = sizeof(BmTables) + (size_t)(2 * kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
+  const bool aligned = (m_global % 2 == 0) && (row0 % 2 == 0) && (p.rows_per_chunk % 2 == 0);
+  if (!aligned) {
+    auto k = sketch_kernel<NP, false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)p.s_tiles, (unsigned)p.kchunks, (unsigned)(p.np / NP));
+    k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial,
+                                   p.lp, p.np, vec16, st);
+    return cudaGetLastError();
+  }
+  auto k = sketch_kernel<NP, true>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.s_tiles, (unsigned)p.kchunks, (unsigned)(p.np / NP));
@@ -207,6 +271,24 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
 }
 
 }  // namespace
+
+void bm_tables_host(BmTables* t) {
+  for (int i = 0; i < 128; ++i) {
+    long double c = 1.0L + ((long double)i + 0.5L) / 128.0L;
+    if (i >= 53) c *= 0.5L;
+    const double inv = (double)(1.0L / c);
+    const long double v = -logl((long double)inv);
+    t->inv[i] = inv;
+    t->lhi[i] = (double)v;
+    t->llo[i] = (double)(v - (long double)t->lhi[i]);
+  }
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < 66; ++k) {
+    const long double ang = two_pi * (long double)k / 64.0L;
+    t->s[k] = (double)sinl(ang);
+    t->c[k] = (double)cosl(ang);
+  }
+}
 
 SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms) {
   SketchPlan p;
@@ -270,6 +352,8 @@ cudaError_t launch_rng_bits(uint64_t seed, uint64_t k0, long long count, uint64_
 }
 
 cudaError_t launch_rng_gaussian(uint64_t seed, uint64_t k0, long long count, double* out, cudaStream_t s) {
+  cudaError_t e = ensure_tables();
+  if (e != cudaSuccess) return e;
   rng_gauss_kernel<<<256, 256, 0, s>>>(seed, k0, count, out);
   return cudaGetLastError();
 }

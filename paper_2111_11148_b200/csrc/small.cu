@@ -15,6 +15,8 @@
 //  triangular_product_kernel  engine.cpp:103-107 (fma chain over all k) -> bitwise.
 //  normalize_sign_kernel      engine.cpp:109-116 (R rows; Q columns via sgn).
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -98,23 +100,28 @@ __global__ void __launch_bounds__(kT) cholesky_kernel(const double* __restrict__
   }
 }
 
+// Rows [0, rs) of the working matrix live in shared memory, rows [rs, l) in the
+// L1-cached global workspace (c1: 200 of 256 rows in smem, the rest fits L1).
 __global__ void __launch_bounds__(kT) lu_kernel(const double* __restrict__ a1, int l, int n, double* __restrict__ u,
-                                                double* work, int use_smem, DevStatus* st) {
+                                                double* work, int rs, DevStatus* st) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double wb[32];
   __shared__ int wi[32];
   __shared__ int s_piv;
   if (failed(st)) return;
-  double* W = use_smem ? smem : work;
+  auto row = [&](int i) -> double* { return i < rs ? smem + (long long)i * n : work + (long long)i * n; };
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  for (long long e = tid; e < (long long)l * n; e += nt) W[e] = a1[e];
+  for (int i = warp; i < l; i += nw) {
+    double* ri = row(i);
+    for (int c = lane; c < n; c += 32) ri[c] = a1[(long long)i * n + c];
+  }
   __syncthreads();
   for (int j = 0; j < n; ++j) {
     // first maximum of |W(i, j)| over i >= j (kernels.hpp:226-234)
     double best = -1.0;
     int idx = 0x7fffffff;
     for (int i = j + tid; i < l; i += nt) {
-      const double v = fabs(W[(long long)i * n + j]);
+      const double v = fabs(row(i)[j]);
       if (v > best) {
         best = v;
         idx = i;
@@ -150,36 +157,38 @@ __global__ void __launch_bounds__(kT) lu_kernel(const double* __restrict__ a1, i
     }
     __syncthreads();
     const int piv = s_piv;
-    if (piv >= l || W[(long long)piv * n + j] == 0.0) {
+    if (piv >= l || row(piv)[j] == 0.0) {
       if (tid == 0) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, j);
       return;
     }
+    double* pj = row(j);
     if (piv != j) {
+      double* pp = row(piv);
       for (int c = tid; c < n; c += nt) {
-        const double t = W[(long long)j * n + c];
-        W[(long long)j * n + c] = W[(long long)piv * n + c];
-        W[(long long)piv * n + c] = t;
+        const double t = pj[c];
+        pj[c] = pp[c];
+        pp[c] = t;
       }
       __syncthreads();
     }
-    const double d = W[(long long)j * n + j];
-    for (int i = j + 1 + tid; i < l; i += nt) W[(long long)i * n + j] = W[(long long)i * n + j] / d;
+    const double d = pj[j];
+    for (int i = j + 1 + tid; i < l; i += nt) {
+      double* ri = row(i);
+      ri[j] = ri[j] / d;
+    }
     __syncthreads();
-    if (j + 1 < n) {
-      const double* pr = W + (long long)j * n;
-      // warps over rows, lanes over columns (coalesced), no integer division
-      for (int i = j + 1 + warp; i < l; i += nw) {
-        double* Wi = W + (long long)i * n;
-        const double mult = Wi[j];
-        if (mult != 0.0)
-          for (int c = j + 1 + lane; c < n; c += 32) Wi[c] = fma(-mult, pr[c], Wi[c]);
-      }
+    // trailing update: one warp per row, lanes over columns
+    for (int i = j + 1 + warp; i < l; i += nw) {
+      double* ri = row(i);
+      const double mult = ri[j];
+      if (mult != 0.0)
+        for (int c = j + 1 + lane; c < n; c += 32) ri[c] = fma(-mult, pj[c], ri[c]);
     }
     __syncthreads();
   }
-  for (int e = tid; e < n * n; e += nt) {
-    const int i = e / n, c = e % n;
-    u[e] = c >= i ? W[e] : 0.0;
+  for (int i = warp; i < n; i += nw) {
+    const double* ri = row(i);
+    for (int c = lane; c < n; c += 32) u[(long long)i * n + c] = c >= i ? ri[c] : 0.0;
   }
 }
 
@@ -327,9 +336,12 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
 }
 
 cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
-  const size_t bytes = (size_t)l * n * sizeof(double);
-  const int use_smem = bytes <= kSmemCap;
-  return launch_small(lu_kernel, bytes, s, a1, l, n, u, work, use_smem, st);
+  const int rs = (int)std::min<size_t>((size_t)l, kSmemCap / ((size_t)n * sizeof(double)));
+  const size_t smem = (size_t)rs * n * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+  if (e != cudaSuccess) return e;
+  lu_kernel<<<1, kT, smem, s>>>(a1, l, n, u, work, rs, st);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work, DevStatus* st, cudaStream_t s) {
