@@ -101,7 +101,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_input(m_local, n, rank, world, device):
+def make_input(m_local, n, rank, world, device, kappa=None):
     """A_local = U_local diag(sigma) V^T / sqrt(world): every rank's U block is
     orthonormal, so the stacked U has orthogonal columns of norm sqrt(world)."""
     import numpy as np
@@ -114,7 +114,7 @@ def make_input(m_local, n, rank, world, device):
     del x
     rs = np.random.default_rng(SEED)
     v, _ = np.linalg.qr(rs.standard_normal((n, n)))
-    sigma = KAPPA ** (-np.arange(n) / (n - 1))
+    sigma = (KAPPA if kappa is None else kappa) ** (-np.arange(n) / (n - 1))
     svt = torch.as_tensor((sigma[:, None] * v.T) / np.sqrt(world), device=device)
     a = u @ svt
     del u

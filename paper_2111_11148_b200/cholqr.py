@@ -33,7 +33,7 @@ import numpy as np
 from . import _abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcqr.so")
+LIB_PATH = os.environ.get("CQR_LIB") or os.path.join(_HERE, "libcqr.so")
 
 # ---- errors (errors.hpp) ------------------------------------------------------------
 

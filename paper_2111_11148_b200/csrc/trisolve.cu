@@ -254,7 +254,7 @@ __device__ __forceinline__ bool div_exponent_ok(double y) {
   return e - 124u < 1800u;
 }
 
-template <int NP, int WPC, bool BSMEM>
+template <int NP, int WPC, bool BSMEM, bool SGN>
 __global__ void __launch_bounds__(WPC * 32, 1)
     trisolve_sb_kernel(const double* in, long long ldi, double* out, long long ldo, long long m, int n,
                        const double* __restrict__ bpack, const double* __restrict__ dpack,
@@ -314,9 +314,13 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 #pragma unroll 2
         for (int k4 = 0; k4 < c0 / 4; ++k4) {
           double af[MG];
-          const double s = sgn ? sgn[4 * k4 + q] : 1.0;
 #pragma unroll
-          for (int g = 0; g < MG; ++g) af[g] = xrow[g][4 * k4] * s;
+          for (int g = 0; g < MG; ++g) af[g] = xrow[g][4 * k4];
+          if constexpr (SGN) {
+            const double s = sgn[4 * k4 + q];
+#pragma unroll
+            for (int g = 0; g < MG; ++g) af[g] *= s;
+          }
 #pragma unroll
           for (int t = 0; t < W; ++t) {
             const int JJ = 8 * P + t;
@@ -381,7 +385,7 @@ __global__ void __launch_bounds__(WPC * 32, 1)
             for (int u = 0; u < 4; ++u) {
               const int c = 8 * J + 2 * u;
               double v0 = y[2 * u], v1 = y[2 * u + 1];
-              if (sgn) {
+              if constexpr (SGN) {
                 if (c < n) v0 *= sgn[c];
                 if (c + 1 < n) v1 *= sgn[c + 1];
               }
@@ -429,7 +433,7 @@ template <int NP, int WPC, bool BSMEM>
 cudaError_t launch_trisolve_sb_t(const TrisolveArgs& a, cudaStream_t s) {
   constexpr int NT = NP / 8;
   const size_t smem = (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 32 * 10) * sizeof(double);
-  auto k = trisolve_sb_kernel<NP, WPC, BSMEM>;
+  auto k = a.sgn ? trisolve_sb_kernel<NP, WPC, BSMEM, true> : trisolve_sb_kernel<NP, WPC, BSMEM, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + 31) / 32;

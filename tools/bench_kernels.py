@@ -14,7 +14,7 @@ m = int(os.environ.get("PROF_M", bench.M_PER_GPU))
 n = int(os.environ.get("PROF_N", bench.N))
 methods = os.environ.get("PROF_METHODS", "rlu").split(",")
 dev = torch.device("cuda", 0)
-a = bench.make_input(m, n, 0, 1, dev)
+a = bench.make_input(m, n, 0, 1, dev, float(os.environ.get("PROF_KAPPA", bench.KAPPA)))
 ctx = dist.make_context(0, 0, 1)
 cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=2.0, seed=bench._seed_value())
 q = torch.empty_like(a)
