@@ -27,6 +27,15 @@ struct DevStatus {
 __device__ __forceinline__ void set_status(DevStatus* st, int code, long long index) {
   if (atomicCAS(&st->code, 0, code) == 0) st->index = index;
 }
+// Non-finite input (engine.cpp:222) outranks any numerical failure: the check
+// is fused into the first kernel that reads all of A.
+__device__ __forceinline__ void set_status_invalid(DevStatus* st) {
+  atomicExch(&st->code, 3 /*CQR_INVALID_ARGUMENT*/);
+  st->index = -1;
+}
+__device__ __forceinline__ bool nonfinite(double v) {
+  return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
+}
 __device__ __forceinline__ bool failed(const DevStatus* st) {
   return st != nullptr && *(volatile const int*)&st->code != 0;
 }

@@ -240,6 +240,7 @@ struct Job {
   cqr_options opts;
   cqr_precond_fn precond = nullptr;
   void* user = nullptr;
+  int check_first = 0;  // fuse the non-finite check into the first tall kernel
 };
 
 void allreduce(cqr_ctx* c, double* p, size_t count) {
@@ -248,7 +249,7 @@ void allreduce(cqr_ctx* c, double* p, size_t count) {
 }
 
 // Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
-void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g) {
+void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g, int check = 0) {
   cqr::GramPlan p = cqr::gram_plan(m, n);
   double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.workspace_doubles, 1));
   int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
@@ -261,7 +262,8 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
     c->tiles_key = key;
   }
   if (m > 0) {
-    LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, c->status, c->stream));
+    LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
+                                      c->stream));
     LAUNCH(c, cqr::launch_gram_combine(p, part, g, c->world <= 1 ? 1 : 0, c->status, c->stream));
     ++c->launches;
   } else {
@@ -319,13 +321,14 @@ void check_finite(cqr_ctx* c, const double* a, long long m, int n, long long lda
 // One CholeskyQR pass (engine.cpp:78-92): G = X^T X (+shift I), R = chol(G),
 // X <- X R^{-1} (in -> out). shift_mode 0/1/2 as launch_cholesky.
 void cholesky_pass(Job& j, const double* in, long long ldi, Report& rep, double* r_out, int shift_mode,
-                   double shift_value, const double* sgn_for_solve = nullptr, bool defer_solve = false) {
+                   double shift_value, const double* sgn_for_solve = nullptr, bool defer_solve = false,
+                   int check = 0) {
   cqr_ctx* c = j.c;
   const int n = j.n;
   double* g = dbuf<double>(c, B_G, (size_t)n * n);
   {
     StageScope t(c, CQR_STAGE_GRAM);
-    gram_dev(c, in, j.m_local, n, ldi, g);
+    gram_dev(c, in, j.m_local, n, ldi, g, check);
   }
   push_stage(rep, CQR_STAGE_GRAM);
   double* work = dbuf<double>(c, B_WORK, (size_t)n * n);
@@ -365,12 +368,13 @@ Outcome run_cholqr_family(Job& j) {
   double* r3 = dbuf<double>(c, B_RTMP, (size_t)n * n);
   double* r = dbuf<double>(c, B_R, (size_t)n * n);
   const bool r_less = j.opts.r_less != 0;
+  const int chk = j.check_first;
   if (j.method == CQR_CHOLQR) {
-    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0);
+    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0, nullptr, false, chk);
     o.has_r = !r_less;
     o.r_dev = r1;
   } else if (j.method == CQR_CHOLQR2) {
-    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0);
+    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0, nullptr, false, chk);
     cholesky_pass(j, j.q, j.ldq, o.rep, r2, 0, 0.0);
     if (!r_less) {
       StageScope t(c, CQR_STAGE_RECOVER);
@@ -381,7 +385,7 @@ Outcome run_cholqr_family(Job& j) {
     o.r_dev = r;
   } else {  // CQR_SCHOLQR3
     const int mode = j.opts.shift_kind == CQR_SHIFT_FIXED ? 1 : 2;
-    cholesky_pass(j, j.a, j.lda, o.rep, r1, mode, j.opts.shift_value);
+    cholesky_pass(j, j.a, j.lda, o.rep, r1, mode, j.opts.shift_value, nullptr, false, chk);
     cholesky_pass(j, j.q, j.ldq, o.rep, r2, 0, 0.0);
     double* r3b = dbuf<double>(c, B_X, (size_t)n * n);
     cholesky_pass(j, j.q, j.ldq, o.rep, r3b, 0, 0.0);
@@ -434,7 +438,8 @@ Outcome run_precond(Job& j) {
         double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
         if (j.m_local > 0) {
           LAUNCH(c, cqr::launch_sketch_gaussian(sp, j.a, j.lda, m, j.row0, seed, part,
-                                                vec_ok(j.a, j.lda, n) ? 1 : 0, c->status, c->stream));
+                                                vec_ok(j.a, j.lda, n) ? 1 : 0, attempt == 0 ? j.check_first : 0,
+                                                c->status, c->stream));
           LAUNCH(c, cqr::launch_sketch_reduce(sp, part, a1, c->status, c->stream));
         } else {
           ck(cudaMemsetAsync(a1, 0, sizeof(double) * l * n, c->stream), "memset");
@@ -638,7 +643,10 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     // check only sets the status word (read with the attempt's single sync);
     // several ranks agree on it first so they take the same path.
     reset_status(c);
-    check_finite(c, j.a, j.m_local, j.n, j.lda);
+    const bool gaussian = j.method == CQR_RQR_GAUSSIAN || j.cfg.strategy == CQR_GAUSSIAN;
+    const bool family = j.method == CQR_CHOLQR || j.method == CQR_CHOLQR2 || j.method == CQR_SCHOLQR3;
+    j.check_first = (c->world == 1 && !j.precond && (family || gaussian)) ? 1 : 0;
+    if (!j.check_first) check_finite(c, j.a, j.m_local, j.n, j.lda);
     if (c->world > 1) {
       DevStatus s0 = read_status(c);
       int bad = s0.code != 0;
@@ -1012,7 +1020,7 @@ int cqr_sketch_gaussian_dev(cqr_ctx* c, const double* a, int64_t m_local, int64_
     double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
     if (m_local > 0) {
       LAUNCH(c, cqr::launch_sketch_gaussian(sp, a, lda, m_global, row0, seed, part, vec_ok(a, lda, (int)n) ? 1 : 0,
-                                            c->status, c->stream));
+                                            0, c->status, c->stream));
       LAUNCH(c, cqr::launch_sketch_reduce(sp, part, a1_dev, c->status, c->stream));
     } else {
       ck(cudaMemsetAsync(a1_dev, 0, sizeof(double) * l * n, c->stream), "memset");
@@ -1035,7 +1043,7 @@ int cqr_sketch_gaussian(cqr_ctx* c, const double* a, int64_t m, int64_t n, int64
     reset_status(c);
     cqr::SketchPlan sp = cqr::sketch_plan(m, (int)n, (int)l, c->num_sms);
     double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
-    LAUNCH(c, cqr::launch_sketch_gaussian(sp, da, n, m, 0, seed, part, vec_ok(da, n, (int)n) ? 1 : 0, c->status,
+    LAUNCH(c, cqr::launch_sketch_gaussian(sp, da, n, m, 0, seed, part, vec_ok(da, n, (int)n) ? 1 : 0, 0, c->status,
                                           c->stream));
     LAUNCH(c, cqr::launch_sketch_reduce(sp, part, d1, c->status, c->stream));
     ck(cudaMemcpyAsync(a1, d1, sizeof(double) * l * n, cudaMemcpyDeviceToHost, c->stream), "A1 D2H");

@@ -37,8 +37,8 @@ template <int NP, int MAXT, int CH>
 __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __restrict__ x, long long ldx,
                                                                long long m, int n, int parts,
                                                                const int32_t* __restrict__ tiles,
-                                                               double* __restrict__ partial, int vec16,
-                                                               const DevStatus* st) {
+                                                               double* __restrict__ partial, int vec16, int check,
+                                                               DevStatus* st) {
   constexpr int LDX = NP + 4;
   extern __shared__ __align__(16) double smem[];
   if (failed(st)) return;
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
   const double* xg = x + r0 * ldx;
   const int nch = (rows + CH - 1) / CH;
   double* buf[2] = {smem, smem + CH * LDX};
+  bool bad = false;  // the union of the warps' fragments covers every column of the leaf
   stage_rows(buf[0], LDX, xg, ldx, min(CH, rows), CH, n, NP, tid, kWpc * 32, vec16 != 0);
   cp_async_commit();
   for (int c = 0; c < nch; ++c) {
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
         const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
         const double a0 = xr[16 * I2], a1 = xr[16 * I2 + 8];
         const double b0 = xr[16 * J2], b1 = xr[16 * J2 + 8];
+        bad |= nonfinite(a0) | nonfinite(a1) | nonfinite(b0) | nonfinite(b1);
         dmma(acc[t][0][0], acc[t][0][1], a0, b0);
         dmma(acc[t][1][0], acc[t][1][1], a0, b1);
         if (I2 != J2) dmma(acc[t][2][0], acc[t][2][1], a1, b0);
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
     }
     __syncthreads();
   }
+  if (check && __any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
   double* out = partial + (long long)leaf * NP * NP;
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) {
@@ -173,12 +176,13 @@ __global__ void mirror_kernel(double* g, int n, const DevStatus* st) {
 
 template <int NP, int MAXT, int CH>
 cudaError_t launch_leaves_t(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
-                            double* partial, int vec16, const DevStatus* st, cudaStream_t s) {
+                            double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s) {
   const size_t smem = (size_t)2 * CH * (NP + 4) * sizeof(double);
   auto k = gram_leaf_kernel<NP, MAXT, CH>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)(p.leaves * p.parts), kWpc * 32, smem, s>>>(x, ldx, p.m, p.n, p.parts, tiles, partial, vec16, st);
+  k<<<(unsigned)(p.leaves * p.parts), kWpc * 32, smem, s>>>(x, ldx, p.m, p.n, p.parts, tiles, partial, vec16, check,
+                                                             const_cast<DevStatus*>(st));
   return cudaGetLastError();
 }
 
@@ -219,14 +223,14 @@ void gram_tiles(const GramPlan& p, int32_t* out) {
 }
 
 cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
-                               double* partial, int vec16, const DevStatus* st, cudaStream_t s) {
+                               double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s) {
 #define CQR_GRAM_CASE(NP_, CH_)                                                                     \
   case NP_:                                                                                          \
     switch (p.maxt) {                                                                                \
-      case 1: return launch_leaves_t<NP_, 1, CH_>(p, x, ldx, tiles, partial, vec16, st, s);         \
-      case 2: return launch_leaves_t<NP_, 2, CH_>(p, x, ldx, tiles, partial, vec16, st, s);         \
-      case 5: return launch_leaves_t<NP_, 5, CH_>(p, x, ldx, tiles, partial, vec16, st, s);         \
-      default: return launch_leaves_t<NP_, 9, CH_>(p, x, ldx, tiles, partial, vec16, st, s);        \
+      case 1: return launch_leaves_t<NP_, 1, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);         \
+      case 2: return launch_leaves_t<NP_, 2, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);         \
+      case 5: return launch_leaves_t<NP_, 5, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);         \
+      default: return launch_leaves_t<NP_, 9, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);        \
     }
   switch (p.np) {
     CQR_GRAM_CASE(16, 32)

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
                                                              long long m_local, long long m_global, long long row0,
                                                              int n, int l, uint64_t seed, long long rows_per_chunk,
                                                              double* __restrict__ partial, int lp, int np_total,
-                                                             int vec16, const DevStatus* st) {
+                                                             int vec16, int check, DevStatus* st) {
   constexpr int NT = NP / 8;
   constexpr int WN = NT < 8 ? NT : 8;  // warps along n
   constexpr int WM = 8 / WN;           // warps along Omega rows
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
 #pragma unroll
     for (int h = 0; h < NG; ++h) acc[g][h][0] = acc[g][h][1] = 0.0;
   const int nsteps = k_end > k_begin ? (int)((k_end - k_begin + kKS - 1) / kKS) : 0;
+  bool bad = false;  // non-finite A values seen in this warp's B fragments (they cover all of A)
   if (nsteps > 0) {
     stage_rows(sA[0], LDA, a + k_begin * lda, lda, (int)min((long long)kKS, k_end - k_begin), kKS, n, NP, tid,
                kThreads, vec16 != 0);
@@ -153,7 +154,10 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
 #pragma unroll
         for (int g = 0; g < MG; ++g) af[g] = O[g * 8 * LDO + 4 * k4];
 #pragma unroll
-        for (int h = 0; h < NG; ++h) bf[h] = A[(4 * k4 + q) * LDA + (wn * NG + h) * 8 + gr];
+        for (int h = 0; h < NG; ++h) {
+          bf[h] = A[(4 * k4 + q) * LDA + (wn * NG + h) * 8 + gr];
+          bad |= nonfinite(bf[h]);
+        }
 #pragma unroll
         for (int g = 0; g < MG; ++g)
 #pragma unroll
@@ -161,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
       }
     }
   }
+  if (check && __any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
   // partial[chunk][s0 + i][col0 + col], lp rows per chunk, np_total columns
   double* out = partial + (long long)blockIdx.y * lp * np_total + col0;
 #pragma unroll
@@ -247,7 +252,8 @@ cudaError_t ensure_tables() {
 
 template <int NP>
 cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
-                            uint64_t seed, double* partial, int vec16, const DevStatus* st, cudaStream_t s) {
+                            uint64_t seed, double* partial, int vec16, int check, const DevStatus* st,
+                            cudaStream_t s) {
   cudaError_t e0 = ensure_tables();
   if (e0 != cudaSuccess) return e0;
   const size_t smem = sizeof(BmTables) + (size_t)(2 * kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
@@ -258,7 +264,7 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)p.s_tiles, (unsigned)p.kchunks, (unsigned)(p.np / NP));
     k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial,
-                                   p.lp, p.np, vec16, st);
+                                   p.lp, p.np, vec16, check, const_cast<DevStatus*>(st));
     return cudaGetLastError();
   }
   auto k = sketch_kernel<NP, true>;
@@ -266,7 +272,7 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.s_tiles, (unsigned)p.kchunks, (unsigned)(p.np / NP));
   k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial, p.lp,
-                                 p.np, vec16, st);
+                                 p.np, vec16, check, const_cast<DevStatus*>(st));
   return cudaGetLastError();
 }
 
@@ -316,16 +322,16 @@ SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms) {
 }
 
 cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,
-                                   long long row0, uint64_t seed, double* partial, int vec16, const DevStatus* st,
-                                   cudaStream_t s) {
+                                   long long row0, uint64_t seed, double* partial, int vec16, int check,
+                                   const DevStatus* st, cudaStream_t s) {
   switch (p.np) {
-    case 8: return launch_sketch_t<8>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
-    case 16: return launch_sketch_t<16>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
-    case 32: return launch_sketch_t<32>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
-    case 64: return launch_sketch_t<64>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
-    case 128: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+    case 8: return launch_sketch_t<8>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
+    case 16: return launch_sketch_t<16>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
+    case 32: return launch_sketch_t<32>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
+    case 64: return launch_sketch_t<64>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
+    case 128: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
     case 256:
-    case 512: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, st, s);
+    case 512: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -292,6 +292,12 @@ def test_r_less_and_non_finite():
     b[3, 1] = np.nan
     with pytest.raises(ValueError):
         G.cholesky_qr(b)
+    # every path rejects non-finite input up front, before any breakdown (engine.cpp:222)
+    c = o.synthesize(5000, 16, 1e14, 3)
+    c[4321, 7] = np.inf
+    for meth in (_abi.CHOLQR2, _abi.SCHOLQR3, _abi.RQR_GAUSSIAN, _abi.RLU, _abi.RQR):
+        with pytest.raises(ValueError):
+            G._factor(meth, c, G.SketchConfig(seed=3), _abi.options())
 
 
 def test_diagnostics_cond_x():  # test_cholqr.cpp:154-171 (20 of the 100 trials)
