@@ -192,6 +192,283 @@ __global__ void __launch_bounds__(kT) lu_kernel(const double* __restrict__ a1, i
   }
 }
 
+// Blocked right-looking LU (kernels.hpp:211-257), bitwise equal to the unblocked
+// fma form: 32-column panels are factored in shared memory exactly as the
+// unblocked loop (first maximum, zero-pivot check, multipliers, fma updates
+// skipped for zero multipliers); the trailing columns then get the panel's
+// row swaps, the unit-lower solve U12 = L11^-1 A12 (per column, fma chain over
+// the pivots in order, zero multipliers skipped) and A22 += (-L21) U12 on DMMA
+// (k = the panel's pivots in ascending order). Every trailing element thus sees
+// the same fma sequence as in the unblocked algorithm. Only U is returned, so
+// the L part left of a panel is never permuted.
+constexpr int kLuPanel = 32;
+constexpr int kLuLdp = kLuPanel + 1;
+
+__global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restrict__ a1, int l, int n,
+                                                        double* __restrict__ u, double* W, double* Pg,
+                                                        DevStatus* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double wb[32];
+  __shared__ int wi[32];
+  __shared__ int s_piv[kLuPanel];
+  __shared__ int s_bad;
+  if (failed(st)) return;
+  double* P = Pg ? Pg : smem;  // (l - j0) x kLuPanel panel, stride kLuLdp (smem, or global when too tall)
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int i = warp; i < l; i += nw)
+    for (int c = lane; c < n; c += 32) W[(long long)i * n + c] = a1[(long long)i * n + c];
+  if (tid == 0) s_bad = -1;
+  __syncthreads();
+  for (int j0 = 0; j0 < n; j0 += kLuPanel) {
+    const int w = min(kLuPanel, n - j0);
+    const int pr = l - j0;  // panel rows
+    for (int r = warp; r < pr; r += nw)
+      if (lane < w) P[r * kLuLdp + lane] = W[(long long)(j0 + r) * n + j0 + lane];
+    __syncthreads();
+    // ---- panel factorization (unblocked, shared memory)
+    for (int jj = 0; jj < w; ++jj) {
+      double best = -1.0;
+      int idx = 0x7fffffff;
+      for (int r = jj + tid; r < pr; r += nt) {
+        const double v = fabs(P[r * kLuLdp + jj]);
+        if (v > best) {
+          best = v;
+          idx = r;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ob > best || (ob == best && oi < idx)) {
+          best = ob;
+          idx = oi;
+        }
+      }
+      if (lane == 0) {
+        wb[warp] = best;
+        wi[warp] = idx;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        best = lane < nw ? wb[lane] : -1.0;
+        idx = lane < nw ? wi[lane] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+          if (ob > best || (ob == best && oi < idx)) {
+            best = ob;
+            idx = oi;
+          }
+        }
+        if (lane == 0) {
+          s_piv[jj] = idx;
+          if (idx >= pr || P[idx * kLuLdp + jj] == 0.0) s_bad = j0 + jj;
+        }
+      }
+      __syncthreads();
+      if (s_bad >= 0) {
+        if (tid == 0) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, s_bad);
+        return;
+      }
+      const int piv = s_piv[jj];
+      if (piv != jj && tid < w) {
+        const double t = P[jj * kLuLdp + tid];
+        P[jj * kLuLdp + tid] = P[piv * kLuLdp + tid];
+        P[piv * kLuLdp + tid] = t;
+      }
+      __syncthreads();
+      const double d = P[jj * kLuLdp + jj];
+      for (int r = jj + 1 + tid; r < pr; r += nt) P[r * kLuLdp + jj] = P[r * kLuLdp + jj] / d;
+      __syncthreads();
+      // rank-1 update of the panel: warps over rows, lanes over the panel columns
+      for (int r = jj + 1 + warp; r < pr; r += nw) {
+        const double mult = P[r * kLuLdp + jj];
+        const int c = lane;
+        if (mult != 0.0 && c > jj && c < w) P[r * kLuLdp + c] = fma(-mult, P[jj * kLuLdp + c], P[r * kLuLdp + c]);
+      }
+      __syncthreads();
+    }
+    // U rows of the panel (the L part stays in P for the trailing update)
+    for (int r = warp; r < w; r += nw)
+      if (lane < w) W[(long long)(j0 + r) * n + j0 + lane] = P[r * kLuLdp + lane];
+    const int c1 = j0 + w;
+    if (c1 < n) {
+      // row swaps on the trailing columns, in pivot order
+      for (int jj = 0; jj < w; ++jj) {
+        const int piv = s_piv[jj];
+        if (piv != jj) {
+          double* ra = W + (long long)(j0 + jj) * n;
+          double* rb = W + (long long)(j0 + piv) * n;
+          for (int c = c1 + tid; c < n; c += nt) {
+            const double t = ra[c];
+            ra[c] = rb[c];
+            rb[c] = t;
+          }
+        }
+        __syncthreads();
+      }
+      // U12 = L11^-1 A12: one thread per trailing column, fma chain over the pivots
+      for (int c = c1 + tid; c < n; c += nt) {
+        double x[kLuPanel];
+#pragma unroll
+        for (int jj = 0; jj < kLuPanel; ++jj) x[jj] = jj < w ? W[(long long)(j0 + jj) * n + c] : 0.0;
+#pragma unroll
+        for (int jj = 1; jj < kLuPanel; ++jj) {
+          if (jj < w) {
+#pragma unroll
+            for (int k = 0; k < jj; ++k) {
+              const double mult = P[jj * kLuLdp + k];
+              if (mult != 0.0) x[jj] = fma(-mult, x[k], x[jj]);
+            }
+          }
+        }
+#pragma unroll
+        for (int jj = 1; jj < kLuPanel; ++jj)
+          if (jj < w) W[(long long)(j0 + jj) * n + c] = x[jj];
+      }
+      __syncthreads();
+      // A22 += (-L21) U12 on DMMA: 8x8 tiles over rows [j0+w, l) x cols [c1, n)
+      const int q = lane & 3, gr = lane >> 2;
+      const int tr = (l - c1 + 7) / 8, tc = (n - c1 + 7) / 8;
+      for (int t = warp; t < tr * tc; t += nw) {
+        const int rt = t / tc, ct = t - (t / tc) * tc;
+        const int r0 = c1 + rt * 8, cc0 = c1 + ct * 8;  // absolute row / column of the tile
+        const int row = r0 + gr, col = cc0 + 2 * q;
+        double c0v = 0.0, c1v = 0.0;
+        if (row < l && col < n) c0v = W[(long long)row * n + col];
+        if (row < l && col + 1 < n) c1v = W[(long long)row * n + col + 1];
+        for (int k4 = 0; k4 < (w + 3) / 4; ++k4) {
+          const int kk = 4 * k4 + q;                 // A: row gr, k = q
+          const double av = (row < l && kk < w) ? -P[(row - j0) * kLuLdp + kk] : 0.0;
+          const int bk = 4 * k4 + q, bc = cc0 + gr;  // B: k = q, col = gr
+          const double bv = (bk < w && bc < n) ? W[(long long)(j0 + bk) * n + bc] : 0.0;
+          dmma(c0v, c1v, av, bv);
+        }
+        if (row < l && col < n) W[(long long)row * n + col] = c0v;
+        if (row < l && col + 1 < n) W[(long long)row * n + col + 1] = c1v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = warp; i < n; i += nw)
+    for (int c = lane; c < n; c += 32) u[(long long)i * n + c] = c >= i ? W[(long long)i * n + c] : 0.0;
+}
+
+// Blocked right-looking Cholesky (kernels.hpp:76-90 in the oracle's pinned
+// right-looking order), bitwise equal to cholesky_kernel: for each 32-row
+// panel the panel rows are factored exactly as the unblocked loop (rows of R
+// divided by the pivot, updates inside the panel rows), then the trailing
+// upper triangle gets s(a,b) += sum_i (-r(i,a)) r(i,b) over the panel's i in
+// ascending order on DMMA. S lives in the L2-resident global workspace, the
+// panel rows in shared memory.
+constexpr int kChPanel = 32;
+
+__device__ __forceinline__ double div_rn(double y, double d, double inv) {
+  // correctly rounded y / d from inv = RN(1/d) (two Markstein corrections)
+  const double ay = fabs(y);
+  if (!(ay >= 0x1p-900 && ay <= 0x1p+900) || !(fabs(d) >= 0x1p-500 && fabs(d) <= 0x1p+500))
+    return y / d;
+  const double q0 = y * inv;
+  double r = fma(-q0, d, y);
+  const double q1 = fma(r, inv, q0);
+  r = fma(-q1, d, y);
+  return fma(r, inv, q1);
+}
+
+__global__ void __launch_bounds__(512) cholesky_blocked_kernel(const double* __restrict__ g, int n,
+                                                               double* __restrict__ r, double* S, int shift_mode,
+                                                               double shift_value, double theory_coef,
+                                                               double* shift_out, DevStatus* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double s_d, s_inv;
+  __shared__ int s_bad;
+  if (failed(st)) return;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int ldp = n + 1;
+  double* Pn = smem;  // kChPanel x n panel rows (stride ldp), absolute column index
+  for (int i = warp; i < n; i += nw)
+    for (int c = lane; c < n; c += 32) S[(long long)i * n + c] = g[(long long)i * n + c];
+  __syncthreads();
+  if (shift_mode != 0 && tid == 0) {
+    double sh = shift_value;
+    if (shift_mode == 2) {
+      double tr = 0.0;
+      for (int j = 0; j < n; ++j) tr += g[(long long)j * n + j];
+      sh = theory_coef * tr;
+    }
+    for (int j = 0; j < n; ++j) S[(long long)j * n + j] += sh;
+    if (shift_out) *shift_out = sh;
+  }
+  __syncthreads();
+  for (int j0 = 0; j0 < n; j0 += kChPanel) {
+    const int w = min(kChPanel, n - j0);
+    for (int rr = warp; rr < w; rr += nw)
+      for (int c = j0 + rr + lane; c < n; c += 32) Pn[rr * ldp + c] = S[(long long)(j0 + rr) * n + c];
+    __syncthreads();
+    for (int ii = 0; ii < w; ++ii) {
+      const int i = j0 + ii;
+      double* Pi = Pn + ii * ldp;
+      if (tid == 0) {
+        const double sii = Pi[i];
+        if (!(sii > 0.0)) {
+          s_bad = 1;
+          set_status(st, 1 /*CQR_CHOLESKY_BREAKDOWN*/, i);
+        } else {
+          s_bad = 0;
+          s_d = sqrt(sii);
+          s_inv = 1.0 / s_d;
+          Pi[i] = s_d;
+        }
+      }
+      __syncthreads();
+      if (s_bad) return;
+      const double d = s_d, inv = s_inv;
+      for (int c = i + 1 + tid; c < n; c += nt) Pi[c] = div_rn(Pi[c], d, inv);
+      __syncthreads();
+      // update the remaining panel rows a in (i, j0+w), columns b >= a
+      for (int aa = ii + 1 + warp; aa < w; aa += nw) {
+        const int a = j0 + aa;
+        const double ra = Pi[a];
+        double* Pa = Pn + aa * ldp;
+        for (int b = a + lane; b < n; b += 32) Pa[b] = fma(-ra, Pi[b], Pa[b]);
+      }
+      __syncthreads();
+    }
+    // panel rows of R back to S
+    for (int rr = warp; rr < w; rr += nw)
+      for (int c = j0 + rr + lane; c < n; c += 32) S[(long long)(j0 + rr) * n + c] = Pn[rr * ldp + c];
+    // trailing upper triangle: S22 += (-R12^T) R12, 8x8 tiles, k = panel rows ascending
+    const int c1 = j0 + w;
+    if (c1 < n) {
+      const int q = lane & 3, gr = lane >> 2;
+      const int T = (n - c1 + 7) / 8;
+      for (int t = warp; t < T * T; t += nw) {
+        const int ti = t / T, tj = t - (t / T) * T;
+        if (tj < ti) continue;  // upper tiles only (diagonal tiles include a harmless lower part)
+        const int a0 = c1 + 8 * ti, b0 = c1 + 8 * tj;
+        const int row = a0 + gr, col = b0 + 2 * q;
+        double c0v = 0.0, c1v = 0.0;
+        if (row < n && col < n) c0v = S[(long long)row * n + col];
+        if (row < n && col + 1 < n) c1v = S[(long long)row * n + col + 1];
+#pragma unroll
+        for (int k4 = 0; k4 < kChPanel / 4; ++k4) {
+          const int k = 4 * k4 + q;
+          const double av = (k < w && row < n) ? -Pn[k * ldp + row] : 0.0;          // A[row][k] = -R(j0+k, row)
+          const double bv = (k < w && b0 + gr < n) ? Pn[k * ldp + b0 + gr] : 0.0;  // B[k][col] = R(j0+k, col)
+          dmma(c0v, c1v, av, bv);
+        }
+        if (row < n && col < n) S[(long long)row * n + col] = c0v;
+        if (row < n && col + 1 < n) S[(long long)row * n + col + 1] = c1v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = warp; i < n; i += nw)
+    for (int c = lane; c < n; c += 32) r[(long long)i * n + c] = c >= i ? S[(long long)i * n + c] : 0.0;
+}
+
 __global__ void __launch_bounds__(kT) qr_kernel(const double* __restrict__ a1, int l, int n, double* __restrict__ r,
                                                 double* work, int use_smem, DevStatus* st) {
   extern __shared__ __align__(16) double smem[];
@@ -329,6 +606,14 @@ size_t small_work_doubles(int rows, int n) { return (size_t)rows * n; }
 
 cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int shift_mode, double shift_value,
                             double theory_coef, double* shift_out, DevStatus* st, cudaStream_t s) {
+  if (n > 64) {
+    const size_t smem = (size_t)kChPanel * (n + 1) * sizeof(double);
+    cudaError_t e =
+        cudaFuncSetAttribute(cholesky_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cholesky_blocked_kernel<<<1, 512, smem, s>>>(g, n, r, work, shift_mode, shift_value, theory_coef, shift_out, st);
+    return cudaGetLastError();
+  }
   const size_t bytes = (size_t)n * n * sizeof(double);
   const int use_smem = bytes <= kSmemCap;
   return launch_small(cholesky_kernel, bytes, s, g, n, r, work, use_smem, shift_mode, shift_value, theory_coef,
@@ -336,6 +621,15 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
 }
 
 cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
+  {
+    const bool fits = (size_t)l * kLuLdp * sizeof(double) <= 220 * 1024;
+    const size_t smem = fits ? (size_t)l * kLuLdp * sizeof(double) : 0;
+    cudaError_t e = cudaFuncSetAttribute(lu_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return e;
+    // work holds l*n doubles for W, followed by the tall panel when it does not fit
+    lu_blocked_kernel<<<1, 512, smem, s>>>(a1, l, n, u, work, fits ? nullptr : work + (size_t)l * n, st);
+    return cudaGetLastError();
+  }
   const int rs = (int)std::min<size_t>((size_t)l, kSmemCap / ((size_t)n * sizeof(double)));
   const size_t smem = (size_t)rs * n * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
