@@ -254,13 +254,27 @@ __device__ __forceinline__ bool div_exponent_ok(double y) {
   return e - 124u < 1800u;
 }
 
-template <int NP, int WPC, bool BSMEM, bool SGN>
+// Straight-line correctly rounded division for the fast path (inv = RN(1/d),
+// d in [2^-500, 2^500]); `ok` is false when y needs the IEEE fallback.
+__device__ __forceinline__ double div_fast(double y, double d, double inv, bool& ok) {
+  const double q0 = y * inv;
+  double r = fma(-q0, d, y);
+  const double q1 = fma(r, inv, q0);
+  r = fma(-q1, d, y);
+  const double q = fma(r, inv, q1);
+  ok = div_exponent_ok(y);
+  return q;
+}
+
+template <int NP, int WPC, bool BSMEM, bool SGN, int WIN, int MG>
 __global__ void __launch_bounds__(WPC * 32, 1)
     trisolve_sb_kernel(const double* in, long long ldi, double* out, long long ldo, long long m, int n,
                        const double* __restrict__ bpack, const double* __restrict__ dpack,
                        const double* __restrict__ sgn, int vec16, const DevStatus* st) {
   constexpr int NT = NP / 8;
-  constexpr int MG = 4, RW = 32, W = NT < 8 ? NT : 8;  // window (blocks per pass)
+  constexpr int RW = 8 * MG;   // rows per warp
+  constexpr int RPL = MG / 4;  // rows per lane in the diagonal recurrence (independent chains)
+  constexpr int W = NT < WIN ? NT : WIN;  // window (blocks per pass)
   constexpr int NPASS = NT / W;
   constexpr int NB = BSMEM ? NT * (NT - 1) * 32 : 0;
   constexpr int ND = NT * kDiagStride;
@@ -279,9 +293,19 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   }
   __syncthreads();
   const long long groups = (m + RW - 1) / RW;
-  for (long long grp = (long long)blockIdx.x * WPC + warp; grp < groups; grp += (long long)gridDim.x * WPC) {
+  const long long gstride = (long long)gridDim.x * WPC;
+  for (long long grp = (long long)blockIdx.x * WPC + warp; grp < groups; grp += gstride) {
     const long long row0 = grp * RW;
     const int rows = (int)min((long long)RW, m - row0);
+    if constexpr (NP >= 256) {  // pull this warp's next row group into L2 while this one is solved
+      const long long nrow0 = (grp + gstride) * RW;
+      const int nrows = (int)max(0LL, min((long long)RW, m - nrow0));
+      const int lines = (n * 8 + 127) / 128;
+      for (int e = lane; e < nrows * lines; e += 32) {
+        const int r = e / lines, li = e - r * lines;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(in + (nrow0 + r) * ldi + li * 16));
+      }
+    }
 #pragma unroll 1
     for (int P = 0; P < NPASS; ++P) {
       const int c0 = 8 * W * P;
@@ -323,7 +347,7 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           }
 #pragma unroll
           for (int t = 0; t < W; ++t) {
-            const int JJ = 8 * P + t;
+            const int JJ = W * P + t;
             const int bi = (JJ * (JJ - 1) + k4) * 32 + lane;
             const double b = BSMEM ? sB[bi] : __ldg(sB + bi);
 #pragma unroll
@@ -340,60 +364,76 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           *reinterpret_cast<double2*>(sS + (g * 8 + gr) * LDS_ + 2 * q) = make_double2(acc[g][0][0], acc[g][0][1]);
         __syncwarp();
         {
-          double* xr = sS + lane * LDS_;
-          double y[8];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double2 v = *reinterpret_cast<const double2*>(xr + 2 * u);
-            y[2 * u] = v.x;
-            y[2 * u + 1] = v.y;
-          }
           const double* D = sD + J * kDiagStride;
-          if (D[80] != 0.0) {  // no zero in the block's strict upper part, divisors safe (uniform)
+          double y[RPL][8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-#pragma unroll
-              for (int kk = 0; kk < j; ++kk) y[j] = fma(-D[kk * 8 + j], y[kk], y[j]);
-              const double d = D[j * 8 + j], inv = D[64 + j];
-              const double yy = y[j];
-              if (div_exponent_ok(yy)) {
-                const double q0 = yy * inv;
-                double rr = fma(-q0, d, yy);
-                const double q1 = fma(rr, inv, q0);
-                rr = fma(-q1, d, yy);
-                y[j] = fma(rr, inv, q1);
-              } else {
-                y[j] = (yy == 0.0) ? yy * inv : yy / d;
-              }
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-#pragma unroll
-              for (int kk = 0; kk < j; ++kk) {
-                const double rr = D[kk * 8 + j];
-                if (rr != 0.0) y[j] = fma(-rr, y[kk], y[j]);
-              }
-              y[j] = fast_div(y[j], D[j * 8 + j], D[64 + j], D[72 + j] != 0.0);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(xr + 2 * u) = make_double2(y[2 * u], y[2 * u + 1]);
-          if (lane < rows) {
-            double* o = out + (row0 + lane) * ldo + 8 * J;
+          for (int rr = 0; rr < RPL; ++rr) {
+            const double* xr = sS + (lane + 32 * rr) * LDS_;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int c = 8 * J + 2 * u;
-              double v0 = y[2 * u], v1 = y[2 * u + 1];
-              if constexpr (SGN) {
-                if (c < n) v0 *= sgn[c];
-                if (c + 1 < n) v1 *= sgn[c + 1];
+              const double2 v = *reinterpret_cast<const double2*>(xr + 2 * u);
+              y[rr][2 * u] = v.x;
+              y[rr][2 * u + 1] = v.y;
+            }
+          }
+          bool good = D[80] != 0.0;  // uniform: no zero in the strict upper block, safe divisors
+          if (good) {
+            bool ok = true;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const double d = D[j * 8 + j], inv = D[64 + j];
+#pragma unroll
+              for (int rr = 0; rr < RPL; ++rr) {
+#pragma unroll
+                for (int kk = 0; kk < j; ++kk) y[rr][j] = fma(-D[kk * 8 + j], y[rr][kk], y[rr][j]);
+                bool okj;
+                y[rr][j] = div_fast(y[rr][j], d, inv, okj);
+                ok &= okj;
               }
-              if (vec16 && c + 1 < n) {
-                *reinterpret_cast<double2*>(o + 2 * u) = make_double2(v0, v1);
-              } else {
-                if (c < n) o[2 * u] = v0;
-                if (c + 1 < n) o[2 * u + 1] = v1;
+            }
+            good = __all_sync(0xffffffffu, ok);
+          }
+          if (!good) {  // rare: zeros in the block, extreme exponents or exact zeros
+#pragma unroll
+            for (int rr = 0; rr < RPL; ++rr) {
+              const double* xr = sS + (lane + 32 * rr) * LDS_;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) y[rr][j] = xr[j];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                for (int kk = 0; kk < j; ++kk) {
+                  const double rv = D[kk * 8 + j];
+                  if (rv != 0.0) y[rr][j] = fma(-rv, y[rr][kk], y[rr][j]);
+                }
+                y[rr][j] = fast_div(y[rr][j], D[j * 8 + j], D[64 + j], D[72 + j] != 0.0);
+              }
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int rr = 0; rr < RPL; ++rr) {
+            const int rl = lane + 32 * rr;
+            double* xr = sS + rl * LDS_;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              *reinterpret_cast<double2*>(xr + 2 * u) = make_double2(y[rr][2 * u], y[rr][2 * u + 1]);
+            if (rl < rows) {
+              double* o = out + (row0 + rl) * ldo + 8 * J;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int c = 8 * J + 2 * u;
+                double v0 = y[rr][2 * u], v1 = y[rr][2 * u + 1];
+                if constexpr (SGN) {
+                  if (c < n) v0 *= sgn[c];
+                  if (c + 1 < n) v1 *= sgn[c + 1];
+                }
+                if (vec16 && c + 1 < n) {
+                  *reinterpret_cast<double2*>(o + 2 * u) = make_double2(v0, v1);
+                } else {
+                  if (c < n) o[2 * u] = v0;
+                  if (c + 1 < n) o[2 * u + 1] = v1;
+                }
               }
             }
           }
@@ -429,14 +469,16 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   }
 }
 
-template <int NP, int WPC, bool BSMEM>
+template <int NP, int WPC, bool BSMEM, int WIN = 8, int MG = 4>
 cudaError_t launch_trisolve_sb_t(const TrisolveArgs& a, cudaStream_t s) {
   constexpr int NT = NP / 8;
-  const size_t smem = (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 32 * 10) * sizeof(double);
-  auto k = a.sgn ? trisolve_sb_kernel<NP, WPC, BSMEM, true> : trisolve_sb_kernel<NP, WPC, BSMEM, false>;
+  const size_t smem =
+      (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * 10) * sizeof(double);
+  auto k = a.sgn ? trisolve_sb_kernel<NP, WPC, BSMEM, true, WIN, MG>
+                 : trisolve_sb_kernel<NP, WPC, BSMEM, false, WIN, MG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long groups = (a.m + 31) / 32;
+  const long long groups = (a.m + 8 * MG - 1) / (8 * MG);
   long long grid = (groups + WPC - 1) / WPC;
   if (grid > (long long)a.num_sms) grid = a.num_sms;
   if (grid < 1) grid = 1;
@@ -503,6 +545,21 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   const int nt = np / 8;
   a.bpack = a.pack;
   a.dpack = a.pack + (size_t)nt * (nt - 1) * 32;
+  if (a.variant == 2) {  // 32-column passes, 16 warps
+    switch (np) {
+      case 64: return launch_trisolve_sb_t<64, 16, true, 4>(a, s);
+      case 128: return launch_trisolve_sb_t<128, 16, true, 4>(a, s);
+      case 256: return launch_trisolve_sb_t<256, 16, false, 4>(a, s);
+      case 512: return launch_trisolve_sb_t<512, 16, false, 4>(a, s);
+    }
+  }
+  if (a.variant == 3) {  // 32-column passes, 64 rows per warp (2 rows per lane in the recurrence)
+    switch (np) {
+      case 64: return launch_trisolve_sb_t<64, 8, true, 4, 8>(a, s);
+      case 128: return launch_trisolve_sb_t<128, 8, true, 4, 8>(a, s);
+      case 256: return launch_trisolve_sb_t<256, 8, false, 4, 8>(a, s);
+    }
+  }
   if (a.variant == 1) {  // left-looking (smem panel), kept for comparison and n = 512
     switch (np) {
       case 8: return launch_trisolve_t<8, 2, 16, true>(a, s);
@@ -516,9 +573,9 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   switch (np) {
     case 8: return launch_trisolve_sb_t<8, 12, true>(a, s);
     case 16: return launch_trisolve_sb_t<16, 12, true>(a, s);
-    case 32: return launch_trisolve_sb_t<32, 12, true>(a, s);
-    case 64: return launch_trisolve_sb_t<64, 12, true>(a, s);
-    case 128: return launch_trisolve_sb_t<128, 12, true>(a, s);
+    case 32: return launch_trisolve_sb_t<32, 16, true, 4>(a, s);
+    case 64: return launch_trisolve_sb_t<64, 16, true, 4>(a, s);
+    case 128: return launch_trisolve_sb_t<128, 16, true, 4>(a, s);
     case 256: return launch_trisolve_sb_t<256, 8, false>(a, s);
     case 512: return launch_trisolve_sb_t<512, 8, false>(a, s);
   }
