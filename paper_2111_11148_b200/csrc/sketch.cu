@@ -96,11 +96,10 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
   constexpr int PER = (SLOTS + kThreads - 1) / kThreads;  // pair slots per thread per step
   constexpr int K4 = kKS / 4;
   extern __shared__ __align__(16) double smem[];
+  __shared__ BmTables T;
   if (failed(st)) return;
-  BmTables& T = *reinterpret_cast<BmTables*>(smem);
-  double* base = smem + sizeof(BmTables) / sizeof(double);
-  double* sOm[2] = {base, base + kST * LDO};
-  double* sA[2] = {base + 2 * kST * LDO, base + 2 * kST * LDO + kKS * LDA};
+  // buffers as offsets into smem[] (keeps every access in the shared window: LDS/STS)
+  constexpr int OFF_OM = 0, OFF_A = 2 * kST * LDO;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = lane & 3, gr = lane >> 2;
   const int wm = warp / WN, wn = warp - (warp / WN) * WN;
@@ -123,13 +122,13 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
   const int nsteps = k_end > k_begin ? (int)((k_end - k_begin + kKS - 1) / kKS) : 0;
   bool bad = false;  // non-finite A values seen in this warp's B fragments (they cover all of A)
   if (nsteps > 0) {
-    stage_rows(sA[0], LDA, a + k_begin * lda, lda, (int)min((long long)kKS, k_end - k_begin), kKS, n, NP, tid,
+    stage_rows(smem + OFF_A, LDA, a + k_begin * lda, lda, (int)min((long long)kKS, k_end - k_begin), kKS, n, NP, tid,
                kThreads, vec16 != 0);
     cp_async_commit();
     __syncthreads();  // tables
 #pragma unroll
     for (int u = 0; u < PER; ++u)
-      gen_pair_slot<ALIGNED>(T, sOm[0], s0, l, m_global, row0 + k_begin, seed, tid + kThreads * u);
+      gen_pair_slot<ALIGNED>(T, smem + OFF_OM, s0, l, m_global, row0 + k_begin, seed, tid + kThreads * u);
   }
   for (int st_i = 0; st_i < nsteps; ++st_i) {
     const long long kb = k_begin + (long long)st_i * kKS;
@@ -137,13 +136,13 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
     __syncthreads();
     if (st_i + 1 < nsteps) {
       const long long kn = kb + kKS;
-      stage_rows(sA[(st_i + 1) & 1], LDA, a + kn * lda, lda, (int)min((long long)kKS, k_end - kn), kKS, n, NP, tid,
+      stage_rows(smem + OFF_A + ((st_i + 1) & 1) * kKS * LDA, LDA, a + kn * lda, lda, (int)min((long long)kKS, k_end - kn), kKS, n, NP, tid,
                  kThreads, vec16 != 0);
       cp_async_commit();
     }
-    const double* A = sA[st_i & 1];
-    const double* O = sOm[st_i & 1] + (wm * MG * 8 + gr) * LDO + q;
-    double* On = sOm[(st_i + 1) & 1];
+    const int offA = OFF_A + (st_i & 1) * kKS * LDA;
+    const int offO = OFF_OM + (st_i & 1) * kST * LDO + (wm * MG * 8 + gr) * LDO + q;
+    double* On = smem + OFF_OM + ((st_i + 1) & 1) * kST * LDO;
     const long long kbn = row0 + kb + kKS;
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -152,10 +151,10 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
       for (int k4 = u * K4 / PER; k4 < (u + 1) * K4 / PER; ++k4) {
         double af[MG], bf[NG];
 #pragma unroll
-        for (int g = 0; g < MG; ++g) af[g] = O[g * 8 * LDO + 4 * k4];
+        for (int g = 0; g < MG; ++g) af[g] = smem[offO + g * 8 * LDO + 4 * k4];
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
-          bf[h] = A[(4 * k4 + q) * LDA + (wn * NG + h) * 8 + gr];
+          bf[h] = smem[offA + (4 * k4 + q) * LDA + (wn * NG + h) * 8 + gr];
           bad |= nonfinite(bf[h]);
         }
 #pragma unroll
@@ -256,7 +255,7 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
                             cudaStream_t s) {
   cudaError_t e0 = ensure_tables();
   if (e0 != cudaSuccess) return e0;
-  const size_t smem = sizeof(BmTables) + (size_t)(2 * kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
+  const size_t smem = (size_t)(2 * kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
   const bool aligned = (m_global % 2 == 0) && (row0 % 2 == 0) && (p.rows_per_chunk % 2 == 0);
   if (!aligned) {
     auto k = sketch_kernel<NP, false>;
