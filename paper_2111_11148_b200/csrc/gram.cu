@@ -58,31 +58,31 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
 
   const double* xg = x + r0 * ldx;
   const int nch = (rows + CH - 1) / CH;
-  double* buf[2] = {smem, smem + CH * LDX};
+  // the two chunk buffers as offsets into smem[] (keeps the loads in the shared window)
   bool bad = false;  // the union of the warps' fragments covers every column of the leaf
-  stage_rows(buf[0], LDX, xg, ldx, min(CH, rows), CH, n, NP, tid, kWpc * 32, vec16 != 0);
+  stage_rows(smem, LDX, xg, ldx, min(CH, rows), CH, n, NP, tid, kWpc * 32, vec16 != 0);
   cp_async_commit();
   for (int c = 0; c < nch; ++c) {
     if (c + 1 < nch) {
       const int rr = min(CH, rows - (c + 1) * CH);
-      stage_rows(buf[(c + 1) & 1], LDX, xg + (long long)(c + 1) * CH * ldx, ldx, rr, CH, n, NP, tid, kWpc * 32,
-                 vec16 != 0);
+      stage_rows(smem + ((c + 1) & 1) * CH * LDX, LDX, xg + (long long)(c + 1) * CH * ldx, ldx, rr, CH, n, NP, tid,
+                 kWpc * 32, vec16 != 0);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* b = buf[c & 1];
+    const int boff = (c & 1) * CH * LDX;
 #pragma unroll 2
     for (int k4 = 0; k4 < CH / 4; ++k4) {
-      const double* xr = b + (4 * k4 + q) * LDX + gr;
+      const int xo = boff + (4 * k4 + q) * LDX + gr;
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
         if (mt[t] < 0) continue;
         const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
-        const double a0 = xr[16 * I2], a1 = xr[16 * I2 + 8];
-        const double b0 = xr[16 * J2], b1 = xr[16 * J2 + 8];
+        const double a0 = smem[xo + 16 * I2], a1 = smem[xo + 16 * I2 + 8];
+        const double b0 = smem[xo + 16 * J2], b1 = smem[xo + 16 * J2 + 8];
         bad |= nonfinite(a0) | nonfinite(a1) | nonfinite(b0) | nonfinite(b1);
         dmma(acc[t][0][0], acc[t][0][1], a0, b0);
         dmma(acc[t][1][0], acc[t][1][1], a0, b1);

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kT) lu_kernel(const double* __restrict__ a1, i
 constexpr int kLuPanel = 32;
 constexpr int kLuLdp = kLuPanel + 1;
 
+template <bool PSMEM>
 __global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restrict__ a1, int l, int n,
                                                         double* __restrict__ u, double* W, double* Pg,
                                                         DevStatus* st) {
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restric
   __shared__ int s_piv[kLuPanel];
   __shared__ int s_bad;
   if (failed(st)) return;
-  double* P = Pg ? Pg : smem;  // (l - j0) x kLuPanel panel, stride kLuLdp (smem, or global when too tall)
+  double* P = PSMEM ? smem : Pg;  // (l - j0) x kLuPanel panel, stride kLuLdp (smem, or global when too tall)
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int i = warp; i < l; i += nw)
     for (int c = lane; c < n; c += 32) W[(long long)i * n + c] = a1[(long long)i * n + c];
@@ -624,10 +625,15 @@ cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work,
   {
     const bool fits = (size_t)l * kLuLdp * sizeof(double) <= 220 * 1024;
     const size_t smem = fits ? (size_t)l * kLuLdp * sizeof(double) : 0;
-    cudaError_t e = cudaFuncSetAttribute(lu_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return e;
     // work holds l*n doubles for W, followed by the tall panel when it does not fit
-    lu_blocked_kernel<<<1, 512, smem, s>>>(a1, l, n, u, work, fits ? nullptr : work + (size_t)l * n, st);
+    if (fits) {
+      cudaError_t e =
+          cudaFuncSetAttribute(lu_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      if (e != cudaSuccess) return e;
+      lu_blocked_kernel<true><<<1, 512, smem, s>>>(a1, l, n, u, work, nullptr, st);
+    } else {
+      lu_blocked_kernel<false><<<1, 512, 0, s>>>(a1, l, n, u, work, work + (size_t)l * n, st);
+    }
     return cudaGetLastError();
   }
   const int rs = (int)std::min<size_t>((size_t)l, kSmemCap / ((size_t)n * sizeof(double)));
