@@ -213,6 +213,14 @@ int cqr_orthogonality_error_dev(cqr_ctx* ctx, const double* q, int64_t m, int64_
 int cqr_residual_error_dev(cqr_ctx* ctx, const double* a, int64_t lda, const double* q,
                            int64_t ldq, const double* r_host, int64_t m, int64_t n, double* out);
 
+/* ---- input synthesis on the device (matgen.cpp:21-46) ----------- */
+/* A = U diag(sigma) V^T for rows [row0, row0+m_local) of an m_global x n matrix
+ * (sigma: host array of n values). U, V: orthonormalised counter-RNG Gaussians
+ * (seeds derive(seed,0), derive(seed,1)); same spectrum as the reference's
+ * synthesize, not bit-identical (column signs). Sharded over an attached comm. */
+int cqr_synthesize_dev(cqr_ctx* ctx, int64_t m_local, int64_t m_global, int64_t row0, int64_t n,
+                       const double* sigma, uint64_t seed, double* a, int64_t lda);
+
 /* ---- parexec helpers (parexec.cpp:9-62) ----------------------------------- */
 /* offset(b) = ceil(b*m/p) */
 int64_t cqr_block_offset(int64_t m, int p, int b);

@@ -205,6 +205,7 @@ def _lib():
             "cqr_rng_gaussian": (i32, [vp, u64, u64, i64, vp]),
             "cqr_orthogonality_error_dev": (i32, [vp, vp, i64, i64, i64, pd]),
             "cqr_residual_error_dev": (i32, [vp, vp, i64, vp, i64, vp, i64, i64, pd]),
+            "cqr_synthesize_dev": (i32, [vp, i64, i64, i64, i64, vp, u64, vp, i64]),
             "cqr_block_offset": (i64, [i64, i32, i32]),
             "cqr_comm_model": (i32, [i32, i32, i64, i64, P(C.c_int), P(C.c_int), pd, pd]),
         }
@@ -596,6 +597,30 @@ def rng_gaussian(seed, k0, count, ctx=None):
     out = np.empty(count)
     ctx._check(_lib().cqr_rng_gaussian(ctx.h, seed & (2**64 - 1), k0, count, _ptr(out)))
     return out
+
+
+def geometric_sigma(n, kappa):
+    """sigma_i = exp(-ln(kappa) i/(n-1)) (matgen.cpp:27-31)."""
+    sig = np.ones(n)
+    if n > 1:
+        sig[1:] = np.exp(-np.log(kappa) * np.arange(1, n) / (n - 1))
+    return sig
+
+
+def synthesize_dev(m, n, kappa=None, seed=0, sigma=None, device=0, m_global=None, row0=0, ctx=None):
+    """matgen::synthesize on the device (matgen.cpp:21-46): rows [row0, row0+m) of
+    an m_global x n matrix U diag(sigma) V^T, returned as a CUDA tensor. Same
+    spectrum as the reference's generator; U, V differ from its Householder Q
+    factors by column signs (they are orthonormalised with device CholeskyQR2)."""
+    import torch
+
+    ctx = ctx or context(device)
+    sig = np.ascontiguousarray(sigma if sigma is not None else geometric_sigma(n, kappa), dtype=np.float64)
+    a = torch.empty((m, n), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    mg = m if m_global is None else m_global
+    ctx._check(_lib().cqr_synthesize_dev(ctx.h, m, mg, row0, n, _ptr(sig), seed & (2**64 - 1),
+                                         C.c_void_p(a.data_ptr()), n))
+    return a
 
 
 def orthogonality_error_dev(q, ctx=None):

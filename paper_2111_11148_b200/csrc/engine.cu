@@ -59,13 +59,14 @@ struct cqr_ctx {
   std::vector<StageEv> stage_evs;
   long long launches = 0;
   int tiles_key = -1;  // gram tile table currently on the device
+  int local_only = 0;  // temporarily treat an attached communicator as absent (replicated small work)
 };
 
 namespace {
 
 enum BufId {
   B_A1 = 0, B_SKPART, B_GPART, B_GTILES, B_G, B_RT, B_RH, B_R, B_RTMP, B_SGN, B_PACK1, B_PACK2, B_WORK,
-  B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X
+  B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X, B_SYN, B_SYNV
 };
 
 struct Fail {
@@ -244,7 +245,7 @@ struct Job {
 };
 
 void allreduce(cqr_ctx* c, double* p, size_t count) {
-  if (c->world <= 1) return;
+  if (c->world <= 1 || c->local_only) return;
   ckn(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->comm, c->stream), "ncclAllReduce");
 }
 
@@ -264,12 +265,12 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
   if (m > 0) {
     LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
                                       c->stream));
-    LAUNCH(c, cqr::launch_gram_combine(p, part, g, c->world <= 1 ? 1 : 0, c->status, c->stream));
+    LAUNCH(c, cqr::launch_gram_combine(p, part, g, (c->world <= 1 || c->local_only) ? 1 : 0, c->status, c->stream));
     ++c->launches;
   } else {
     ck(cudaMemsetAsync(g, 0, sizeof(double) * n * n, c->stream), "memset");
   }
-  if (c->world > 1) {
+  if (c->world > 1 && !c->local_only) {
     allreduce(c, g, (size_t)n * n);
     LAUNCH(c, cqr::launch_mirror_upper(g, n, c->status, c->stream));
   }
@@ -1137,6 +1138,71 @@ int cqr_residual_error_dev(cqr_ctx* c, const double* a, int64_t lda, const doubl
     ck(cudaMemcpyAsync(c->scal_h, o, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
     *out = std::sqrt(c->scal_h[0]) / std::sqrt(c->scal_h[1]);
+  });
+}
+
+// matgen.cpp:21-46 on the device: A = U diag(sigma) V^T with
+// U = orthonormalised gaussian_matrix(m, n, derive(seed, 0)) rows [row0, row0+m_local)
+// (global counters; orthonormalised by device CholeskyQR2, whose R has a positive
+// diagonal, so U matches the reference's Householder Q up to column signs) and
+// V = the same for gaussian_matrix(n, n, derive(seed, 1)). Same spectrum as the
+// reference's synthesize; not bit-identical to it.
+int cqr_synthesize_dev(cqr_ctx* c, int64_t m_local, int64_t m_global, int64_t row0, int64_t n, const double* sigma,
+                       uint64_t seed, double* a, int64_t lda) {
+  if (!c || n < 1 || n > 512 || m_global < n || m_local < 0 || row0 + m_local > m_global || lda < n || !sigma)
+    return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* u = dbuf<double>(c, B_SYN, (size_t)std::max<int64_t>(m_local, 1) * n);
+    double* v = dbuf<double>(c, B_SYNV, (size_t)n * n * 2);
+    // U: Gaussian rows, then CholeskyQR2 (sharded over the communicator when attached)
+    if (m_local > 0) LAUNCH(c, cqr::launch_rng_gaussian(derive(seed, 0), (uint64_t)row0 * n, m_local * n, u, c->stream));
+    cqr_options o = default_opts();
+    o.r_less = 1;
+    Job j{};
+    j.c = c;
+    j.method = CQR_CHOLQR2;
+    j.a = u;
+    j.m_local = m_local;
+    j.m_global = m_global;
+    j.row0 = row0;
+    j.n = (int)n;
+    j.lda = n;
+    j.q = u;
+    j.ldq = n;
+    j.cfg = default_cfg();
+    j.opts = o;
+    reset_status(c);
+    run_cholqr_family(j);
+    // V: n x n, replicated on every rank
+    LAUNCH(c, cqr::launch_rng_gaussian(derive(seed, 1), 0, n * n, v, c->stream));
+    Job jv = j;
+    jv.a = v;
+    jv.q = v;
+    jv.m_local = n;
+    jv.m_global = n;
+    jv.row0 = 0;
+    jv.lda = n;
+    jv.ldq = n;
+    c->local_only = 1;
+    reset_status(c);
+    try {
+      run_cholqr_family(jv);
+    } catch (...) {
+      c->local_only = 0;
+      throw;
+    }
+    c->local_only = 0;
+    std::vector<double> hv((size_t)n * n), svt((size_t)n * n);
+    ck(cudaMemcpy(hv.data(), v, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "V D2H");
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t jj = 0; jj < n; ++jj) svt[(size_t)(i * n + jj)] = sigma[i] * hv[(size_t)(jj * n + i)];
+    double* b = v + (size_t)n * n;
+    ck(cudaMemcpy(b, svt.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice), "SVt H2D");
+    if (m_local > 0) LAUNCH(c, cqr::launch_gemm_tall(u, n, b, a, lda, m_local, (int)n, c->num_sms, c->stream));
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->stage_evs.clear();
+    c->ev_used = 0;
   });
 }
 

@@ -94,6 +94,11 @@ cudaError_t launch_triangular_product(const double* left, const double* right, i
 // is then applied to Q's columns by the final trisolve.
 cudaError_t launch_normalize_sign(double* r, int n, double* sgn, const DevStatus* st, cudaStream_t s);
 
+// ---- matgen.cu ---------------------------------------------------------------------------
+// C = X * B, X m x n (ldx), B n x n row-major, C m x n (ldc), C != X.
+cudaError_t launch_gemm_tall(const double* x, long long ldx, const double* b, double* c, long long ldc, long long m,
+                             int n, int num_sms, cudaStream_t s);
+
 // ---- diag.cu ------------------------------------------------------------------------------
 // sum over rows of ||a_i - q_i R||^2 and ||a_i||^2 into out[0], out[1] (fixed order).
 cudaError_t launch_residual(const double* a, long long lda, const double* q, long long ldq, const double* r,
