@@ -101,25 +101,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_input(m_local, n, rank, world, device, kappa=None):
-    """A_local = U_local diag(sigma) V^T / sqrt(world): every rank's U block is
-    orthonormal, so the stacked U has orthogonal columns of norm sqrt(world)."""
-    import numpy as np
-    import torch
+def make_input(m_local, n, rank, world, device, kappa=None, ctx=None):
+    """Rows [rank*m_local, (rank+1)*m_local) of A = U diag(sigma) V^T, generated on
+    the device by the library (matgen.cpp:21-46 restated: counter-RNG Gaussians,
+    seeds derive(SEED, 0/1), orthonormalised across all ranks)."""
+    from paper_2111_11148_b200 import cholqr as cq
 
-    g = torch.Generator(device=device)
-    g.manual_seed(1000 + rank)
-    x = torch.randn((m_local, n), dtype=torch.float64, device=device, generator=g)
-    u, _ = torch.linalg.qr(x)
-    del x
-    rs = np.random.default_rng(SEED)
-    v, _ = np.linalg.qr(rs.standard_normal((n, n)))
-    sigma = (KAPPA if kappa is None else kappa) ** (-np.arange(n) / (n - 1))
-    svt = torch.as_tensor((sigma[:, None] * v.T) / np.sqrt(world), device=device)
-    a = u @ svt
-    del u
-    torch.cuda.synchronize(device)
-    return a.contiguous()
+    if ctx is None:
+        from paper_2111_11148_b200 import dist
+
+        ctx = dist.make_context(device.index if hasattr(device, "index") else int(device), rank, world)
+    k = KAPPA if kappa is None else kappa
+    return cq.synthesize_dev(m_local, n, k, SEED, device=ctx.device, m_global=m_local * world,
+                             row0=rank * m_local, ctx=ctx)
 
 
 def run_ours(args):
@@ -142,7 +136,7 @@ def run_ours(args):
     m_local, n = M_PER_GPU, N
     m_global = m_local * world
     row0 = rank * m_local
-    a = make_input(m_local, n, rank, world, dev)
+    a = make_input(m_local, n, rank, world, dev, ctx=ctx)
     q = torch.empty_like(a)
     cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=RATE, seed=_seed_value())
     l = cfg.resolved_size(m_global, n)
@@ -228,7 +222,7 @@ def run_ours(args):
     line = {"metric": "rQR/rLU-CholeskyQR fp64 TFLOP/s (ms/factorization in ms_per_step)", "value": value,
             "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded U diag(sigma) V^T, sigma log-spaced 1..1e-14)",
+            "data": "synthetic: A = U diag(sigma) V^T generated on the device (matgen.cpp restated), sigma log-spaced 1..1e-14",
             "config": {"workload": WORKLOAD, "method": "rlu", "sketch": "gaussian", "m_per_gpu": m_local,
                        "m_global": m_global, "n": n, "l": l, "kappa": KAPPA,
                        "l2": "inputs larger than L2 (1.02 GB per GPU vs 126 MB L2), no flush",

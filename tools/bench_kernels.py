@@ -14,8 +14,8 @@ m = int(os.environ.get("PROF_M", bench.M_PER_GPU))
 n = int(os.environ.get("PROF_N", bench.N))
 methods = os.environ.get("PROF_METHODS", "rlu").split(",")
 dev = torch.device("cuda", 0)
-a = bench.make_input(m, n, 0, 1, dev, float(os.environ.get("PROF_KAPPA", bench.KAPPA)))
 ctx = dist.make_context(0, 0, 1)
+a = bench.make_input(m, n, 0, 1, dev, float(os.environ.get("PROF_KAPPA", bench.KAPPA)), ctx=ctx)
 cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=2.0, seed=bench._seed_value())
 q = torch.empty_like(a)
 ids = {"rlu": _abi.RLU, "rqr": _abi.RQR_GAUSSIAN, "cholqr2": _abi.CHOLQR2, "scholqr3": _abi.SCHOLQR3,

@@ -14,8 +14,8 @@ n = int(os.environ.get("PROF_N", bench.N))
 method = {"rlu": _abi.RLU, "rqr": _abi.RQR_GAUSSIAN, "cholqr2": _abi.CHOLQR2}[os.environ.get("PROF_METHOD", "rlu")]
 reps = int(os.environ.get("PROF_REPS", "2"))
 dev = torch.device("cuda", 0)
-a = bench.make_input(m, n, 0, 1, dev)
 ctx = dist.make_context(0, 0, 1)
+a = bench.make_input(m, n, 0, 1, dev, ctx=ctx)
 cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=2.0, seed=bench._seed_value())
 q = torch.empty_like(a)
 for _ in range(reps):
