@@ -60,6 +60,8 @@ struct cqr_ctx {
   long long launches = 0;
   int tiles_key = -1;  // gram tile table currently on the device
   int local_only = 0;  // temporarily treat an attached communicator as absent (replicated small work)
+  cudaStream_t cstream = nullptr;  // copy stream of the host-buffer pipeline
+  std::vector<cudaEvent_t> pipe_ev;
 };
 
 namespace {
@@ -242,7 +244,28 @@ struct Job {
   cqr_precond_fn precond = nullptr;
   void* user = nullptr;
   int check_first = 0;  // fuse the non-finite check into the first tall kernel
+  // host-buffer pipeline (cqr_factor): A arrives in row chunks on the copy
+  // stream, the first tall pass consumes them as they land, and the final solve
+  // streams Q back chunk by chunk
+  const double* a_host = nullptr;
+  long long lda_host = 0;
+  double* q_host = nullptr;
+  long long ldq_host = 0;
+  std::vector<long long> bounds;  // chunk row boundaries, bounds.front() = 0, bounds.back() = m
+  int waited = 0;                 // H2D chunks the compute stream already waits on
 };
+
+bool pipelined(const Job& j) { return j.a_host != nullptr; }
+
+// make the compute stream wait for every H2D chunk that starts below row `rows_end`
+void wait_rows(Job& j, long long rows_end) {
+  cqr_ctx* c = j.c;
+  while (pipelined(j) && j.waited + 1 < (int)j.bounds.size() && j.bounds[j.waited] < rows_end) {
+    ck(cudaStreamWaitEvent(c->stream, c->pipe_ev[j.waited], 0), "wait H2D");
+    ++j.waited;
+  }
+}
+void wait_all(Job& j) { wait_rows(j, std::numeric_limits<long long>::max()); }
 
 void allreduce(cqr_ctx* c, double* p, size_t count) {
   if (c->world <= 1 || c->local_only) return;
@@ -250,7 +273,8 @@ void allreduce(cqr_ctx* c, double* p, size_t count) {
 }
 
 // Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
-void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g, int check = 0) {
+void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g, int check = 0,
+              Job* pj = nullptr) {
   cqr::GramPlan p = cqr::gram_plan(m, n);
   double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.workspace_doubles, 1));
   int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
@@ -263,8 +287,22 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
     c->tiles_key = key;
   }
   if (m > 0) {
-    LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
-                                      c->stream));
+    if (pj && pipelined(*pj) && pj->waited + 1 < (int)pj->bounds.size()) {
+      // leaves as their rows land (whole leaves per launch: the partials are per leaf, so identical)
+      int leaf = 0;
+      for (size_t i = 1; i < pj->bounds.size() && leaf < p.leaves; ++i) {
+        wait_rows(*pj, pj->bounds[i]);
+        const int leaf1 = (i + 1 == pj->bounds.size()) ? p.leaves : (int)(pj->bounds[i] / 1024);
+        if (leaf1 > leaf)
+          LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
+                                            c->stream, leaf, leaf1));
+        leaf = std::max(leaf, leaf1);
+      }
+    } else {
+      if (pj) wait_all(*pj);
+      LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
+                                        c->stream));
+    }
     LAUNCH(c, cqr::launch_gram_combine(p, part, g, (c->world <= 1 || c->local_only) ? 1 : 0, c->status, c->stream));
     ++c->launches;
   } else {
@@ -321,15 +359,17 @@ void check_finite(cqr_ctx* c, const double* a, long long m, int n, long long lda
 
 // One CholeskyQR pass (engine.cpp:78-92): G = X^T X (+shift I), R = chol(G),
 // X <- X R^{-1} (in -> out). shift_mode 0/1/2 as launch_cholesky.
+void final_solve(Job& j, const double* in, long long ldi, const double* pack, const double* sgn);
+
 void cholesky_pass(Job& j, const double* in, long long ldi, Report& rep, double* r_out, int shift_mode,
                    double shift_value, const double* sgn_for_solve = nullptr, bool defer_solve = false,
-                   int check = 0) {
+                   int check = 0, bool last = false) {
   cqr_ctx* c = j.c;
   const int n = j.n;
   double* g = dbuf<double>(c, B_G, (size_t)n * n);
   {
     StageScope t(c, CQR_STAGE_GRAM);
-    gram_dev(c, in, j.m_local, n, ldi, g, check);
+    gram_dev(c, in, j.m_local, n, ldi, g, check, &j);
   }
   push_stage(rep, CQR_STAGE_GRAM);
   double* work = dbuf<double>(c, B_WORK, (size_t)n * n);
@@ -348,9 +388,33 @@ void cholesky_pass(Job& j, const double* in, long long ldi, Report& rep, double*
   {
     StageScope t(c, CQR_STAGE_TRISOLVE);
     LAUNCH(c, cqr::launch_pack_r(r_out, n, n, pack, 0, c->status, c->stream));
-    trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, n, pack, sgn_for_solve);
+    if (last)
+      final_solve(j, in, ldi, pack, sgn_for_solve);
+    else
+      trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, n, pack, sgn_for_solve);
   }
   push_stage(rep, CQR_STAGE_TRISOLVE);
+}
+
+// The last solve of a factorization; with the host pipeline each row chunk of Q
+// is copied back as soon as it is solved (rows are independent, so the chunked
+// solve is bit-identical).
+void final_solve(Job& j, const double* in, long long ldi, const double* pack, const double* sgn) {
+  cqr_ctx* c = j.c;
+  if (!pipelined(j)) {
+    trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, j.n, pack, sgn);
+    return;
+  }
+  for (size_t i = 0; i + 1 < j.bounds.size(); ++i) {
+    const long long r0 = j.bounds[i], r1 = j.bounds[i + 1];
+    trisolve_dev(c, in + r0 * ldi, ldi, j.q + r0 * j.ldq, j.ldq, r1 - r0, j.n, pack, sgn);
+    cudaEvent_t e = c->pipe_ev[j.bounds.size() - 1 + i];
+    ck(cudaEventRecord(e, c->stream), "record");
+    ck(cudaStreamWaitEvent(c->cstream, e, 0), "wait solve");
+    ck(cudaMemcpy2DAsync(j.q_host + r0 * j.ldq_host, sizeof(double) * j.ldq_host, j.q + r0 * j.ldq,
+                         sizeof(double) * j.ldq, sizeof(double) * j.n, r1 - r0, cudaMemcpyDeviceToHost, c->cstream),
+       "Q D2H");
+  }
 }
 
 struct Outcome {
@@ -371,12 +435,12 @@ Outcome run_cholqr_family(Job& j) {
   const bool r_less = j.opts.r_less != 0;
   const int chk = j.check_first;
   if (j.method == CQR_CHOLQR) {
-    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0, nullptr, false, chk);
+    cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0, nullptr, false, chk, true);
     o.has_r = !r_less;
     o.r_dev = r1;
   } else if (j.method == CQR_CHOLQR2) {
     cholesky_pass(j, j.a, j.lda, o.rep, r1, 0, 0.0, nullptr, false, chk);
-    cholesky_pass(j, j.q, j.ldq, o.rep, r2, 0, 0.0);
+    cholesky_pass(j, j.q, j.ldq, o.rep, r2, 0, 0.0, nullptr, false, 0, true);
     if (!r_less) {
       StageScope t(c, CQR_STAGE_RECOVER);
       LAUNCH(c, cqr::launch_triangular_product(r2, r1, n, r, c->status, c->stream));
@@ -389,7 +453,7 @@ Outcome run_cholqr_family(Job& j) {
     cholesky_pass(j, j.a, j.lda, o.rep, r1, mode, j.opts.shift_value, nullptr, false, chk);
     cholesky_pass(j, j.q, j.ldq, o.rep, r2, 0, 0.0);
     double* r3b = dbuf<double>(c, B_X, (size_t)n * n);
-    cholesky_pass(j, j.q, j.ldq, o.rep, r3b, 0, 0.0);
+    cholesky_pass(j, j.q, j.ldq, o.rep, r3b, 0, 0.0, nullptr, false, 0, true);
     if (!r_less) {
       StageScope t(c, CQR_STAGE_RECOVER);
       LAUNCH(c, cqr::launch_triangular_product(r2, r1, n, r3, c->status, c->stream));
@@ -438,9 +502,23 @@ Outcome run_precond(Job& j) {
         cqr::SketchPlan sp = cqr::sketch_plan(j.m_local, n, (int)l, c->num_sms);
         double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
         if (j.m_local > 0) {
-          LAUNCH(c, cqr::launch_sketch_gaussian(sp, j.a, j.lda, m, j.row0, seed, part,
-                                                vec_ok(j.a, j.lda, n) ? 1 : 0, attempt == 0 ? j.check_first : 0,
-                                                c->status, c->stream));
+          const int vec = vec_ok(j.a, j.lda, n) ? 1 : 0, chk = attempt == 0 ? j.check_first : 0;
+          if (pipelined(j) && j.waited + 1 < (int)j.bounds.size()) {
+            // k-chunks as their rows land (whole k-chunks per launch: identical partials)
+            int y = 0;
+            for (size_t i = 1; i < j.bounds.size() && y < sp.kchunks; ++i) {
+              wait_rows(j, j.bounds[i]);
+              const int y1 = (i + 1 == j.bounds.size()) ? sp.kchunks : (int)(j.bounds[i] / sp.rows_per_chunk);
+              if (y1 > y)
+                LAUNCH(c, cqr::launch_sketch_gaussian(sp, j.a, j.lda, m, j.row0, seed, part, vec, chk, c->status,
+                                                      c->stream, y, y1));
+              y = std::max(y, y1);
+            }
+          } else {
+            wait_all(j);
+            LAUNCH(c, cqr::launch_sketch_gaussian(sp, j.a, j.lda, m, j.row0, seed, part, vec, chk, c->status,
+                                                  c->stream));
+          }
           LAUNCH(c, cqr::launch_sketch_reduce(sp, part, a1, c->status, c->stream));
         } else {
           ck(cudaMemsetAsync(a1, 0, sizeof(double) * l * n, c->stream), "memset");
@@ -459,6 +537,7 @@ Outcome run_precond(Job& j) {
           ck(cudaMemcpyAsync(idx, h.data(), sizeof(long long) * l, cudaMemcpyHostToDevice, c->stream), "idx H2D");
           ck(cudaStreamSynchronize(c->stream), "sync");
         }
+        wait_all(j);
         LAUNCH(c, cqr::launch_gather_rows(j.a, j.lda, j.m_local, m, j.row0, n, (int)l, seed, idx, a1, nullptr,
                                           c->status, c->stream));
       }
@@ -495,6 +574,7 @@ Outcome run_precond(Job& j) {
     // ---- X = A R~^{-1} (A -> Q buffer; A stays intact for a retry)
     {
       StageScope t(c, CQR_STAGE_TRISOLVE);
+      wait_all(j);
       trisolve_dev(c, j.a, j.lda, j.q, j.ldq, j.m_local, n, pack1, nullptr);
     }
     const bool diag = j.opts.diagnostics != 0;
@@ -533,7 +613,7 @@ Outcome run_precond(Job& j) {
     {
       StageScope t(c, CQR_STAGE_TRISOLVE);
       LAUNCH(c, cqr::launch_pack_r(rh, n, n, pack2, 0, c->status, c->stream));
-      trisolve_dev(c, j.q, j.ldq, j.q, j.ldq, j.m_local, n, pack2, r_less ? nullptr : sgn);
+      final_solve(j, j.q, j.ldq, pack2, r_less ? nullptr : sgn);
     }
     push_stage(o.rep, CQR_STAGE_TRISOLVE);
     if (!r_less) push_stage(o.rep, CQR_STAGE_RECOVER);
@@ -647,7 +727,10 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     const bool gaussian = j.method == CQR_RQR_GAUSSIAN || j.cfg.strategy == CQR_GAUSSIAN;
     const bool family = j.method == CQR_CHOLQR || j.method == CQR_CHOLQR2 || j.method == CQR_SCHOLQR3;
     j.check_first = (c->world == 1 && !j.precond && (family || gaussian)) ? 1 : 0;
-    if (!j.check_first) check_finite(c, j.a, j.m_local, j.n, j.lda);
+    if (!j.check_first) {
+      wait_all(j);
+      check_finite(c, j.a, j.m_local, j.n, j.lda);
+    }
     if (c->world > 1) {
       DevStatus s0 = read_status(c);
       int bad = s0.code != 0;
@@ -749,6 +832,8 @@ int cqr_destroy(cqr_ctx* c) {
   if (c->status_h) cudaFreeHost(c->status_h);
   if (c->scal_h) cudaFreeHost(c->scal_h);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
+  for (auto e : c->pipe_ev) cudaEventDestroy(e);
   delete c;
   return CQR_OK;
 }
@@ -831,10 +916,30 @@ static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     double* da = dbuf<double>(c, B_HA, (size_t)m * n);
     double* dq = dbuf<double>(c, B_HQ, (size_t)m * n);
-    ck(cudaMemcpy2DAsync(da, sizeof(double) * n, a, sizeof(double) * lda, sizeof(double) * n, m,
-                         cudaMemcpyHostToDevice, c->stream),
-       "A H2D");
     Job j{};
+    // chunked H2D on the copy stream (8 chunks of >= 8 MB), consumed as it lands
+    if (!c->cstream) ck(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking), "copy stream");
+    int nch = (int)std::min<long long>(8, std::max<long long>(1, (m * n * 8) / (8 << 20)));
+    j.bounds.clear();
+    for (int i = 0; i <= nch; ++i) j.bounds.push_back(m * i / nch);
+    while ((int)c->pipe_ev.size() < 2 * nch) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      c->pipe_ev.push_back(e);
+    }
+    ck(cudaEventRecord(c->pipe_ev[0], c->stream), "record");  // previous work on the compute stream done
+    ck(cudaStreamWaitEvent(c->cstream, c->pipe_ev[0], 0), "wait");
+    for (int i = 0; i < nch; ++i) {
+      const long long r0 = j.bounds[i], r1 = j.bounds[i + 1];
+      ck(cudaMemcpy2DAsync(da + r0 * n, sizeof(double) * n, a + r0 * lda, sizeof(double) * lda, sizeof(double) * n,
+                           r1 - r0, cudaMemcpyHostToDevice, c->cstream),
+         "A H2D");
+      ck(cudaEventRecord(c->pipe_ev[i], c->cstream), "record");
+    }
+    j.a_host = a;
+    j.lda_host = lda;
+    j.q_host = q;
+    j.ldq_host = ldq;
     j.c = c;
     j.method = method;
     j.a = da;
@@ -850,10 +955,8 @@ static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64
     j.precond = fn;
     j.user = user;
     const int s = factor_dev_impl(c, j, r, ldr, report);
+    ck(cudaStreamSynchronize(c->cstream), "sync copies");
     if (s != CQR_OK) throw Fail{s, report ? report->index : -1, c->err};
-    ck(cudaMemcpy2DAsync(q, sizeof(double) * ldq, dq, sizeof(double) * n, sizeof(double) * n, m,
-                         cudaMemcpyDeviceToHost, c->stream),
-       "Q D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
   return st;

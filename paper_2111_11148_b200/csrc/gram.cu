@@ -38,11 +38,11 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
                                                                long long m, int n, int parts,
                                                                const int32_t* __restrict__ tiles,
                                                                double* __restrict__ partial, int vec16, int check,
-                                                               DevStatus* st) {
+                                                               int leaf0, DevStatus* st) {
   constexpr int LDX = NP + 4;
   extern __shared__ __align__(16) double smem[];
   if (failed(st)) return;
-  const int leaf = blockIdx.x / parts, part = blockIdx.x - (blockIdx.x / parts) * parts;
+  const int leaf = blockIdx.x / parts + leaf0, part = blockIdx.x - (blockIdx.x / parts) * parts;
   const long long r0 = (long long)leaf * kLeafRows;
   const int rows = (int)min((long long)kLeafRows, m - r0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -176,13 +176,16 @@ __global__ void mirror_kernel(double* g, int n, const DevStatus* st) {
 
 template <int NP, int MAXT, int CH>
 cudaError_t launch_leaves_t(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
-                            double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s) {
+                            double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s, int leaf0,
+                            int leaf1) {
+  if (leaf1 < 0) leaf1 = p.leaves;
+  if (leaf1 <= leaf0) return cudaSuccess;
   const size_t smem = (size_t)2 * CH * (NP + 4) * sizeof(double);
   auto k = gram_leaf_kernel<NP, MAXT, CH>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)(p.leaves * p.parts), kWpc * 32, smem, s>>>(x, ldx, p.m, p.n, p.parts, tiles, partial, vec16, check,
-                                                             const_cast<DevStatus*>(st));
+  k<<<(unsigned)((leaf1 - leaf0) * p.parts), kWpc * 32, smem, s>>>(x, ldx, p.m, p.n, p.parts, tiles, partial, vec16,
+                                                                     check, leaf0, const_cast<DevStatus*>(st));
   return cudaGetLastError();
 }
 
@@ -223,14 +226,15 @@ void gram_tiles(const GramPlan& p, int32_t* out) {
 }
 
 cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
-                               double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s) {
+                               double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s, int leaf0,
+                               int leaf1) {
 #define CQR_GRAM_CASE(NP_, CH_)                                                                     \
   case NP_:                                                                                          \
     switch (p.maxt) {                                                                                \
-      case 1: return launch_leaves_t<NP_, 1, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);         \
-      case 2: return launch_leaves_t<NP_, 2, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);         \
-      case 5: return launch_leaves_t<NP_, 5, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);         \
-      default: return launch_leaves_t<NP_, 9, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s);        \
+      case 1: return launch_leaves_t<NP_, 1, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1);         \
+      case 2: return launch_leaves_t<NP_, 2, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1);         \
+      case 5: return launch_leaves_t<NP_, 5, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1);         \
+      default: return launch_leaves_t<NP_, 9, CH_>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1);        \
     }
   switch (p.np) {
     CQR_GRAM_CASE(16, 32)

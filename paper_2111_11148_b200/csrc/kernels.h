@@ -46,8 +46,10 @@ GramPlan gram_plan(long long m, int n);
 void gram_tiles(const GramPlan& p, int32_t* out);
 // Leaf partials (1024-row leaves, kernels.hpp:20-38) -> partial[leaf][np*np] (upper tiles).
 // check=1: also flag non-finite input (status INVALID_ARGUMENT, outranks others).
+// [leaf0, leaf1): the leaves this launch computes (default all); results are per leaf.
 cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles_dev,
-                               double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s);
+                               double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s,
+                               int leaf0 = 0, int leaf1 = -1);
 // Pairwise tree over leaves (kernels.hpp:42-57, streaming form) -> g upper (ld = n);
 // mirror=1 also writes the lower triangle (kernels.hpp:69).
 cudaError_t launch_gram_combine(const GramPlan& p, double* partial, double* g, int mirror,
@@ -61,9 +63,10 @@ struct SketchPlan {
   size_t partial_doubles = 0;
 };
 SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms);
+// [y0, y1): the k-chunks (rows_per_chunk rows each) this launch covers (default all).
 cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,
                                    long long row0, uint64_t seed, double* partial, int vec16, int check,
-                                   const DevStatus* st, cudaStream_t s);
+                                   const DevStatus* st, cudaStream_t s, int y0 = 0, int y1 = -1);
 // a1[i][c] = sum over k-chunks (ascending) of partial -> l x n (ld = n)
 cudaError_t launch_sketch_reduce(const SketchPlan& p, const double* partial, double* a1, const DevStatus* st,
                                  cudaStream_t s);

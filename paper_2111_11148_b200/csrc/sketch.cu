@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
                                                              long long m_local, long long m_global, long long row0,
                                                              int n, int l, uint64_t seed, long long rows_per_chunk,
                                                              double* __restrict__ partial, int lp, int np_total,
-                                                             int vec16, int check, DevStatus* st) {
+                                                             int vec16, int check, int y0, DevStatus* st) {
   constexpr int NT = NP / 8;
   constexpr int WN = NT < 8 ? NT : 8;  // warps along n
   constexpr int WM = 8 / WN;           // warps along Omega rows
@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
   const int col0 = blockIdx.z * NP;
   a += col0;
   n = min(NP, n - col0);
-  const long long k_begin = (long long)blockIdx.y * rows_per_chunk;
+  const int ky = blockIdx.y + y0;  // k-chunk index (launches may cover a sub-range of chunks)
+  const long long k_begin = (long long)ky * rows_per_chunk;
   const long long k_end = min(m_local, k_begin + rows_per_chunk);
   {
     const double* src = reinterpret_cast<const double*>(&c_bm);
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
   }
   if (check && __any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
   // partial[chunk][s0 + i][col0 + col], lp rows per chunk, np_total columns
-  double* out = partial + (long long)blockIdx.y * lp * np_total + col0;
+  double* out = partial + (long long)ky * lp * np_total + col0;
 #pragma unroll
   for (int g = 0; g < MG; ++g) {
     const int i = s0 + (wm * MG + g) * 8 + gr;
@@ -252,7 +253,9 @@ cudaError_t ensure_tables() {
 template <int NP>
 cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
                             uint64_t seed, double* partial, int vec16, int check, const DevStatus* st,
-                            cudaStream_t s) {
+                            cudaStream_t s, int y0, int y1) {
+  if (y1 < 0) y1 = p.kchunks;
+  if (y1 <= y0) return cudaSuccess;
   cudaError_t e0 = ensure_tables();
   if (e0 != cudaSuccess) return e0;
   const size_t smem = (size_t)(2 * kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
@@ -261,17 +264,17 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
     auto k = sketch_kernel<NP, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)p.s_tiles, (unsigned)p.kchunks, (unsigned)(p.np / NP));
+    dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NP));
     k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial,
-                                   p.lp, p.np, vec16, check, const_cast<DevStatus*>(st));
+                                   p.lp, p.np, vec16, check, y0, const_cast<DevStatus*>(st));
     return cudaGetLastError();
   }
   auto k = sketch_kernel<NP, true>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)p.s_tiles, (unsigned)p.kchunks, (unsigned)(p.np / NP));
+  dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NP));
   k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial, p.lp,
-                                 p.np, vec16, check, const_cast<DevStatus*>(st));
+                                 p.np, vec16, check, y0, const_cast<DevStatus*>(st));
   return cudaGetLastError();
 }
 
@@ -322,15 +325,15 @@ SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms) {
 
 cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,
                                    long long row0, uint64_t seed, double* partial, int vec16, int check,
-                                   const DevStatus* st, cudaStream_t s) {
+                                   const DevStatus* st, cudaStream_t s, int y0, int y1) {
   switch (p.np) {
-    case 8: return launch_sketch_t<8>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
-    case 16: return launch_sketch_t<16>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
-    case 32: return launch_sketch_t<32>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
-    case 64: return launch_sketch_t<64>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
-    case 128: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
+    case 8: return launch_sketch_t<8>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
+    case 16: return launch_sketch_t<16>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
+    case 32: return launch_sketch_t<32>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
+    case 64: return launch_sketch_t<64>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
+    case 128: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
     case 256:
-    case 512: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s);
+    case 512: return launch_sketch_t<128>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
   }
   return cudaErrorInvalidValue;
 }
