@@ -29,9 +29,12 @@ struct TrisolveArgs {
   int vec16;
   int num_sms;
   const DevStatus* status;
-  int variant = 0;  // 0: right-looking register kernel (n <= 256), 1: left-looking smem panel
+  int variant = 0;  // 0: TMA kernel when eligible, else the register kernel; 1..7: fixed kernels (tuning)
 };
 cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s);
+// trisolve_tma.cu: the TMA-staged kernel (16-byte aligned bases, even leading dimensions, np >= 32)
+bool trisolve_tma_eligible(const TrisolveArgs& a, int np);
+cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s);
 
 // ---- gram.cu ---------------------------------------------------------------------
 struct GramPlan {

@@ -24,20 +24,12 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "trisolve_common.cuh"
 
 namespace cqr {
 
 namespace {
-
-// Packed R for a padded width np (R padded with the identity):
-//   bpack[(J*(J-1) + k4)*32 + lane] = -R[4*k4 + (lane&3)][8J + (lane>>2)]   (k4 < 2J)
-//   dpack[J*80 + kk*8 + j]          =  R[8J+kk][8J+j]                       (8x8 diag block)
-//   dpack[J*80 + 64 + j]            =  RN(1 / R[8J+j][8J+j])
-//   dpack[J*80 + 72 + j]            =  1 if the fast division is safe for column j
-//   dpack[J*80 + 80]                =  1 if the block's strict upper part has no zero and
-//                                      all its divisions are safe (uniform fast path)
-// (per-block stride kDiagStride = 88)
-constexpr int kDiagStride = 88;
+using namespace tri;
 
 __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int np, double* __restrict__ bpack,
                               double* __restrict__ dpack, int* __restrict__ bad_min, int degenerate,
@@ -64,7 +56,13 @@ __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int 
       const long long d = e - nb;
       const int J = (int)(d / kDiagStride), w = (int)(d % kDiagStride);
       double v;
-      if (w < 64) {
+      if (w >= kColBase) {
+        const int o = w - kColBase;
+        int j = 0;
+        while (j < 7 && col_start(j + 1) <= o) ++j;
+        const int p = o - col_start(j), jj = 8 * J + j;
+        v = p < j ? R(8 * J + p, jj) : p == j ? R(jj, jj) : p == j + 1 ? 1.0 / R(jj, jj) : 0.0;
+      } else if (w < 64) {
         v = R(8 * J + w / 8, 8 * J + w % 8);
       } else if (w >= 80) {
         v = 0.0;
@@ -99,18 +97,6 @@ __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int 
 
 __global__ void pack_status_kernel(const int* bad_min, int n, DevStatus* st) {
   if (*bad_min < n) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, *bad_min);
-}
-
-__device__ __forceinline__ double fast_div(double y, double d, double inv, bool safe) {
-  const double ay = fabs(y);
-  if (!safe || !(ay >= 0x1p-900 && ay <= 0x1p+900)) {
-    return (y == 0.0 && safe) ? y * inv : y / d;
-  }
-  const double q0 = y * inv;
-  double r = fma(-q0, d, y);
-  const double q1 = fma(r, inv, q0);
-  r = fma(-q1, d, y);
-  return fma(r, inv, q1);
 }
 
 template <int NP, int MG, int WPC, bool BSMEM>
@@ -249,21 +235,12 @@ __global__ void __launch_bounds__(WPC * 32) trisolve_kernel(const double* in, lo
 //     blocks with DMMA; the 8-block window rotates so the loop is not unrolled.
 // Every element therefore receives k = 0, 1, ..., j-1 in ascending order, the
 // in-block terms last, then the division: the reference recurrence exactly.
-__device__ __forceinline__ bool div_exponent_ok(double y) {
-  const unsigned e = ((unsigned)__double2hiint(y) >> 20) & 0x7ffu;  // |y| in [2^-899, 2^900]
-  return e - 124u < 1800u;
-}
-
-// Straight-line correctly rounded division for the fast path (inv = RN(1/d),
-// d in [2^-500, 2^500]); `ok` is false when y needs the IEEE fallback.
-__device__ __forceinline__ double div_fast(double y, double d, double inv, bool& ok) {
-  const double q0 = y * inv;
-  double r = fma(-q0, d, y);
-  const double q1 = fma(r, inv, q0);
-  r = fma(-q1, d, y);
-  const double q = fma(r, inv, q1);
-  ok = div_exponent_ok(y);
-  return q;
+// The 8-column staging tile of a warp: row-major, 64 bytes per row, its four
+// 16-byte chunks XOR-swizzled by bits 1-2 of the row so that the C-fragment
+// stores, the row-per-lane loads/stores and the A-fragment loads are all
+// bank-conflict free.
+__device__ __forceinline__ int swz(int row, int u) {
+  return row * 8 + 2 * (u ^ ((((row >> 1) & 1) << 1) | ((row >> 2) & 1)));
 }
 
 template <int NP, int WPC, bool BSMEM, bool SGN, int WIN, int MG>
@@ -278,14 +255,13 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   constexpr int NPASS = NT / W;
   constexpr int NB = BSMEM ? NT * (NT - 1) * 32 : 0;
   constexpr int ND = NT * kDiagStride;
-  constexpr int LDS_ = 8 + 2;
   extern __shared__ __align__(16) double smem[];
   if (failed(st)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, gr = lane >> 2;
   double* sD = smem;
   const double* sB = bpack;
-  double* sS = smem + ND + NB + warp * RW * LDS_;
+  double* sS = smem + ND + NB + warp * RW * 8;
   for (int e = threadIdx.x; e < ND; e += WPC * 32) sD[e] = dpack[e];
   if constexpr (BSMEM) {
     for (int e = threadIdx.x; e < NB; e += WPC * 32) smem[ND + e] = bpack[e];
@@ -361,17 +337,16 @@ __global__ void __launch_bounds__(WPC * 32, 1)
         const int J = W * P + Jl;
 #pragma unroll
         for (int g = 0; g < MG; ++g)
-          *reinterpret_cast<double2*>(sS + (g * 8 + gr) * LDS_ + 2 * q) = make_double2(acc[g][0][0], acc[g][0][1]);
+          *reinterpret_cast<double2*>(sS + swz(g * 8 + gr, q)) = make_double2(acc[g][0][0], acc[g][0][1]);
         __syncwarp();
         {
           const double* D = sD + J * kDiagStride;
           double y[RPL][8];
 #pragma unroll
           for (int rr = 0; rr < RPL; ++rr) {
-            const double* xr = sS + (lane + 32 * rr) * LDS_;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const double2 v = *reinterpret_cast<const double2*>(xr + 2 * u);
+              const double2 v = *reinterpret_cast<const double2*>(sS + swz(lane + 32 * rr, u));
               y[rr][2 * u] = v.x;
               y[rr][2 * u + 1] = v.y;
             }
@@ -379,15 +354,22 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           bool good = D[80] != 0.0;  // uniform: no zero in the strict upper block, safe divisors
           if (good) {
             bool ok = true;
+            const double* Dc = D + kColBase;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const double d = D[j * 8 + j], inv = D[64 + j];
+              double v[10];  // column j: R[0..j-1][j], R_jj, RN(1/R_jj), as 16-byte loads
+#pragma unroll
+              for (int h = 0; h < (j + 3) / 2; ++h) {
+                const double2 t = *reinterpret_cast<const double2*>(Dc + col_start(j) + 2 * h);
+                v[2 * h] = t.x;
+                v[2 * h + 1] = t.y;
+              }
 #pragma unroll
               for (int rr = 0; rr < RPL; ++rr) {
 #pragma unroll
-                for (int kk = 0; kk < j; ++kk) y[rr][j] = fma(-D[kk * 8 + j], y[rr][kk], y[rr][j]);
+                for (int kk = 0; kk < j; ++kk) y[rr][j] = fma(-v[kk], y[rr][kk], y[rr][j]);
                 bool okj;
-                y[rr][j] = div_fast(y[rr][j], d, inv, okj);
+                y[rr][j] = div_fast(y[rr][j], v[j], v[j + 1], okj);
                 ok &= okj;
               }
             }
@@ -396,9 +378,8 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           if (!good) {  // rare: zeros in the block, extreme exponents or exact zeros
 #pragma unroll
             for (int rr = 0; rr < RPL; ++rr) {
-              const double* xr = sS + (lane + 32 * rr) * LDS_;
 #pragma unroll
-              for (int j = 0; j < 8; ++j) y[rr][j] = xr[j];
+              for (int j = 0; j < 8; ++j) y[rr][j] = sS[swz(lane + 32 * rr, j >> 1) + (j & 1)];
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
 #pragma unroll
@@ -414,26 +395,31 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 #pragma unroll
           for (int rr = 0; rr < RPL; ++rr) {
             const int rl = lane + 32 * rr;
-            double* xr = sS + rl * LDS_;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              *reinterpret_cast<double2*>(xr + 2 * u) = make_double2(y[rr][2 * u], y[rr][2 * u + 1]);
-            if (rl < rows) {
-              double* o = out + (row0 + rl) * ldo + 8 * J;
+              *reinterpret_cast<double2*>(sS + swz(rl, u)) = make_double2(y[rr][2 * u], y[rr][2 * u + 1]);
+          }
+        }
+        __syncwarp();
+        // write the solved block back, 8 rows x 64 bytes per store (the tile in C-fragment order)
+        {
+          const int c = 8 * J + 2 * q;
+          double s0 = 1.0, s1 = 1.0;
+          if constexpr (SGN) {
+            s0 = c < n ? sgn[c] : 1.0;
+            s1 = c + 1 < n ? sgn[c + 1] : 1.0;
+          }
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int c = 8 * J + 2 * u;
-                double v0 = y[rr][2 * u], v1 = y[rr][2 * u + 1];
-                if constexpr (SGN) {
-                  if (c < n) v0 *= sgn[c];
-                  if (c + 1 < n) v1 *= sgn[c + 1];
-                }
-                if (vec16 && c + 1 < n) {
-                  *reinterpret_cast<double2*>(o + 2 * u) = make_double2(v0, v1);
-                } else {
-                  if (c < n) o[2 * u] = v0;
-                  if (c + 1 < n) o[2 * u + 1] = v1;
-                }
+          for (int g = 0; g < MG; ++g) {
+            const int r = g * 8 + gr;
+            if (r < rows) {
+              const double2 v = *reinterpret_cast<const double2*>(sS + swz(r, q));
+              double* o = out + (row0 + r) * ldo + c;
+              if (vec16 && c + 1 < n) {
+                *reinterpret_cast<double2*>(o) = make_double2(v.x * s0, v.y * s1);
+              } else {
+                if (c < n) o[0] = v.x * s0;
+                if (c + 1 < n) o[1] = v.y * s1;
               }
             }
           }
@@ -443,7 +429,7 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 #pragma unroll
         for (int g = 0; g < MG; ++g)
 #pragma unroll
-          for (int kk4 = 0; kk4 < 2; ++kk4) af[g][kk4] = sS[(g * 8 + gr) * LDS_ + 4 * kk4 + q];
+          for (int kk4 = 0; kk4 < 2; ++kk4) af[g][kk4] = sS[swz(g * 8 + gr, 2 * kk4 + (q >> 1)) + (q & 1)];
         const double* bcol = sB + (2 * J) * 32 + lane;
 #pragma unroll
         for (int t = 1; t < W; ++t) {
@@ -473,7 +459,7 @@ template <int NP, int WPC, bool BSMEM, int WIN = 8, int MG = 4>
 cudaError_t launch_trisolve_sb_t(const TrisolveArgs& a, cudaStream_t s) {
   constexpr int NT = NP / 8;
   const size_t smem =
-      (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * 10) * sizeof(double);
+      (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * 8) * sizeof(double);
   auto k = a.sgn ? trisolve_sb_kernel<NP, WPC, BSMEM, true, WIN, MG>
                  : trisolve_sb_kernel<NP, WPC, BSMEM, false, WIN, MG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -545,22 +531,25 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   const int nt = np / 8;
   a.bpack = a.pack;
   a.dpack = a.pack + (size_t)nt * (nt - 1) * 32;
+  if ((a.variant == 0 || a.variant >= 8) && trisolve_tma_eligible(a, np)) {
+    const cudaError_t e = launch_trisolve_tma(a, np, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (a.variant == 2) {  // 32-column passes, 16 warps
     switch (np) {
       case 64: return launch_trisolve_sb_t<64, 16, true, 4>(a, s);
       case 128: return launch_trisolve_sb_t<128, 16, true, 4>(a, s);
       case 256: return launch_trisolve_sb_t<256, 16, false, 4>(a, s);
-      case 512: return launch_trisolve_sb_t<512, 16, false, 4>(a, s);
     }
   }
-  if (a.variant == 3) {  // 32-column passes, 64 rows per warp (2 rows per lane in the recurrence)
+  if (a.variant == 3) {  // 64-column passes, 8 warps
     switch (np) {
-      case 64: return launch_trisolve_sb_t<64, 8, true, 4, 8>(a, s);
-      case 128: return launch_trisolve_sb_t<128, 8, true, 4, 8>(a, s);
-      case 256: return launch_trisolve_sb_t<256, 8, false, 4, 8>(a, s);
+      case 64: return launch_trisolve_sb_t<64, 8, true, 8>(a, s);
+      case 128: return launch_trisolve_sb_t<128, 8, true, 8>(a, s);
+      case 256: return launch_trisolve_sb_t<256, 8, false, 8>(a, s);
     }
   }
-  if (a.variant == 1) {  // left-looking (smem panel), kept for comparison and n = 512
+  if (a.variant == 1) {  // left-looking (smem panel), kept for comparison
     switch (np) {
       case 8: return launch_trisolve_t<8, 2, 16, true>(a, s);
       case 16: return launch_trisolve_t<16, 2, 16, true>(a, s);
@@ -570,13 +559,14 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
       case 256: return launch_trisolve_t<256, 2, 5, false>(a, s);
     }
   }
+  // register kernel (best measured configuration per width)
   switch (np) {
     case 8: return launch_trisolve_sb_t<8, 12, true>(a, s);
     case 16: return launch_trisolve_sb_t<16, 12, true>(a, s);
     case 32: return launch_trisolve_sb_t<32, 16, true, 4>(a, s);
     case 64: return launch_trisolve_sb_t<64, 16, true, 4>(a, s);
-    case 128: return launch_trisolve_sb_t<128, 16, true, 4>(a, s);
-    case 256: return launch_trisolve_sb_t<256, 8, false>(a, s);
+    case 128: return launch_trisolve_sb_t<128, 12, true, 4>(a, s);
+    case 256: return launch_trisolve_sb_t<256, 12, false, 4>(a, s);
     case 512: return launch_trisolve_sb_t<512, 8, false>(a, s);
   }
   return cudaErrorInvalidValue;

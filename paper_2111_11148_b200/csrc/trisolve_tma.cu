@@ -1,0 +1,357 @@
+// trisolve_tma.cu — the super-block right trisolve X R = A with TMA-staged
+// tiles (the default when A and X are TMA-addressable: 16-byte aligned bases,
+// even leading dimensions).
+//
+// Same arithmetic as trisolve_sb_kernel (trisolve.cu) — per element k = 0..j-1
+// ascending through DMMA chains, the in-block terms as scalar fma, then the
+// correctly rounded division: the reference recurrence (kernels.hpp:116-123)
+// bit for bit. What changes is how the tall data moves, because the register
+// kernel is bound by the L1 data pipe (profiles/r01_trisolve_tma.md):
+//  * a pass's input columns arrive by TMA as 8-column x 32-row tiles and are read
+//    into the DMMA accumulators with conflict-free 16-byte shared loads;
+//  * the left-looking operand (this warp's already-solved columns) streams
+//    back by TMA as 4-column x 32-row slabs, double buffered, so each DMMA A
+//    fragment is one conflict-free 8-byte shared load instead of an 8-line
+//    global load;
+//  * each solved 8-column block leaves through a TMA tensor store from the
+//    64-byte-swizzled staging tile that the diagonal recurrence already uses.
+// A warp owns 32 rows; its TMA traffic is issued by lane 0 and tracked with
+// two mbarriers (loads) and bulk async-groups (stores).
+
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tma.cuh"
+#include "trisolve_common.cuh"
+
+namespace cqr {
+
+namespace {
+using namespace tri;
+
+// TMA SWIZZLE_64B layout of an 8-column tile (64-byte rows): 16-byte chunk u
+// of row r sits at chunk u ^ ((r >> 1) & 3).
+__device__ __forceinline__ int swz64(int r, int u) { return r * 8 + 2 * (u ^ ((r >> 1) & 3)); }
+
+constexpr int kRW = 32;                  // rows per warp
+constexpr int kTile = kRW * 8;           // doubles in an 8-column tile (2 KB)
+constexpr int kSlab = kRW * 4;           // doubles in a 4-column slab (1 KB)
+constexpr int kWarpDoubles = 6 * kTile;  // 2 staging tiles + an 8 KB input / left-looking buffer
+
+template <int NP, bool BSMEM>
+constexpr int head_doubles() {
+  return ((NP / 8) * kDiagStride + (BSMEM ? (NP / 8) * (NP / 8 - 1) * 32 : 0) + 127) / 128 * 128;
+}
+
+template <int NP, int WPC, bool BSMEM, bool SGN>
+__global__ void __launch_bounds__(WPC * 32, 1)
+    trisolve_tma_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_ll,
+                        const __grid_constant__ CUtensorMap tm_st, long long m, int n,
+                        const double* __restrict__ bpack, const double* __restrict__ dpack,
+                        const double* __restrict__ sgn, const DevStatus* st) {
+  constexpr int NT = NP / 8;
+  constexpr int W = NT < 4 ? NT : 4;  // blocks per pass
+  constexpr int NPASS = NT / W;
+  constexpr int NB = BSMEM ? NT * (NT - 1) * 32 : 0;
+  constexpr int ND = NT * kDiagStride;
+  constexpr int HEAD = head_doubles<NP, BSMEM>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (failed(st)) return;
+  double* smem = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 3, gr = lane >> 2;
+  double* sD = smem;
+  const double* sB = bpack;
+  double* sT = smem + HEAD + warp * kWarpDoubles;  // two staging tiles
+  double* sL = sT + 2 * kTile;                     // input tiles / left-looking slabs
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + HEAD + WPC * kWarpDoubles) + 2 * warp;
+  for (int e = threadIdx.x; e < ND; e += WPC * 32) sD[e] = dpack[e];
+  if constexpr (BSMEM) {
+    for (int e = threadIdx.x; e < NB; e += WPC * 32) smem[ND + e] = bpack[e];
+    sB = smem + ND;
+  }
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_shared();
+  }
+  __syncthreads();
+
+  auto sgn_at = [&](int c) -> double { return c < n ? __ldg(sgn + c) : 1.0; };
+  // left-looking chunk ch (columns 16ch .. 16ch+15) -> buffer b, four slabs
+  auto issue_ll = [&](int ch, int b, int row0) {
+    mbar_expect_tx(bar + b, 4 * kSlab * 8);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) tma_load_2d(sL + b * 2 * kTile + s * kSlab, &tm_ll, 16 * ch + 4 * s, row0, bar + b);
+  };
+
+  // the input tiles of (pass P, group grp) -> sL on bar[0]
+  auto issue_in = [&](int P, long long grp) {
+    mbar_expect_tx(bar, W * kTile * 8);
+#pragma unroll
+    for (int t = 0; t < W; ++t) tma_load_2d(sL + t * kTile, &tm_in, 8 * W * P + 8 * t, (int)(grp * kRW), bar);
+  };
+
+  uint32_t ph0 = 0, ph1 = 0;
+  const long long groups = (m + kRW - 1) / kRW;
+  const long long gstride = (long long)gridDim.x * WPC;
+  long long grp = (long long)blockIdx.x * WPC + warp;
+  if (lane == 0 && grp < groups) issue_in(0, grp);
+  for (; grp < groups; grp += gstride) {
+    const int row0 = (int)(grp * kRW);
+#pragma unroll 1
+    for (int P = 0; P < NPASS; ++P) {
+      const int c0 = 8 * W * P;
+      // 1. the pass's input columns (zero-filled beyond m and n), prefetched
+      mbar_wait(bar, ph0);
+      ph0 ^= 1;
+      double acc[4][W][2];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+          const double2 v = *reinterpret_cast<const double2*>(sL + t * kTile + (8 * g + gr) * 8 + 2 * q);
+          acc[g][t][0] = v.x;
+          acc[g][t][1] = v.y;
+        }
+      // 2. left-looking: k in [0, c0) ascending, from this warp's stored rows
+      if (P > 0) {
+        const int nch = c0 / 16;
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          bulk_wait<0>();  // this warp's earlier blocks have landed in global memory
+          fence_async_global();
+          issue_ll(0, 0, row0);
+          if (nch > 1) issue_ll(1, 1, row0);
+        }
+#pragma unroll 1
+        for (int ch = 0; ch < nch; ++ch) {
+          const int b = ch & 1;
+          if (b == 0) {
+            mbar_wait(bar, ph0);
+            ph0 ^= 1;
+          } else {
+            mbar_wait(bar + 1, ph1);
+            ph1 ^= 1;
+          }
+          const double* buf = sL + b * 2 * kTile;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const int k4 = 4 * ch + s;
+            double af[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) af[g] = buf[s * kSlab + (8 * g + gr) * 4 + q];
+            if constexpr (SGN) {
+              const double sv = sgn_at(4 * k4 + q);  // undo the stored sign (exact)
+#pragma unroll
+              for (int g = 0; g < 4; ++g) af[g] *= sv;
+            }
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+              const int JJ = W * P + t;
+              const int bi = (JJ * (JJ - 1) + k4) * 32 + lane;
+              const double bv = BSMEM ? sB[bi] : __ldg(sB + bi);
+#pragma unroll
+              for (int g = 0; g < 4; ++g) dmma(acc[g][t][0], acc[g][t][1], af[g], bv);
+            }
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0 && ch + 2 < nch) issue_ll(ch + 2, b, row0);
+        }
+      }
+      // prefetch the next pass's input (sL is free again)
+      {
+        const bool last = P + 1 == NPASS;
+        if (!last || grp + gstride < groups) {
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) issue_in(last ? 0 : P + 1, last ? grp + gstride : grp);
+        }
+      }
+      // 3. right-looking inside the pass
+#pragma unroll 1
+      for (int Jl = 0; Jl < W; ++Jl) {
+        const int J = W * P + Jl;
+        double* tile = sT + (J & 1) * kTile;
+        if (lane == 0) {
+          if constexpr (NT == 1)
+            bulk_wait_read<0>();
+          else
+            bulk_wait_read<1>();  // the store that last used this tile has read it
+        }
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          *reinterpret_cast<double2*>(tile + swz64(8 * g + gr, q)) = make_double2(acc[g][0][0], acc[g][0][1]);
+        __syncwarp();
+        {
+          const double* D = sD + J * kDiagStride;
+          double y[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double2 v = *reinterpret_cast<const double2*>(tile + swz64(lane, u));
+            y[2 * u] = v.x;
+            y[2 * u + 1] = v.y;
+          }
+          bool good = D[80] != 0.0;  // uniform: no zero in the strict upper block, safe divisors
+          if (good) {
+            bool ok = true;
+            const double* Dc = D + kColBase;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              double v[10];
+#pragma unroll
+              for (int h = 0; h < (j + 3) / 2; ++h) {
+                const double2 t2 = *reinterpret_cast<const double2*>(Dc + col_start(j) + 2 * h);
+                v[2 * h] = t2.x;
+                v[2 * h + 1] = t2.y;
+              }
+#pragma unroll
+              for (int kk = 0; kk < j; ++kk) y[j] = fma(-v[kk], y[kk], y[j]);
+              bool okj;
+              y[j] = div_fast(y[j], v[j], v[j + 1], okj);
+              ok &= okj;
+            }
+            good = __all_sync(0xffffffffu, ok);
+          }
+          if (!good) {  // rare: zeros in the block, extreme exponents or exact zeros
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] = tile[swz64(lane, j >> 1) + (j & 1)];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+#pragma unroll
+              for (int kk = 0; kk < j; ++kk) {
+                const double rv = D[kk * 8 + j];
+                if (rv != 0.0) y[j] = fma(-rv, y[kk], y[j]);
+              }
+              y[j] = fast_div(y[j], D[j * 8 + j], D[64 + j], D[72 + j] != 0.0);
+            }
+          }
+          if constexpr (SGN) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] *= sgn_at(8 * J + j);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<double2*>(tile + swz64(lane, u)) = make_double2(y[2 * u], y[2 * u + 1]);
+        }
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tm_st, 8 * J, row0, tile);
+          bulk_commit();
+        }
+        double af[4][2];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+          for (int kk4 = 0; kk4 < 2; ++kk4) {
+            af[g][kk4] = tile[swz64(8 * g + gr, 2 * kk4 + (q >> 1)) + (q & 1)];
+            if constexpr (SGN) af[g][kk4] *= sgn_at(8 * J + 4 * kk4 + q);
+          }
+        const double* bcol = sB + (2 * J) * 32 + lane;
+#pragma unroll
+        for (int t = 1; t < W; ++t) {
+          if (Jl + t < W) {
+            const int JJ = J + t;
+            const double* bp = bcol + (JJ * (JJ - 1)) * 32;
+#pragma unroll
+            for (int kk4 = 0; kk4 < 2; ++kk4) {
+              const double bv = BSMEM ? bp[kk4 * 32] : __ldg(bp + kk4 * 32);
+#pragma unroll
+              for (int g = 0; g < 4; ++g) dmma(acc[g][t][0], acc[g][t][1], af[g][kk4], bv);
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            acc[g][t - 1][0] = acc[g][t][0];
+            acc[g][t - 1][1] = acc[g][t][1];
+          }
+        }
+      }
+    }
+  }
+  if (lane == 0) bulk_wait<0>();
+  __syncwarp();
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+template <int NP, int WPC, bool BSMEM>
+cudaError_t launch_t(const TrisolveArgs& a, cudaStream_t s) {
+  CUtensorMap tin, tll, tst;
+  if (!make_tmap_2d(&tin, a.in, a.n, a.m, a.ldi, 8, kRW, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_tmap_2d(&tll, a.out, a.n, a.m, a.ldo, 4, kRW, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_tmap_2d(&tst, a.out, a.n, a.m, a.ldo, 8, kRW, CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorNotSupported;
+  const size_t smem = (size_t)(head_doubles<NP, BSMEM>() + WPC * kWarpDoubles) * 8 + WPC * 16 + 1024;
+  auto k = a.sgn ? trisolve_tma_kernel<NP, WPC, BSMEM, true> : trisolve_tma_kernel<NP, WPC, BSMEM, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long groups = (a.m + kRW - 1) / kRW;
+  long long grid = (groups + WPC - 1) / WPC;
+  if (grid > (long long)a.num_sms) grid = a.num_sms;
+  if (grid < 1) grid = 1;
+  k<<<(unsigned)grid, WPC * 32, smem, s>>>(tin, tll, tst, a.m, a.n, a.bpack, a.dpack, a.sgn, a.status);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool make_tmap_2d(CUtensorMap* map, const double* base, long long cols, long long rows, long long ld, int box_cols,
+                  int box_rows, CUtensorMapSwizzle swizzle) {
+  auto fn = encode_fn();
+  if (!fn || ((uintptr_t)base & 15) || ((ld * 8) & 15) || cols < 1 || rows < 1 || ld < cols) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool trisolve_tma_eligible(const TrisolveArgs& a, int np) {
+  return np >= 32 && a.m <= (1LL << 31) - 64 && ((uintptr_t)a.in & 15) == 0 && ((uintptr_t)a.out & 15) == 0 &&
+         (a.ldi & 1) == 0 && (a.ldo & 1) == 0 && encode_fn() != nullptr;
+}
+
+cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s) {
+  if (a.variant == 8) {  // tuning: 16 warps, R tiles through L1
+    switch (np) {
+      case 64: return launch_t<64, 16, false>(a, s);
+      case 128: return launch_t<128, 16, false>(a, s);
+    }
+  }
+  if (a.variant == 9) {  // tuning: 12 warps, R tiles through L1
+    switch (np) {
+      case 64: return launch_t<64, 12, false>(a, s);
+      case 128: return launch_t<128, 12, false>(a, s);
+    }
+  }
+  switch (np) {
+    case 32: return launch_t<32, 16, true>(a, s);
+    case 64: return launch_t<64, 12, true>(a, s);
+    case 128: return launch_t<128, 12, true>(a, s);
+    case 256: return launch_t<256, 12, false>(a, s);
+    case 512: return launch_t<512, 12, false>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace cqr
