@@ -278,7 +278,7 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
   cqr::GramPlan p = cqr::gram_plan(m, n);
   double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.workspace_doubles, 1));
   int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
-  const int key = p.np * 100000 + p.parts * 100 + p.maxt;
+  const int key = p.np * 1000000 + p.wpc * 10000 + p.parts * 100 + p.maxt;
   if (c->tiles_key != key) {  // the table depends on (np, parts, maxt) only: upload once
     std::vector<int32_t> ht(p.tiles_bytes / sizeof(int32_t));
     cqr::gram_tiles(p, ht.data());
@@ -295,13 +295,13 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
         const int leaf1 = (i + 1 == pj->bounds.size()) ? p.leaves : (int)(pj->bounds[i] / 1024);
         if (leaf1 > leaf)
           LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
-                                            c->stream, leaf, leaf1));
+                                            c->stream, leaf, leaf1, c->num_sms));
         leaf = std::max(leaf, leaf1);
       }
     } else {
       if (pj) wait_all(*pj);
       LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
-                                        c->stream));
+                                        c->stream, 0, -1, c->num_sms));
     }
     LAUNCH(c, cqr::launch_gram_combine(p, part, g, (c->world <= 1 || c->local_only) ? 1 : 0, c->status, c->stream));
     ++c->launches;

@@ -14,6 +14,9 @@
 //
 // HBM bytes per row: 8n; flops: n(n+1) per row (upper triangle incl. diagonal).
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -108,6 +111,101 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
   }
 }
 
+// Persistent variant (the default where the tile count divides evenly over the
+// warps): one CTA per SM walks the leaves blockIdx.x, +gridDim.x, ...; the row
+// chunks of consecutive leaves form one cp.async stream, so the next leaf's
+// first chunk loads during the current leaf's last. Same per-leaf arithmetic as
+// gram_leaf_kernel (the partials are identical); balanced waves: 977 leaves
+// (c1) over 148 CTAs is 6.6 per CTA instead of 3.3 per slot over 2 per SM.
+template <int NP, int WPC, int MAXT, int CH, bool CHECK>
+__global__ void __launch_bounds__(WPC * 32, 1)
+    gram_leaf_p_kernel(const double* __restrict__ x, long long ldx, long long m, int n,
+                       const int32_t* __restrict__ tiles, double* __restrict__ partial, int vec16, int leaf0,
+                       int leaf1, DevStatus* st) {
+  constexpr int LDX = NP + 4;
+  constexpr int NTH = WPC * 32;
+  extern __shared__ __align__(16) double smem[];
+  if (failed(st)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, gr = lane >> 2;
+  int leaf = leaf0 + blockIdx.x;
+  if (leaf >= leaf1) return;
+  int mt[MAXT];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) mt[t] = tiles[warp * MAXT + t];
+  double acc[MAXT][4][2];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  auto leaf_rows = [&](int lf) { return (int)min((long long)kLeafRows, m - (long long)lf * kLeafRows); };
+  auto stage = [&](int lf, int c, int buf) {
+    const int rows = leaf_rows(lf);
+    stage_rows(smem + buf * CH * LDX, LDX, x + ((long long)lf * kLeafRows + (long long)c * CH) * ldx, ldx,
+               min(CH, rows - c * CH), CH, n, NP, tid, NTH, vec16 != 0);
+    cp_async_commit();
+  };
+  bool bad = false;
+  int c = 0, buf = 0;
+  stage(leaf, 0, 0);
+  while (true) {
+    const int nch = (leaf_rows(leaf) + CH - 1) / CH;
+    int nleaf = leaf, nc = c + 1;
+    if (nc == nch) {
+      nleaf = leaf + gridDim.x;
+      nc = 0;
+    }
+    if (nleaf < leaf1) {
+      stage(nleaf, nc, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int boff = buf * CH * LDX;
+#pragma unroll 2
+    for (int k4 = 0; k4 < CH / 4; ++k4) {
+      const int xo = boff + (4 * k4 + q) * LDX + gr;
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        if (mt[t] < 0) continue;
+        const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
+        const double a0 = smem[xo + 16 * I2], a1 = smem[xo + 16 * I2 + 8];
+        const double b0 = smem[xo + 16 * J2], b1 = smem[xo + 16 * J2 + 8];
+        if constexpr (CHECK) bad |= nonfinite(a0) | nonfinite(a1) | nonfinite(b0) | nonfinite(b1);
+        dmma(acc[t][0][0], acc[t][0][1], a0, b0);
+        dmma(acc[t][1][0], acc[t][1][1], a0, b1);
+        if (I2 != J2) dmma(acc[t][2][0], acc[t][2][1], a1, b0);
+        dmma(acc[t][3][0], acc[t][3][1], a1, b1);
+      }
+    }
+    __syncthreads();
+    if (nc == 0) {  // leaf done: write its partial, restart the chains
+      double* out = partial + (long long)leaf * NP * NP;
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        if (mt[t] < 0) continue;
+        const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int si = u >> 1, sj = u & 1;
+          if (I2 == J2 && si == 1 && sj == 0) continue;
+          const int i = 16 * I2 + 8 * si + gr, j = 16 * J2 + 8 * sj + 2 * q;
+          *reinterpret_cast<double2*>(out + i * NP + j) = make_double2(acc[t][u][0], acc[t][u][1]);
+          acc[t][u][0] = acc[t][u][1] = 0.0;
+        }
+      }
+    }
+    leaf = nleaf;
+    c = nc;
+    buf ^= 1;
+    if (leaf >= leaf1) break;
+  }
+  if constexpr (CHECK) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
+  }
+}
+
 // The pairwise tree of kernels.hpp:42-57 in streaming form: after pushing leaf
 // i, merge (top-1) + top once per trailing zero of (i+1); at the end fold the
 // stack right to left. Two levels for parallelism: level A folds each aligned
@@ -189,6 +287,22 @@ cudaError_t launch_leaves_t(const GramPlan& p, const double* x, long long ldx, c
   return cudaGetLastError();
 }
 
+template <int NP, int WPC, int MAXT, int CH>
+cudaError_t launch_leaves_p(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
+                            double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s, int leaf0,
+                            int leaf1, int num_sms) {
+  if (leaf1 < 0) leaf1 = p.leaves;
+  if (leaf1 <= leaf0) return cudaSuccess;
+  const size_t smem = (size_t)2 * CH * (NP + 4) * sizeof(double);
+  auto k = check ? gram_leaf_p_kernel<NP, WPC, MAXT, CH, true> : gram_leaf_p_kernel<NP, WPC, MAXT, CH, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = std::min(leaf1 - leaf0, num_sms);
+  k<<<(unsigned)grid, WPC * 32, smem, s>>>(x, ldx, p.m, p.n, tiles, partial, vec16, leaf0, leaf1,
+                                           const_cast<DevStatus*>(st));
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 GramPlan gram_plan(long long m, int n) {
@@ -197,23 +311,32 @@ GramPlan gram_plan(long long m, int n) {
   p.m = m;
   p.np = gram_np(n);
   p.leaves = (int)((m + kLeafRows - 1) / kLeafRows);
-  p.wpc = kWpc;
   const int nm = p.np / 16;
   const int macros = nm * (nm + 1) / 2;
-  const int cap = 9;
-  p.parts = (macros + kWpc * cap - 1) / (kWpc * cap);
-  int maxt = (macros + kWpc * p.parts - 1) / (kWpc * p.parts);
-  p.maxt = maxt <= 1 ? 1 : maxt <= 2 ? 2 : maxt <= 5 ? 5 : 9;
-  p.ch = p.np <= 128 ? 32 : 16;
+  static const bool legacy = std::getenv("CQR_GRAM_LEGACY") != nullptr;  // tuning: the per-leaf kernel
+  if (p.np == 128 && !legacy) {  // persistent: the 36 macro tiles divide evenly over 12 warps (measured: n = 64 is faster per leaf)
+    p.persistent = 1;
+    p.wpc = p.np == 64 ? 10 : 12;
+    p.parts = 1;
+    p.maxt = macros / p.wpc;
+    p.ch = 32;
+  } else {
+    p.wpc = kWpc;
+    const int cap = 9;
+    p.parts = (macros + kWpc * cap - 1) / (kWpc * cap);
+    int maxt = (macros + kWpc * p.parts - 1) / (kWpc * p.parts);
+    p.maxt = maxt <= 1 ? 1 : maxt <= 2 ? 2 : maxt <= 5 ? 5 : 9;
+    p.ch = p.np <= 128 ? 32 : 16;
+  }
   p.partial_doubles = (size_t)p.leaves * p.np * p.np;
   p.workspace_doubles = p.partial_doubles + (size_t)((p.leaves + kGroup - 1) / kGroup) * p.np * p.np;
-  p.tiles_bytes = (size_t)p.parts * kWpc * p.maxt * sizeof(int32_t);
+  p.tiles_bytes = (size_t)p.parts * p.wpc * p.maxt * sizeof(int32_t);
   return p;
 }
 
 void gram_tiles(const GramPlan& p, int32_t* out) {
   const int nm = p.np / 16;
-  const int slots = p.parts * kWpc;
+  const int slots = p.parts * p.wpc;
   for (int e = 0; e < slots * p.maxt; ++e) out[e] = -1;
   // round-robin the upper macro tiles over (part, warp) slots, filling each slot's list
   int idx = 0;
@@ -227,7 +350,14 @@ void gram_tiles(const GramPlan& p, int32_t* out) {
 
 cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
                                double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s, int leaf0,
-                               int leaf1) {
+                               int leaf1, int num_sms) {
+  if (p.persistent) {
+    if (p.np == 128 && p.maxt == 3)
+      return launch_leaves_p<128, 12, 3, 32>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 64 && p.maxt == 1)
+      return launch_leaves_p<64, 10, 1, 32>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1, num_sms);
+    return cudaErrorInvalidValue;
+  }
 #define CQR_GRAM_CASE(NP_, CH_)                                                                     \
   case NP_:                                                                                          \
     switch (p.maxt) {                                                                                \

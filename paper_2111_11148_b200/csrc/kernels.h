@@ -38,7 +38,7 @@ cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s);
 
 // ---- gram.cu ---------------------------------------------------------------------
 struct GramPlan {
-  int n = 0, np = 0, leaves = 0, parts = 0, maxt = 0, wpc = 0, ch = 0;
+  int n = 0, np = 0, leaves = 0, parts = 0, maxt = 0, wpc = 0, ch = 0, persistent = 0;
   long long m = 0;
   size_t partial_doubles = 0;    // leaves * np * np
   size_t workspace_doubles = 0;  // partials + the per-group sums of the combine
@@ -52,7 +52,7 @@ void gram_tiles(const GramPlan& p, int32_t* out);
 // [leaf0, leaf1): the leaves this launch computes (default all); results are per leaf.
 cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles_dev,
                                double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s,
-                               int leaf0 = 0, int leaf1 = -1);
+                               int leaf0 = 0, int leaf1 = -1, int num_sms = 148);
 // Pairwise tree over leaves (kernels.hpp:42-57, streaming form) -> g upper (ld = n);
 // mirror=1 also writes the lower triangle (kernels.hpp:69).
 cudaError_t launch_gram_combine(const GramPlan& p, double* partial, double* g, int mirror,
