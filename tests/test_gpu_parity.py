@@ -135,10 +135,26 @@ def test_trisolve_identity_and_singular():
     assert e.value.index == 1
 
 
-@pytest.mark.parametrize("l,n,seed", [(2, 2, 1), (30, 10, 2), (128, 64, 3), (256, 128, 4), (300, 150, 5)])
+@pytest.mark.parametrize("l,n,seed", [(2, 2, 1), (30, 10, 2), (128, 64, 3), (256, 128, 4), (300, 150, 5),
+                                      (512, 256, 6), (768, 512, 7), (1100, 40, 8)])
 def test_lu_bitwise(l, n, seed):
     a1 = o.gaussian_matrix(l, n, seed)
     assert np.array_equal(G.lu_u_factor(a1), o.lu_u_factor(a1))
+
+
+@pytest.mark.parametrize("l,n,seed", [(64, 32, 1), (300, 100, 2), (1100, 40, 3), (96, 96, 4)])
+def test_lu_pivot_ties(l, n, seed):
+    # small integers: many equal |pivot| candidates, so the "first maximum in the
+    # reference's swapped row order" rule decides; also exact zero pivots
+    a1 = np.random.default_rng(seed).integers(-2, 3, size=(l, n)).astype(np.float64)
+    try:
+        ref = o.lu_u_factor(a1)
+    except o.OracleError as e:
+        with pytest.raises(G.SingularTriangular) as eg:
+            G.lu_u_factor(a1)
+        assert eg.value.index == e.index
+        return
+    assert np.array_equal(G.lu_u_factor(a1), ref)
 
 
 def test_lu_known_and_singular():
