@@ -277,6 +277,35 @@ inline ParallelRun run_parallel(Method m, const MatrixView& a, int p, const Meth
   return run;
 }
 
+// rng::derive (rng.hpp:36-38)
+inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+inline uint64_t derive(uint64_t seed, uint64_t salt) { return mix64(seed ^ mix64(salt + 0x51ED270B8A5EC473ull)); }
+
+// The RSVD caller's orthogonalizer (apps.hpp:48, apps.cpp:166-196): Q only (r_less);
+// rQR draws a fresh uniform sketch per call, seed derive(seed, 0xA110 + call_counter).
+enum class Orth { HouseholderQr, RqrCholeskyQr, CholeskyQr2 };
+inline Matrix orthonormalize(const MatrixView& y, Orth orth, uint64_t seed, int call_counter, int workers = 1) {
+  Options o;
+  o.r_less = true;
+  o.workers = workers;
+  switch (orth) {
+    case Orth::RqrCholeskyQr: {
+      SketchConfig cfg;
+      cfg.rate = 2.0;
+      cfg.seed = derive(seed, 0xA110 + static_cast<uint64_t>(call_counter));
+      return rqr_cholesky_qr(y, cfg, o).q;
+    }
+    case Orth::CholeskyQr2:
+      return cholesky_qr2(y, o).q;
+    default:
+      throw std::invalid_argument("orthonormalize: HouseholderQr is the dense baseline, not on the device path");
+  }
+}
+
 namespace kernels {  // kernels.hpp
 
 inline Matrix gram(const MatrixView& x) {

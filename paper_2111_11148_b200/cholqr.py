@@ -415,6 +415,45 @@ def rlu_cholesky_qr(a, cfg: SketchConfig, opts: Options | None = None):
     return _factor(Method.RluCholeskyQr, a, cfg, _opts(opts))[0]
 
 
+# ---- the RSVD caller's orthogonalizer (apps.cpp:166-196) ----------------------
+_M64 = (1 << 64) - 1
+
+
+def _mix64(z):
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def derive(seed, salt):
+    """rng::derive (rng.hpp:36-38): mix64(seed ^ mix64(salt + 0x51ED270B8A5EC473))."""
+    return _mix64((seed & _M64) ^ _mix64((salt + 0x51ED270B8A5EC473) & _M64))
+
+
+class Orth:
+    HouseholderQr, RqrCholeskyQr, CholeskyQr2 = 0, 1, 2
+
+
+def orth_name(o):
+    return {Orth.HouseholderQr: "qr", Orth.RqrCholeskyQr: "rqr", Orth.CholeskyQr2: "cholqr2"}[o]
+
+
+def orthonormalize(y, orth, seed, call_counter, workers=1, ctx=None):
+    """apps.cpp:166-196 orthonormalize: Q of Y with R discarded (r_less). rQR
+    draws fresh rows every call: uniform sketch, rate 2, seed
+    derive(seed, 0xA110 + call_counter). Householder QR is the dense baseline,
+    not on the device path (CQR_UNSUPPORTED)."""
+    opts = Options(diagnostics=False, r_less=True, workers=workers)
+    if orth == Orth.RqrCholeskyQr:
+        cfg = SketchConfig(rate=2.0, seed=derive(seed, 0xA110 + int(call_counter)))
+        return _factor(Method.RqrCholeskyQr, y, cfg, _opts(opts), ctx=ctx)[0].q
+    if orth == Orth.CholeskyQr2:
+        return _factor(Method.CholeskyQr2, y, None, _opts(opts), ctx=ctx)[0].q
+    if orth == Orth.HouseholderQr:
+        raise NotImplementedError("orthonormalize: HouseholderQr is the dense baseline, not on the device path")
+    raise ValueError(f"unknown orthogonalizer {orth}")
+
+
 def run_parallel(method, a, p=1, cfg: MethodConfig | None = None, ctx=None):
     """parexec::run_parallel (parexec.hpp:89-90). On one process `p` only sets
     the communication-model counters (the device does not split work by it);

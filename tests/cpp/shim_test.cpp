@@ -94,6 +94,26 @@ int main() {
   Matrix lu(2, 2);
   lu.data = {2, 1, 4, 3};
   CHECK((kernels::lu_u_factor(lu).data == std::vector<double>{4, 3, 0, -0.5}));
+  // the RSVD caller's orthogonalizer: Q of Y equals the r_less factorization with the derived seed
+  {
+    Matrix y(400, 6);
+    for (Index i = 0; i < y.rows; ++i)
+      for (Index j = 0; j < y.cols; ++j) y(i, j) = std::sin(0.37 * (double)(i * 7 + j * 13 + 1)) + (i == j ? 3.0 : 0.0);
+    Matrix q1 = orthonormalize(y, Orth::RqrCholeskyQr, 99, 2);
+    SketchConfig cfg;
+    cfg.seed = derive(99, 0xA110 + 2);
+    Options o;
+    o.r_less = true;
+    CHECK(q1.data == rqr_cholesky_qr(y, cfg, o).q.data);
+    CHECK(orthonormalize(y, Orth::CholeskyQr2, 99, 0).data == cholesky_qr2(y, o).q.data);
+    threw = false;
+    try {
+      (void)orthonormalize(y, Orth::HouseholderQr, 99, 0);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   std::printf("shim_test %s (%d failures)\n", fails ? "FAILED" : "ok", fails);
   return fails ? 1 : 0;
 }

@@ -47,6 +47,13 @@ def test_host_helpers_match_oracle():
         assert cfg.resolved_size(100, 10) == o.resolved_size(cfg._c(), 100, 10)
 
 
+def test_derive_and_orth_names():  # rng.hpp:36-38, apps.cpp:155-162
+    for seed, salt in [(0, 0), (1, 0x5E7C), (2**64 - 1, 0xA110 + 3), (123456789, 7)]:
+        assert G.derive(seed, salt) == o.derive(seed, salt)
+    assert [G.orth_name(x) for x in (G.Orth.HouseholderQr, G.Orth.RqrCholeskyQr, G.Orth.CholeskyQr2)] == \
+        ["qr", "rqr", "cholqr2"]
+
+
 def test_abi_version():
     assert G._lib().cqr_abi_version() == 1
 

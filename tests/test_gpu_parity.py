@@ -357,3 +357,20 @@ def test_launch_count_and_determinism():
     f2 = G.rlu_cholesky_qr(a, G.SketchConfig(strategy=G.Strategy.Gaussian, seed=5))
     assert ctx.launches - before >= 2 * 8
     assert np.array_equal(f1.q, f2.q) and np.array_equal(f1.r, f2.r)
+
+
+@pytest.mark.parametrize("orth", [G.Orth.RqrCholeskyQr, G.Orth.CholeskyQr2])
+def test_orthonormalize_matches_reference_caller(orth):  # apps.cpp:166-196
+    y = o.synthesize(3000, 20, 1e6, 9)
+    seed, calls = 77, [0, 1, 5]
+    for call in calls:
+        q = G.orthonormalize(y, orth, seed, call)
+        if orth == G.Orth.RqrCholeskyQr:
+            cfg = _abi.sketch_cfg(strategy=_abi.UNIFORM, rate=2.0, seed=o.derive(seed, 0xA110 + call))
+            ref = o.factor(_abi.RQR, y, cfg, _abi.options(r_less=True)).q
+            assert np.linalg.norm(q - ref) / math.sqrt(20) <= 1e-10
+        else:
+            ref = o.factor(_abi.CHOLQR2, y, None, _abi.options(r_less=True)).q
+            assert np.array_equal(q, ref)
+    with pytest.raises(NotImplementedError):
+        G.orthonormalize(y, G.Orth.HouseholderQr, seed, 0)
