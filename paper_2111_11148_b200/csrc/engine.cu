@@ -316,7 +316,7 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
 
 // X R = A on device rows; in may alias out.
 void trisolve_dev(cqr_ctx* c, const double* in, long long ldi, double* out, long long ldo, long long m, int n,
-                  const double* pack, const double* sgn) {
+                  const double* pack) {
   if (m <= 0) return;
   cqr::TrisolveArgs t{};
   t.in = in;
@@ -326,7 +326,6 @@ void trisolve_dev(cqr_ctx* c, const double* in, long long ldi, double* out, long
   t.m = m;
   t.n = n;
   t.pack = pack;
-  t.sgn = sgn;
   t.vec16 = (vec_ok(in, ldi, n) && vec_ok(out, ldo, n)) ? 1 : 0;
   t.num_sms = c->num_sms;
   t.status = c->status;
@@ -359,7 +358,7 @@ void check_finite(cqr_ctx* c, const double* a, long long m, int n, long long lda
 
 // One CholeskyQR pass (engine.cpp:78-92): G = X^T X (+shift I), R = chol(G),
 // X <- X R^{-1} (in -> out). shift_mode 0/1/2 as launch_cholesky.
-void final_solve(Job& j, const double* in, long long ldi, const double* pack, const double* sgn);
+void final_solve(Job& j, const double* in, long long ldi, const double* pack);
 
 void cholesky_pass(Job& j, const double* in, long long ldi, Report& rep, double* r_out, int shift_mode,
                    double shift_value, const double* sgn_for_solve = nullptr, bool defer_solve = false,
@@ -387,11 +386,11 @@ void cholesky_pass(Job& j, const double* in, long long ldi, Report& rep, double*
   double* pack = dbuf<double>(c, B_PACK2, cqr::trisolve_pack_doubles(n));
   {
     StageScope t(c, CQR_STAGE_TRISOLVE);
-    LAUNCH(c, cqr::launch_pack_r(r_out, n, n, pack, 0, c->status, c->stream));
+    LAUNCH(c, cqr::launch_pack_r(r_out, n, n, pack, 0, c->status, c->stream, sgn_for_solve));
     if (last)
-      final_solve(j, in, ldi, pack, sgn_for_solve);
+      final_solve(j, in, ldi, pack);
     else
-      trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, n, pack, sgn_for_solve);
+      trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, n, pack);
   }
   push_stage(rep, CQR_STAGE_TRISOLVE);
 }
@@ -399,15 +398,15 @@ void cholesky_pass(Job& j, const double* in, long long ldi, Report& rep, double*
 // The last solve of a factorization; with the host pipeline each row chunk of Q
 // is copied back as soon as it is solved (rows are independent, so the chunked
 // solve is bit-identical).
-void final_solve(Job& j, const double* in, long long ldi, const double* pack, const double* sgn) {
+void final_solve(Job& j, const double* in, long long ldi, const double* pack) {
   cqr_ctx* c = j.c;
   if (!pipelined(j)) {
-    trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, j.n, pack, sgn);
+    trisolve_dev(c, in, ldi, j.q, j.ldq, j.m_local, j.n, pack);
     return;
   }
   for (size_t i = 0; i + 1 < j.bounds.size(); ++i) {
     const long long r0 = j.bounds[i], r1 = j.bounds[i + 1];
-    trisolve_dev(c, in + r0 * ldi, ldi, j.q + r0 * j.ldq, j.ldq, r1 - r0, j.n, pack, sgn);
+    trisolve_dev(c, in + r0 * ldi, ldi, j.q + r0 * j.ldq, j.ldq, r1 - r0, j.n, pack);
     cudaEvent_t e = c->pipe_ev[j.bounds.size() - 1 + i];
     ck(cudaEventRecord(e, c->stream), "record");
     ck(cudaStreamWaitEvent(c->cstream, e, 0), "wait solve");
@@ -575,7 +574,7 @@ Outcome run_precond(Job& j) {
     {
       StageScope t(c, CQR_STAGE_TRISOLVE);
       wait_all(j);
-      trisolve_dev(c, j.a, j.lda, j.q, j.ldq, j.m_local, n, pack1, nullptr);
+      trisolve_dev(c, j.a, j.lda, j.q, j.ldq, j.m_local, n, pack1);
     }
     const bool diag = j.opts.diagnostics != 0;
     // ---- CholeskyQR on X (Gram, Cholesky; the solve is deferred past Recover so
@@ -612,8 +611,8 @@ Outcome run_precond(Job& j) {
     double* pack2 = dbuf<double>(c, B_PACK2, cqr::trisolve_pack_doubles(n));
     {
       StageScope t(c, CQR_STAGE_TRISOLVE);
-      LAUNCH(c, cqr::launch_pack_r(rh, n, n, pack2, 0, c->status, c->stream));
-      final_solve(j, j.q, j.ldq, pack2, r_less ? nullptr : sgn);
+      LAUNCH(c, cqr::launch_pack_r(rh, n, n, pack2, 0, c->status, c->stream, r_less ? nullptr : sgn));
+      final_solve(j, j.q, j.ldq, pack2);  // the column signs are folded into the pack
     }
     push_stage(o.rep, CQR_STAGE_TRISOLVE);
     if (!r_less) push_stage(o.rep, CQR_STAGE_RECOVER);
@@ -1035,7 +1034,7 @@ int cqr_trisolve_inplace_dev(cqr_ctx* c, double* x, int64_t m, int64_t n, int64_
     double* pack = dbuf<double>(c, B_PACK1, cqr::trisolve_pack_doubles((int)n));
     reset_status(c);
     LAUNCH(c, cqr::launch_pack_r(r_dev, (int)n, (int)n, pack, 0, c->status, c->stream));
-    trisolve_dev(c, x, ldx, x, ldx, m, (int)n, pack, nullptr);
+    trisolve_dev(c, x, ldx, x, ldx, m, (int)n, pack);
     DevStatus s = read_status(c);
     if (s.code) {
       idx = s.index;
@@ -1068,7 +1067,7 @@ int cqr_trisolve_inplace(cqr_ctx* c, double* x, int64_t m, int64_t n, int64_t ld
          "X H2D");
     reset_status(c);
     LAUNCH(c, cqr::launch_pack_r(dr, (int)n, (int)n, pack, 0, c->status, c->stream));
-    trisolve_dev(c, dx, n, dx, n, m, (int)n, pack, nullptr);
+    trisolve_dev(c, dx, n, dx, n, m, (int)n, pack);
     DevStatus s = read_status(c);
     if (s.code) throw Fail{s.code, s.index, "singular triangular factor"};
     if (m > 0)

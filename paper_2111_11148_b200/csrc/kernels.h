@@ -14,7 +14,7 @@ struct DevStatus;
 int trisolve_np(int n);                 // padded width bucket of the trisolve kernel
 size_t trisolve_pack_doubles(int n);    // workspace for the packed R
 cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int degenerate, DevStatus* st,
-                          cudaStream_t s);
+                          cudaStream_t s, const double* sgn = nullptr);  // sgn: pack diag(sgn) R
 struct TrisolveArgs {
   const double* in;
   long long ldi;
@@ -25,7 +25,6 @@ struct TrisolveArgs {
   const double* pack;  // from launch_pack_r
   const double* bpack;
   const double* dpack;
-  const double* sgn;  // optional column signs applied to the stored result (normalize_sign)
   int vec16;
   int num_sms;
   const DevStatus* status;

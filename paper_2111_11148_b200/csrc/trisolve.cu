@@ -33,10 +33,13 @@ using namespace tri;
 
 __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int np, double* __restrict__ bpack,
                               double* __restrict__ dpack, int* __restrict__ bad_min, int degenerate,
-                              DevStatus* st) {
+                              const double* __restrict__ sgn, DevStatus* st) {
   if (failed(st)) return;
+  // With column signs s (normalize_sign, engine.cpp:109-116) the pack holds diag(s) R: solving with it gives
+  // Q = X R^-1 diag(s) directly, bit for bit (every product and quotient only changes sign, and
+  // s_k R_kj * s_k x_k == R_kj x_k exactly, zeros included).
   auto R = [&](int i, int j) -> double {
-    if (i < n && j < n) return r[(long long)i * ldr + j];
+    if (i < n && j < n) return sgn ? r[(long long)i * ldr + j] * sgn[i] : r[(long long)i * ldr + j];
     return (i == j) ? 1.0 : 0.0;
   };
   const int nt = np / 8;
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(WPC * 32) trisolve_kernel(const double* in, lo
                                                             long long ldo, long long m, int n,
                                                             const double* __restrict__ bpack,
                                                             const double* __restrict__ dpack,
-                                                            const double* __restrict__ sgn, int vec16,
+                                                            int vec16,
                                                             const DevStatus* st) {
   constexpr int NT = NP / 8;
   constexpr int RW = 8 * MG;
@@ -200,22 +203,17 @@ __global__ void __launch_bounds__(WPC * 32) trisolve_kernel(const double* in, lo
       }
       __syncwarp();
     }
-    // write the solved panel (coalesced rows), applying the column signs
+    // write the solved panel (coalesced rows)
     if (vec16) {
       for (int r = 0; r < rows; ++r)
         for (int c2 = lane; 2 * c2 < n; c2 += 32) {
           double2 v = *reinterpret_cast<const double2*>(sX + r * LDX + 2 * c2);
-          if (sgn) {
-            v.x *= sgn[2 * c2];
-            v.y *= sgn[2 * c2 + 1];
-          }
           *reinterpret_cast<double2*>(out + (row0 + r) * ldo + 2 * c2) = v;
         }
     } else {
       for (int r = 0; r < rows; ++r)
         for (int c = lane; c < n; c += 32) {
           double v = sX[r * LDX + c];
-          if (sgn) v *= sgn[c];
           out[(row0 + r) * ldo + c] = v;
         }
     }
@@ -243,11 +241,11 @@ __device__ __forceinline__ int swz(int row, int u) {
   return row * 8 + 2 * (u ^ ((((row >> 1) & 1) << 1) | ((row >> 2) & 1)));
 }
 
-template <int NP, int WPC, bool BSMEM, bool SGN, int WIN, int MG>
+template <int NP, int WPC, bool BSMEM, int WIN, int MG>
 __global__ void __launch_bounds__(WPC * 32, 1)
     trisolve_sb_kernel(const double* in, long long ldi, double* out, long long ldo, long long m, int n,
                        const double* __restrict__ bpack, const double* __restrict__ dpack,
-                       const double* __restrict__ sgn, int vec16, const DevStatus* st) {
+                       int vec16, const DevStatus* st) {
   constexpr int NT = NP / 8;
   constexpr int RW = 8 * MG;   // rows per warp
   constexpr int RPL = MG / 4;  // rows per lane in the diagonal recurrence (independent chains)
@@ -316,11 +314,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           double af[MG];
 #pragma unroll
           for (int g = 0; g < MG; ++g) af[g] = xrow[g][4 * k4];
-          if constexpr (SGN) {
-            const double s = sgn[4 * k4 + q];
-#pragma unroll
-            for (int g = 0; g < MG; ++g) af[g] *= s;
-          }
 #pragma unroll
           for (int t = 0; t < W; ++t) {
             const int JJ = W * P + t;
@@ -404,11 +397,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
         // write the solved block back, 8 rows x 64 bytes per store (the tile in C-fragment order)
         {
           const int c = 8 * J + 2 * q;
-          double s0 = 1.0, s1 = 1.0;
-          if constexpr (SGN) {
-            s0 = c < n ? sgn[c] : 1.0;
-            s1 = c + 1 < n ? sgn[c + 1] : 1.0;
-          }
 #pragma unroll
           for (int g = 0; g < MG; ++g) {
             const int r = g * 8 + gr;
@@ -416,10 +404,10 @@ __global__ void __launch_bounds__(WPC * 32, 1)
               const double2 v = *reinterpret_cast<const double2*>(sS + swz(r, q));
               double* o = out + (row0 + r) * ldo + c;
               if (vec16 && c + 1 < n) {
-                *reinterpret_cast<double2*>(o) = make_double2(v.x * s0, v.y * s1);
+                *reinterpret_cast<double2*>(o) = v;
               } else {
-                if (c < n) o[0] = v.x * s0;
-                if (c + 1 < n) o[1] = v.y * s1;
+                if (c < n) o[0] = v.x;
+                if (c + 1 < n) o[1] = v.y;
               }
             }
           }
@@ -460,15 +448,14 @@ cudaError_t launch_trisolve_sb_t(const TrisolveArgs& a, cudaStream_t s) {
   constexpr int NT = NP / 8;
   const size_t smem =
       (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * 8) * sizeof(double);
-  auto k = a.sgn ? trisolve_sb_kernel<NP, WPC, BSMEM, true, WIN, MG>
-                 : trisolve_sb_kernel<NP, WPC, BSMEM, false, WIN, MG>;
+  auto k = trisolve_sb_kernel<NP, WPC, BSMEM, WIN, MG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + 8 * MG - 1) / (8 * MG);
   long long grid = (groups + WPC - 1) / WPC;
   if (grid > (long long)a.num_sms) grid = a.num_sms;
   if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, WPC * 32, smem, s>>>(a.in, a.ldi, a.out, a.ldo, a.m, a.n, a.bpack, a.dpack, a.sgn, a.vec16,
+  k<<<(unsigned)grid, WPC * 32, smem, s>>>(a.in, a.ldi, a.out, a.ldo, a.m, a.n, a.bpack, a.dpack, a.vec16,
                                            a.status);
   return cudaGetLastError();
 }
@@ -485,7 +472,7 @@ cudaError_t launch_trisolve_t(const TrisolveArgs& a, cudaStream_t s) {
   long long grid = (groups + WPC - 1) / WPC;
   if (grid > a.num_sms) grid = a.num_sms;
   if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, WPC * 32, smem, s>>>(a.in, a.ldi, a.out, a.ldo, a.m, a.n, a.bpack, a.dpack, a.sgn, a.vec16,
+  k<<<(unsigned)grid, WPC * 32, smem, s>>>(a.in, a.ldi, a.out, a.ldo, a.m, a.n, a.bpack, a.dpack, a.vec16,
                                            a.status);
   return cudaGetLastError();
 }
@@ -509,7 +496,7 @@ size_t trisolve_pack_doubles(int n) {
 }
 
 cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int degenerate, DevStatus* st,
-                          cudaStream_t s) {
+                          cudaStream_t s, const double* sgn) {
   const int np = trisolve_np(n);
   const int nt = np / 8;
   double* bpack = pack;
@@ -521,7 +508,7 @@ cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int deg
   if (grid < 1) grid = 1;
   cudaError_t e = cudaMemsetAsync(bad, 0x7f, sizeof(int), s);  // 0x7f7f7f7f > any n
   if (e != cudaSuccess) return e;
-  pack_r_kernel<<<grid, 256, 0, s>>>(r, ldr, n, np, bpack, dpack, bad, degenerate, st);
+  pack_r_kernel<<<grid, 256, 0, s>>>(r, ldr, n, np, bpack, dpack, bad, degenerate, sgn, st);
   pack_status_kernel<<<1, 1, 0, s>>>(bad, n, st);
   return cudaGetLastError();
 }

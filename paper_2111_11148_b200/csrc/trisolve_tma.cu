@@ -44,12 +44,12 @@ constexpr int head_doubles() {
   return ((NP / 8) * kDiagStride + (BSMEM ? (NP / 8) * (NP / 8 - 1) * 32 : 0) + 127) / 128 * 128;
 }
 
-template <int NP, int WPC, bool BSMEM, bool SGN>
+template <int NP, int WPC, bool BSMEM>
 __global__ void __launch_bounds__(WPC * 32, 1)
     trisolve_tma_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_ll,
                         const __grid_constant__ CUtensorMap tm_st, long long m, int n,
                         const double* __restrict__ bpack, const double* __restrict__ dpack,
-                        const double* __restrict__ sgn, const DevStatus* st) {
+                        const DevStatus* st) {
   constexpr int NT = NP / 8;
   constexpr int W = NT < 4 ? NT : 4;  // blocks per pass
   constexpr int NPASS = NT / W;
@@ -79,7 +79,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   }
   __syncthreads();
 
-  auto sgn_at = [&](int c) -> double { return c < n ? __ldg(sgn + c) : 1.0; };
   // left-looking chunk ch (columns 16ch .. 16ch+15) -> buffer b, four slabs
   auto issue_ll = [&](int ch, int b, int row0) {
     mbar_expect_tx(bar + b, 4 * kSlab * 8);
@@ -144,11 +143,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
             double af[4];
 #pragma unroll
             for (int g = 0; g < 4; ++g) af[g] = buf[s * kSlab + (8 * g + gr) * 4 + q];
-            if constexpr (SGN) {
-              const double sv = sgn_at(4 * k4 + q);  // undo the stored sign (exact)
-#pragma unroll
-              for (int g = 0; g < 4; ++g) af[g] *= sv;
-            }
 #pragma unroll
             for (int t = 0; t < W; ++t) {
               const int JJ = W * P + t;
@@ -231,10 +225,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
               y[j] = fast_div(y[j], D[j * 8 + j], D[64 + j], D[72 + j] != 0.0);
             }
           }
-          if constexpr (SGN) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) y[j] *= sgn_at(8 * J + j);
-          }
           __syncwarp();
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -252,7 +242,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 #pragma unroll
           for (int kk4 = 0; kk4 < 2; ++kk4) {
             af[g][kk4] = tile[swz64(8 * g + gr, 2 * kk4 + (q >> 1)) + (q & 1)];
-            if constexpr (SGN) af[g][kk4] *= sgn_at(8 * J + 4 * kk4 + q);
           }
         const double* bcol = sB + (2 * J) * 32 + lane;
 #pragma unroll
@@ -300,14 +289,14 @@ cudaError_t launch_t(const TrisolveArgs& a, cudaStream_t s) {
       !make_tmap_2d(&tst, a.out, a.n, a.m, a.ldo, 8, kRW, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorNotSupported;
   const size_t smem = (size_t)(head_doubles<NP, BSMEM>() + WPC * kWarpDoubles) * 8 + WPC * 16 + 1024;
-  auto k = a.sgn ? trisolve_tma_kernel<NP, WPC, BSMEM, true> : trisolve_tma_kernel<NP, WPC, BSMEM, false>;
+  auto k = trisolve_tma_kernel<NP, WPC, BSMEM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + kRW - 1) / kRW;
   long long grid = (groups + WPC - 1) / WPC;
   if (grid > (long long)a.num_sms) grid = a.num_sms;
   if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, WPC * 32, smem, s>>>(tin, tll, tst, a.m, a.n, a.bpack, a.dpack, a.sgn, a.status);
+  k<<<(unsigned)grid, WPC * 32, smem, s>>>(tin, tll, tst, a.m, a.n, a.bpack, a.dpack, a.status);
   return cudaGetLastError();
 }
 
