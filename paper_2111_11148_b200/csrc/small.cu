@@ -367,15 +367,12 @@ __global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restric
 constexpr int kChPanel = 32;
 
 __device__ __forceinline__ double div_rn(double y, double d, double inv) {
-  // correctly rounded y / d from inv = RN(1/d) (two Markstein corrections)
+  // correctly rounded y / d from inv = RN(1/d), one Markstein correction (see trisolve_common.cuh)
   const double ay = fabs(y);
-  if (!(ay >= 0x1p-900 && ay <= 0x1p+900) || !(fabs(d) >= 0x1p-500 && fabs(d) <= 0x1p+500))
-    return y / d;
+  if (!(ay >= 0x1p-400 && ay <= 0x1p+400) || !(fabs(d) >= 0x1p-500 && fabs(d) <= 0x1p+500)) return y / d;
   const double q0 = y * inv;
-  double r = fma(-q0, d, y);
-  const double q1 = fma(r, inv, q0);
-  r = fma(-q1, d, y);
-  return fma(r, inv, q1);
+  const double r = fma(-q0, d, y);
+  return fma(r, inv, q0);
 }
 
 __global__ void __launch_bounds__(512) cholesky_blocked_kernel(const double* __restrict__ g, int n,

@@ -13,11 +13,9 @@
 //     the reference's chain bit for bit (zero terms are not skipped: only the
 //     sign of an exact zero can differ);
 //  2. diagonal 8x8 block, one lane per row: the remaining k in [8J, j) as
-//     scalar fma, then the division. The division uses RN(1/r_jj) (computed
-//     once per column by pack_r) and two Markstein corrections, which is the
-//     correctly rounded quotient (tools/probe/markstein_check.c: 2e8 cases,
-//     0 mismatches; tests/test_gpu_parity.py checks it on device), with the
-//     IEEE division kept for zeros and extreme exponents.
+//     scalar fma, then the division: RN(1/r_jj) (computed once per column by
+//     pack_r) and one Markstein correction, the correctly rounded quotient for
+//     the operand window of trisolve_common.cuh (IEEE division outside it).
 // Rows are independent, so warps never synchronise with each other.
 //
 // Per row: HBM 8n bytes read + 8n written; n^2 flops (n(n-1)/2 fma + n div).

@@ -125,6 +125,25 @@ def test_trisolve_division_is_correctly_rounded():
         assert np.array_equal(x.view(np.int64), ref.view(np.int64))
 
 
+def test_trisolve_division_extreme_operands():
+    # operands across the whole exponent range: the fast division's window
+    # (|y| in [2^-400, 2^400], |d| in [2^-500, 2^500]) and the IEEE fallback
+    # outside it, including subnormal quotients; all must match IEEE bit for bit
+    rng = np.random.default_rng(11)
+    for n in (16, 128):
+        a = rng.standard_normal((2048, n)) * 10.0 ** rng.integers(-300, 300, size=(2048, n))
+        d = rng.standard_normal(n) * 10.0 ** rng.integers(-5, 6, size=n)
+        x = G.right_trisolve(a, np.diag(d))
+        ref = a / d
+        assert np.isfinite(ref).all()
+        assert np.array_equal(x.view(np.int64), ref.view(np.int64))
+        d2 = rng.standard_normal(n) * 10.0 ** rng.integers(-160, 160, size=n)
+        a2 = rng.standard_normal((2048, n)) * 10.0 ** rng.integers(-140, 140, size=(2048, n))
+        ref2 = a2 / d2
+        assert np.isfinite(ref2).all()
+        assert np.array_equal(G.right_trisolve(a2, np.diag(d2)).view(np.int64), ref2.view(np.int64))
+
+
 def test_trisolve_identity_and_singular():
     a = o.gaussian_matrix(30, 5, 1)
     assert np.array_equal(G.right_trisolve(a, np.eye(5)), a)
