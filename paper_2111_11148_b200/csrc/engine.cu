@@ -498,7 +498,8 @@ Outcome run_precond(Job& j) {
     {
       StageScope t(c, CQR_STAGE_SKETCH);
       if (try_cfg.strategy == CQR_GAUSSIAN) {
-        cqr::SketchPlan sp = cqr::sketch_plan(j.m_local, n, (int)l, c->num_sms);
+        cqr::SketchPlan sp = cqr::sketch_plan(j.m_local, n, (int)l, c->num_sms,
+                                              cqr::sketch_ws_ok(j.a, j.lda, m, j.row0, n));
         double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
         if (j.m_local > 0) {
           const int vec = vec_ok(j.a, j.lda, n) ? 1 : 0, chk = attempt == 0 ? j.check_first : 0;
@@ -1119,7 +1120,8 @@ int cqr_sketch_gaussian_dev(cqr_ctx* c, const double* a, int64_t m_local, int64_
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     reset_status(c);
-    cqr::SketchPlan sp = cqr::sketch_plan(m_local, (int)n, (int)l, c->num_sms);
+    cqr::SketchPlan sp =
+        cqr::sketch_plan(m_local, (int)n, (int)l, c->num_sms, cqr::sketch_ws_ok(a, lda, m_global, row0, (int)n));
     double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
     if (m_local > 0) {
       LAUNCH(c, cqr::launch_sketch_gaussian(sp, a, lda, m_global, row0, seed, part, vec_ok(a, lda, (int)n) ? 1 : 0,
@@ -1144,7 +1146,7 @@ int cqr_sketch_gaussian(cqr_ctx* c, const double* a, int64_t m, int64_t n, int64
                          cudaMemcpyHostToDevice, c->stream),
        "A H2D");
     reset_status(c);
-    cqr::SketchPlan sp = cqr::sketch_plan(m, (int)n, (int)l, c->num_sms);
+    cqr::SketchPlan sp = cqr::sketch_plan(m, (int)n, (int)l, c->num_sms, cqr::sketch_ws_ok(da, n, m, 0, (int)n));
     double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
     LAUNCH(c, cqr::launch_sketch_gaussian(sp, da, n, m, 0, seed, part, vec_ok(da, n, (int)n) ? 1 : 0, 0, c->status,
                                           c->stream));

@@ -60,11 +60,13 @@ cudaError_t launch_mirror_upper(double* g, int n, const DevStatus* st, cudaStrea
 
 // ---- sketch.cu ---------------------------------------------------------------------
 struct SketchPlan {
-  int n = 0, np = 0, l = 0, lp = 0, s_tiles = 0, kchunks = 0;
+  int n = 0, np = 0, l = 0, lp = 0, s_tiles = 0, kchunks = 0, ws = 0;  // ws: warp-specialised kernel
   long long m_local = 0, rows_per_chunk = 0;
   size_t partial_doubles = 0;
 };
-SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms);
+// ws_ok: the caller's A qualifies for the warp-specialised kernel (sketch_ws_ok)
+SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok = false);
+bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long row0, int n);
 // [y0, y1): the k-chunks (rows_per_chunk rows each) this launch covers (default all).
 cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,
                                    long long row0, uint64_t seed, double* partial, int vec16, int check,

@@ -14,12 +14,15 @@
 // Algorithmic work: 2*l*m*n flops + l*m Gaussian draws; HBM: 8*m*n bytes of A
 // (each A row is read by l/ST CTAs that run together, the repeats hit L2).
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
 #include "boxmuller.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace cqr {
 
@@ -179,6 +182,137 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
   }
 }
 
+// Warp-specialised variant (the default for n in (64, 128], even counters,
+// TMA-addressable A). The Box-Muller draws and the DMMA stream share the FP64
+// pipe; in the kernel above every warp alternates between them, and the
+// draw latency leaves the pipe ~25% idle (a constant-Omega build of the same
+// kernel runs the sketch in 2.14 ms vs 2.94). Here 8 generator warps fill a
+// 3-stage ring of Omega tiles (64 x 32, the same counters and pair layout) while
+// a TMA load brings the matching 32 x 128 A tile (SWIZZLE_128B boxes of 16
+// columns, one box per MMA warp), and 8 MMA warps consume the stages behind
+// full/empty mbarriers. Per-element arithmetic and k order are those of
+// sketch_kernel<128, true>: the partials are bit-identical.
+#ifndef CQR_WS_STAGES
+#define CQR_WS_STAGES 3
+#endif
+#ifndef CQR_WS_GEN
+#define CQR_WS_GEN 8
+#endif
+#ifndef CQR_WS_UNROLL
+#define CQR_WS_UNROLL 4
+#endif
+constexpr int kWsStages = CQR_WS_STAGES;
+constexpr int kWsGen = CQR_WS_GEN;
+constexpr int kWsUnroll = CQR_WS_UNROLL;
+constexpr int kWsMma = 8;
+constexpr int kWsThreads = (kWsGen + kWsMma) * 32;
+constexpr int kWsATile = kKS * 128;       // doubles per A stage (8 boxes of 32 x 16)
+constexpr int kWsOTile = kST * (kKS + 4);  // doubles per Omega stage (stride 36)
+
+__global__ void __launch_bounds__(kWsThreads, 1)
+    sketch_ws_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global, long long row0,
+                     int l, uint64_t seed, long long rows_per_chunk, double* __restrict__ partial, int lp,
+                     int np_total, int check, int y0, DevStatus* st) {
+  constexpr int LDO = kKS + 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BmTables T;
+  __shared__ __align__(8) uint64_t full[kWsStages], empty[kWsStages];
+  if (failed(st)) return;
+  double* sm = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  double* sA = sm;                            // [stage][box 8][32 rows][16 cols, 128B-swizzled]
+  double* sO = sm + kWsStages * kWsATile;     // [stage][64][36]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s0 = blockIdx.x * kST;
+  const int ky = blockIdx.y + y0;
+  const long long k_begin = (long long)ky * rows_per_chunk;
+  const long long k_end = min(m_local, k_begin + rows_per_chunk);
+  const int nsteps = k_end > k_begin ? (int)((k_end - k_begin + kKS - 1) / kKS) : 0;
+  {
+    const double* src = reinterpret_cast<const double*>(&c_bm);
+    double* dst = reinterpret_cast<double*>(&T);
+    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += kWsThreads) dst[e] = src[e];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kWsStages; ++s) {
+      mbar_init(&full[s], kWsGen * 32 + 1);  // every generator thread + the TMA issuer's expect_tx
+      mbar_init(&empty[s], kWsMma);          // one elected lane per MMA warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_shared();
+  }
+  __syncthreads();
+  if (warp >= kWsMma) {
+    // ---- generator warps: Omega tiles + the A tile's TMA
+    const int gt = tid - kWsMma * 32;
+    for (int stp = 0; stp < nsteps; ++stp) {
+      const int s = stp % kWsStages;
+      mbar_wait(&empty[s], ((stp / kWsStages) & 1) ^ 1);
+      const long long kb = k_begin + (long long)stp * kKS;
+      if (gt == 0) {
+        mbar_expect_tx(&full[s], kWsATile * 8);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) tma_load_2d(sA + s * kWsATile + b * (kKS * 16), &tma_a, 16 * b, (int)kb, &full[s]);
+      }
+      double* Om = sO + s * kWsOTile;
+#pragma unroll kWsUnroll
+      for (int u = 0; u < kST * kKS / 2 / (kWsGen * 32); ++u) {
+        const int e = gt + kWsGen * 32 * u;
+        const int i = e >> 4, pp = e & 15;
+        const unsigned long long c_lo = (unsigned long long)(s0 + i) * (unsigned long long)m_global + row0 + kb;
+        double ge, go;
+        gaussian_pair_fast(T, seed, (c_lo >> 1) + pp, ge, go);
+        const bool live = s0 + i < l;
+        *reinterpret_cast<double2*>(Om + i * LDO + 2 * pp) = make_double2(live ? ge : 0.0, live ? go : 0.0);
+      }
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+    }
+    return;
+  }
+  // ---- MMA warps: 64 Omega rows x 16 columns each (one A box)
+  const int q = lane & 3, gr = lane >> 2;
+  double acc[8][2][2];
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) acc[g][h][0] = acc[g][h][1] = 0.0;
+  bool bad = false;
+  for (int stp = 0; stp < nsteps; ++stp) {
+    const int s = stp % kWsStages;
+    mbar_wait(&full[s], (stp / kWsStages) & 1);
+    const double* Om = sO + s * kWsOTile + gr * LDO + q;
+    const double* Ab = sA + s * kWsATile + warp * (kKS * 16);
+#pragma unroll
+    for (int k4 = 0; k4 < kKS / 4; ++k4) {
+      const int r = 4 * k4 + q;
+      double af[8], bf[2];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) af[g] = Om[g * 8 * LDO + 4 * k4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        bf[h] = Ab[r * 16 + 2 * ((4 * h + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
+        bad |= nonfinite(bf[h]);
+      }
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+  }
+  if (check && __any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
+  double* out = partial + (long long)ky * lp * np_total;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const int i = s0 + g * 8 + gr;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = warp * 16 + h * 8 + 2 * q;
+      *reinterpret_cast<double2*>(out + (long long)i * np_total + j) = make_double2(acc[g][h][0], acc[g][h][1]);
+    }
+  }
+}
+
 __global__ void sketch_reduce_kernel(const double* __restrict__ partial, int kchunks, int lp, int np, int l,
                                      int n, double* __restrict__ a1, const DevStatus* st) {
   if (failed(st)) return;
@@ -298,7 +432,14 @@ void bm_tables_host(BmTables* t) {
   }
 }
 
-SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms) {
+bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long row0, int n) {
+  static const bool off = std::getenv("CQR_SKETCH_LEGACY") != nullptr;  // tuning: force the interleaved kernel
+  if (off || n <= 64 || n > 128 || (m_global & 1) || (row0 & 1)) return false;
+  CUtensorMap probe;
+  return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok) {
   SketchPlan p;
   p.n = n;
   p.l = l;
@@ -306,8 +447,10 @@ SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms) {
   p.m_local = m_local;
   p.s_tiles = (l + kST - 1) / kST;
   p.lp = p.s_tiles * kST;
-  // about 2 resident CTAs per SM over a few waves; chunks are multiples of KS rows
-  const long long target = (long long)num_sms * 4;
+  // interleaved kernel: about 2 resident CTAs per SM over 2 waves; warp-specialised:
+  // one CTA per SM, one wave. Chunks are multiples of KS rows.
+  p.ws = ws_ok && p.np == 128 ? 1 : 0;
+  const long long target = (long long)num_sms * (p.ws ? 1 : 4);
   const int zparts = p.np > 128 ? p.np / 128 : 1;
   long long kc = (target + (long long)p.s_tiles * zparts - 1) / ((long long)p.s_tiles * zparts);
   const long long max_kc = (m_local + kKS - 1) / kKS;
@@ -326,6 +469,21 @@ SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms) {
 cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,
                                    long long row0, uint64_t seed, double* partial, int vec16, int check,
                                    const DevStatus* st, cudaStream_t s, int y0, int y1) {
+  if (p.ws) {
+    if (y1 < 0) y1 = p.kchunks;
+    if (y1 <= y0) return cudaSuccess;
+    cudaError_t e0 = ensure_tables();
+    if (e0 != cudaSuccess) return e0;
+    CUtensorMap tm;
+    if (!make_tmap_2d(&tm, a, p.n, p.m_local, lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)kWsStages * (kWsATile + kWsOTile) * sizeof(double) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(sketch_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0));
+    sketch_ws_kernel<<<grid, kWsThreads, smem, s>>>(tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
+                                                     partial, p.lp, p.np, check, y0, const_cast<DevStatus*>(st));
+    return cudaGetLastError();
+  }
   switch (p.np) {
     case 8: return launch_sketch_t<8>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
     case 16: return launch_sketch_t<16>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
