@@ -211,7 +211,8 @@ def run_ours(args):
     sk_ms = statistics.mean(sketch_ms)
     sk_flops = 2.0 * l * m_local * n
     achieved = sk_flops / (sk_ms * 1e-3) / 1e12
-    roof = {"kernel": "sketch_kernel<128> + sketch_reduce (Sketch stage)", "bound": "tensor",
+    roof = {"kernel": "sketch_ws_kernel (8 Box-Muller warps + 8 DMMA warps) + sketch_reduce (Sketch stage)",
+            "bound": "tensor",
             "achieved": achieved, "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"],
             "peak_src": pk["fp64_src"], "algorithmic": "2*l*m*n flops per launch (l=256, m=1e6, n=128); Omega "
             "generation (l*m Gaussian draws) is extra work not counted", "traffic": _traffic()}
@@ -237,7 +238,7 @@ def run_ours(args):
 
 
 def _traffic():
-    p = os.path.join(ROOT, "profiles", "r01_sketch_traffic.json")
+    p = os.path.join(ROOT, "profiles", "sketch_traffic.json")
     try:
         return json.load(open(p))["bytes_per_launch"]
     except Exception:

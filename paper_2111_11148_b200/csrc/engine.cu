@@ -498,8 +498,9 @@ Outcome run_precond(Job& j) {
     {
       StageScope t(c, CQR_STAGE_SKETCH);
       if (try_cfg.strategy == CQR_GAUSSIAN) {
-        cqr::SketchPlan sp = cqr::sketch_plan(j.m_local, n, (int)l, c->num_sms,
-                                              cqr::sketch_ws_ok(j.a, j.lda, m, j.row0, n));
+        cqr::SketchPlan sp =
+            cqr::sketch_plan(j.m_local, n, (int)l, c->num_sms, cqr::sketch_ws_ok(j.a, j.lda, m, j.row0, n),
+                             pipelined(j) ? (int)j.bounds.size() - 1 : 1);
         double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
         if (j.m_local > 0) {
           const int vec = vec_ok(j.a, j.lda, n) ? 1 : 0, chk = attempt == 0 ? j.check_first : 0;

@@ -64,8 +64,10 @@ struct SketchPlan {
   long long m_local = 0, rows_per_chunk = 0;
   size_t partial_doubles = 0;
 };
-// ws_ok: the caller's A qualifies for the warp-specialised kernel (sketch_ws_ok)
-SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok = false);
+// ws_ok: the caller's A qualifies for the warp-specialised kernel (sketch_ws_ok);
+// splits: the k-chunks will be launched in this many row ranges as A arrives (host pipeline),
+// so each range still fills the GPU
+SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok = false, int splits = 1);
 bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long row0, int n);
 // [y0, y1): the k-chunks (rows_per_chunk rows each) this launch covers (default all).
 cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long long lda, long long m_global,

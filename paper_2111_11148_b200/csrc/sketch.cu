@@ -439,7 +439,7 @@ bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long 
   return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok) {
+SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok, int splits) {
   SketchPlan p;
   p.n = n;
   p.l = l;
@@ -450,7 +450,7 @@ SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok)
   // interleaved kernel: about 2 resident CTAs per SM over 2 waves; warp-specialised:
   // one CTA per SM, one wave. Chunks are multiples of KS rows.
   p.ws = ws_ok && p.np == 128 ? 1 : 0;
-  const long long target = (long long)num_sms * (p.ws ? 1 : 4);
+  const long long target = (long long)num_sms * (p.ws ? std::max(1, splits) : 4);
   const int zparts = p.np > 128 ? p.np / 128 : 1;
   long long kc = (target + (long long)p.s_tiles * zparts - 1) / ((long long)p.s_tiles * zparts);
   const long long max_kc = (m_local + kKS - 1) / kKS;

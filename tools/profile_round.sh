@@ -4,11 +4,11 @@
 set -u
 mkdir -p gpurun_out
 tag=${1:-r01}
-python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
+python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
 python tools/prof_c1.py > gpurun_out/prof_plain_${tag}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${tag}.csv \
     python tools/prof_c1.py > /dev/null 2>&1
 PROF_REPS=1 ncu --set full --clock-control none --import-source on \
-    -k regex:"sketch_kernel|trisolve_sb|gram_leaf|lu_kernel|cholesky_kernel" -c 6 \
+    -k regex:"sketch_ws_kernel|trisolve_tma|gram_leaf_p|lu_blocked|cholesky_blocked" --launch-skip 0 -c 6 \
     -o gpurun_out/full_${tag} python tools/prof_c1.py > gpurun_out/ncu_full_${tag}.log 2>&1
 tail -2 gpurun_out/ncu_full_${tag}.log
