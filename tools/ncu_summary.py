@@ -52,7 +52,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         tot = 0.0
         for name, us in launches(sys.argv[2]):
-            if "cqr" in name or "finite" in name:
+            if "cqr" in name or "unnamed>::" in name or "finite" in name:
                 print(f"{us:10.1f} us  {name[:110]}")
                 tot += us
         print(f"{tot:10.1f} us  total (cqr kernels)")

@@ -18,6 +18,10 @@ ctx = dist.make_context(0, 0, 1)
 a = bench.make_input(m, n, 0, 1, dev, ctx=ctx)
 cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=2.0, seed=bench._seed_value())
 q = torch.empty_like(a)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off: only the factorizations, not the input synthesis
 for _ in range(reps):
     _, r, rep = dist.factor_sharded(ctx, method, a, m, 0, cfg, _abi.options(), q_out=q)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("stage_ms", [round(x, 3) for x in rep.stage_ms], "launches", ctx.launches)

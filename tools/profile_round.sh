@@ -6,9 +6,9 @@ mkdir -p gpurun_out
 tag=${1:-r01}
 python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
 python tools/prof_c1.py > gpurun_out/prof_plain_${tag}.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${tag}.csv \
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${tag}.csv \
     python tools/prof_c1.py > /dev/null 2>&1
-PROF_REPS=1 ncu --set full --clock-control none --import-source on \
-    -k regex:"sketch_ws_kernel|trisolve_tma|gram_leaf_p|lu_blocked|cholesky_blocked" --launch-skip 0 -c 6 \
+PROF_REPS=1 ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -k regex:"sketch_ws_kernel|trisolve_tma|gram_leaf_p|lu_blocked|cholesky_blocked" -c 6 \
     -o gpurun_out/full_${tag} python tools/prof_c1.py > gpurun_out/ncu_full_${tag}.log 2>&1
 tail -2 gpurun_out/ncu_full_${tag}.log
