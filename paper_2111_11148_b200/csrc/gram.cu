@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace cqr {
 
@@ -206,6 +207,119 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   }
 }
 
+// TMA-fed persistent variant (the default for n in (64, 128] when X is
+// TMA-addressable): one producer warp streams the 32-row chunks of this CTA's
+// leaves through a 4-stage ring (SWIZZLE_128B boxes of 16 columns) and 12 MMA
+// warps consume them behind full/empty mbarriers: no block barrier and no
+// cp.async issue work per chunk. Same tiles, same k order as gram_leaf_p_kernel:
+// bit-identical partials.
+constexpr int kGtStages = 4;
+constexpr int kGtMma = 12;
+constexpr int kGtThreads = (kGtMma + 1) * 32;
+constexpr int kGtChunk = 32 * 128;  // doubles per stage (8 boxes of 32 rows x 16 columns)
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kGtThreads, 1)
+    gram_leaf_tma_kernel(const __grid_constant__ CUtensorMap tmx, long long m, const int32_t* __restrict__ tiles,
+                         double* __restrict__ partial, int leaf0, int leaf1, DevStatus* st) {
+  constexpr int NP = 128, MAXT = 3;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kGtStages], empty[kGtStages];
+  if (failed(st)) return;
+  double* sm = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kGtStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kGtMma);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_shared();
+  }
+  __syncthreads();
+  auto leaf_chunks = [&](int lf) {
+    const long long rows = min((long long)kLeafRows, m - (long long)lf * kLeafRows);
+    return (int)((rows + 31) / 32);
+  };
+  if (warp == kGtMma) {  // ---- producer
+    if (lane == 0) {
+      int it = 0;
+      for (int lf = leaf0 + blockIdx.x; lf < leaf1; lf += gridDim.x) {
+        const int nch = leaf_chunks(lf);
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int s = it % kGtStages;
+          mbar_wait(&empty[s], ((it / kGtStages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], kGtChunk * 8);
+          const int row = lf * kLeafRows + c * 32;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) tma_load_2d(sm + s * kGtChunk + b * 512, &tmx, 16 * b, row, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  // ---- MMA warps: three 16x16 macro tiles each
+  const int q = lane & 3, gr = lane >> 2;
+  int mt[MAXT];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) mt[t] = tiles[warp * MAXT + t];
+  double acc[MAXT][4][2];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  bool bad = false;
+  // column group h (8 columns) of row r inside a stage: box h/2, 128B-swizzled 16-byte chunks
+  auto at = [&](const double* base, int r, int h) {
+    return base[(h >> 1) * 512 + r * 16 + 2 * ((4 * (h & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
+  };
+  int it = 0;
+  for (int lf = leaf0 + blockIdx.x; lf < leaf1; lf += gridDim.x) {
+    const int nch = leaf_chunks(lf);
+    for (int c = 0; c < nch; ++c, ++it) {
+      const int s = it % kGtStages;
+      mbar_wait(&full[s], (it / kGtStages) & 1);
+      const double* base = sm + s * kGtChunk;
+#pragma unroll 2
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const int r = 4 * k4 + q;
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          if (mt[t] < 0) continue;
+          const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
+          const double a0 = at(base, r, 2 * I2), a1 = at(base, r, 2 * I2 + 1);
+          const double b0 = at(base, r, 2 * J2), b1 = at(base, r, 2 * J2 + 1);
+          if constexpr (CHECK) bad |= nonfinite(a0) | nonfinite(a1) | nonfinite(b0) | nonfinite(b1);
+          dmma(acc[t][0][0], acc[t][0][1], a0, b0);
+          dmma(acc[t][1][0], acc[t][1][1], a0, b1);
+          if (I2 != J2) dmma(acc[t][2][0], acc[t][2][1], a1, b0);
+          dmma(acc[t][3][0], acc[t][3][1], a1, b1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+    }
+    double* out = partial + (long long)lf * NP * NP;  // leaf done: its partial, then restart the chains
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      if (mt[t] < 0) continue;
+      const int I2 = mt[t] & 0xffff, J2 = mt[t] >> 16;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int si = u >> 1, sj = u & 1;
+        if (!(I2 == J2 && si == 1 && sj == 0)) {
+          const int i = 16 * I2 + 8 * si + gr, j = 16 * J2 + 8 * sj + 2 * q;
+          *reinterpret_cast<double2*>(out + i * NP + j) = make_double2(acc[t][u][0], acc[t][u][1]);
+        }
+        acc[t][u][0] = acc[t][u][1] = 0.0;
+      }
+    }
+  }
+  if constexpr (CHECK) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
+  }
+}
+
 // The pairwise tree of kernels.hpp:42-57 in streaming form: after pushing leaf
 // i, merge (top-1) + top once per trailing zero of (i+1); at the end fold the
 // stack right to left. Two levels for parallelism: level A folds each aligned
@@ -352,6 +466,20 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
                                double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s, int leaf0,
                                int leaf1, int num_sms) {
   if (p.persistent) {
+    static const bool no_tma = std::getenv("CQR_GRAM_NO_TMA") != nullptr;  // tuning: the cp.async kernel
+    CUtensorMap tm;
+    if (p.np == 128 && p.maxt == 3 && !no_tma &&
+        make_tmap_2d(&tm, x, p.n, p.m, ldx, 16, 32, CU_TENSOR_MAP_SWIZZLE_128B)) {
+      if (leaf1 < 0) leaf1 = p.leaves;
+      if (leaf1 <= leaf0) return cudaSuccess;
+      const size_t smem = (size_t)kGtStages * kGtChunk * sizeof(double) + 1024;
+      auto k = check ? gram_leaf_tma_kernel<true> : gram_leaf_tma_kernel<false>;
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      const int grid = std::min(leaf1 - leaf0, num_sms);
+      k<<<(unsigned)grid, kGtThreads, smem, s>>>(tm, p.m, tiles, partial, leaf0, leaf1, const_cast<DevStatus*>(st));
+      return cudaGetLastError();
+    }
     if (p.np == 128 && p.maxt == 3)
       return launch_leaves_p<128, 12, 3, 32>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 64 && p.maxt == 1)
