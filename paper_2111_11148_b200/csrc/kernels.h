@@ -61,6 +61,7 @@ cudaError_t launch_mirror_upper(double* g, int n, const DevStatus* st, cudaStrea
 // ---- sketch.cu ---------------------------------------------------------------------
 struct SketchPlan {
   int n = 0, np = 0, l = 0, lp = 0, s_tiles = 0, kchunks = 0, ws = 0;  // ws: warp-specialised kernel
+  int st = 64, npc = 128;  // Omega rows and A columns per CTA
   long long m_local = 0, rows_per_chunk = 0;
   size_t partial_doubles = 0;
 };

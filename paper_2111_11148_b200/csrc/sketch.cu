@@ -206,24 +206,37 @@ constexpr int kWsGen = CQR_WS_GEN;
 constexpr int kWsUnroll = CQR_WS_UNROLL;
 constexpr int kWsMma = 8;
 constexpr int kWsThreads = (kWsGen + kWsMma) * 32;
-constexpr int kWsATile = kKS * 128;       // doubles per A stage (8 boxes of 32 x 16)
-constexpr int kWsOTile = kST * (kKS + 4);  // doubles per Omega stage (stride 36)
 
+// NPC columns of A per CTA (128, or 256 for wider A with 32 Omega rows per CTA so
+// that each drawn Omega entry feeds twice the DMMA work), ST Omega rows per CTA.
+template <int NPC, int ST>
+struct WsShape {
+  static constexpr int ATILE = kKS * NPC;       // doubles per A stage (NPC/16 boxes of 32 x 16)
+  static constexpr int OTILE = ST * (kKS + 4);  // doubles per Omega stage (stride 36)
+  static constexpr int NGW = NPC / 64;          // 8-column groups per MMA warp
+  static constexpr int MGW = ST / 8;            // 8-row groups per MMA warp
+  static constexpr int PAIRS = ST * kKS / 2 / (kWsGen * 32);  // Box-Muller pairs per generator thread per step
+  static constexpr size_t SMEM = (size_t)kWsStages * (ATILE + OTILE) * sizeof(double) + 1024;
+};
+
+template <int NPC, int ST>
 __global__ void __launch_bounds__(kWsThreads, 1)
     sketch_ws_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global, long long row0,
                      int l, uint64_t seed, long long rows_per_chunk, double* __restrict__ partial, int lp,
                      int np_total, int check, int y0, DevStatus* st) {
+  using S = WsShape<NPC, ST>;
   constexpr int LDO = kKS + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ BmTables T;
   __shared__ __align__(8) uint64_t full[kWsStages], empty[kWsStages];
   if (failed(st)) return;
   double* sm = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-  double* sA = sm;                            // [stage][box 8][32 rows][16 cols, 128B-swizzled]
-  double* sO = sm + kWsStages * kWsATile;     // [stage][64][36]
+  double* sA = sm;                            // [stage][box][32 rows][16 cols, 128B-swizzled]
+  double* sO = sm + kWsStages * S::ATILE;     // [stage][ST][36]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int s0 = blockIdx.x * kST;
+  const int s0 = blockIdx.x * ST;
   const int ky = blockIdx.y + y0;
+  const int col0 = blockIdx.z * NPC;
   const long long k_begin = (long long)ky * rows_per_chunk;
   const long long k_end = min(m_local, k_begin + rows_per_chunk);
   const int nsteps = k_end > k_begin ? (int)((k_end - k_begin + kKS - 1) / kKS) : 0;
@@ -249,13 +262,14 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       mbar_wait(&empty[s], ((stp / kWsStages) & 1) ^ 1);
       const long long kb = k_begin + (long long)stp * kKS;
       if (gt == 0) {
-        mbar_expect_tx(&full[s], kWsATile * 8);
+        mbar_expect_tx(&full[s], S::ATILE * 8);
 #pragma unroll
-        for (int b = 0; b < 8; ++b) tma_load_2d(sA + s * kWsATile + b * (kKS * 16), &tma_a, 16 * b, (int)kb, &full[s]);
+        for (int b = 0; b < NPC / 16; ++b)
+          tma_load_2d(sA + s * S::ATILE + b * (kKS * 16), &tma_a, col0 + 16 * b, (int)kb, &full[s]);
       }
-      double* Om = sO + s * kWsOTile;
-#pragma unroll kWsUnroll
-      for (int u = 0; u < kST * kKS / 2 / (kWsGen * 32); ++u) {
+      double* Om = sO + s * S::OTILE;
+#pragma unroll
+      for (int u = 0; u < S::PAIRS; ++u) {
         const int e = gt + kWsGen * 32 * u;
         const int i = e >> 4, pp = e & 15;
         const unsigned long long c_lo = (unsigned long long)(s0 + i) * (unsigned long long)m_global + row0 + kb;
@@ -268,49 +282,66 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     }
     return;
   }
-  // ---- MMA warps: 64 Omega rows x 16 columns each (one A box)
+  // ---- MMA warps: all ST Omega rows x NPC/8 columns each
   const int q = lane & 3, gr = lane >> 2;
-  double acc[8][2][2];
+  double acc[S::MGW][S::NGW][2];
 #pragma unroll
-  for (int g = 0; g < 8; ++g)
+  for (int g = 0; g < S::MGW; ++g)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) acc[g][h][0] = acc[g][h][1] = 0.0;
+    for (int h = 0; h < S::NGW; ++h) acc[g][h][0] = acc[g][h][1] = 0.0;
   bool bad = false;
   for (int stp = 0; stp < nsteps; ++stp) {
     const int s = stp % kWsStages;
     mbar_wait(&full[s], (stp / kWsStages) & 1);
-    const double* Om = sO + s * kWsOTile + gr * LDO + q;
-    const double* Ab = sA + s * kWsATile + warp * (kKS * 16);
+    const double* Om = sO + s * S::OTILE + gr * LDO + q;
+    const double* As = sA + s * S::ATILE;
 #pragma unroll
     for (int k4 = 0; k4 < kKS / 4; ++k4) {
       const int r = 4 * k4 + q;
-      double af[8], bf[2];
+      double af[S::MGW], bf[S::NGW];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) af[g] = Om[g * 8 * LDO + 4 * k4];
+      for (int g = 0; g < S::MGW; ++g) af[g] = Om[g * 8 * LDO + 4 * k4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        bf[h] = Ab[r * 16 + 2 * ((4 * h + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
+      for (int h = 0; h < S::NGW; ++h) {
+        const int cg = warp * S::NGW + h;  // 8-column group: box cg/2, half cg&1
+        bf[h] = As[(cg >> 1) * (kKS * 16) + r * 16 + 2 * ((4 * (cg & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
         bad |= nonfinite(bf[h]);
       }
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
+      for (int g = 0; g < S::MGW; ++g)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
+        for (int h = 0; h < S::NGW; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
   }
   if (check && __any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
-  double* out = partial + (long long)ky * lp * np_total;
+  double* out = partial + (long long)ky * lp * np_total + col0;
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
+  for (int g = 0; g < S::MGW; ++g) {
     const int i = s0 + g * 8 + gr;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = warp * 16 + h * 8 + 2 * q;
+    for (int h = 0; h < S::NGW; ++h) {
+      const int j = (warp * S::NGW + h) * 8 + 2 * q;
       *reinterpret_cast<double2*>(out + (long long)i * np_total + j) = make_double2(acc[g][h][0], acc[g][h][1]);
     }
   }
+}
+
+template <int NPC, int ST>
+cudaError_t launch_ws(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
+                      uint64_t seed, double* partial, int check, const DevStatus* st, cudaStream_t s, int y0,
+                      int y1) {
+  CUtensorMap tm;
+  if (!make_tmap_2d(&tm, a, p.n, p.m_local, lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  auto k = sketch_ws_kernel<NPC, ST>;
+  cudaError_t e =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsShape<NPC, ST>::SMEM);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NPC));
+  k<<<grid, kWsThreads, WsShape<NPC, ST>::SMEM, s>>>(tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
+                                                      partial, p.lp, p.np, check, y0, const_cast<DevStatus*>(st));
+  return cudaGetLastError();
 }
 
 __global__ void sketch_reduce_kernel(const double* __restrict__ partial, int kchunks, int lp, int np, int l,
@@ -434,7 +465,7 @@ void bm_tables_host(BmTables* t) {
 
 bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long row0, int n) {
   static const bool off = std::getenv("CQR_SKETCH_LEGACY") != nullptr;  // tuning: force the interleaved kernel
-  if (off || n <= 64 || n > 128 || (m_global & 1) || (row0 & 1)) return false;
+  if (off || n <= 64 || n > 512 || (m_global & 1) || (row0 & 1)) return false;
   CUtensorMap probe;
   return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B);
 }
@@ -445,14 +476,19 @@ SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok,
   p.l = l;
   p.np = sketch_np(n);
   p.m_local = m_local;
-  p.s_tiles = (l + kST - 1) / kST;
-  p.lp = p.s_tiles * kST;
   // interleaved kernel: about 2 resident CTAs per SM over 2 waves; warp-specialised:
-  // one CTA per SM, one wave. Chunks are multiples of KS rows.
-  p.ws = ws_ok && p.np == 128 ? 1 : 0;
+  // one CTA per SM, one wave (n = 128: 64 Omega rows x 128 columns per CTA; wider:
+  // 32 Omega rows x 256 columns). Chunks are multiples of KS rows.
+  p.ws = ws_ok && p.np >= 128 ? 1 : 0;
+  p.st = p.ws && p.np > 128 ? 32 : kST;
+  p.npc = p.ws ? std::min(p.np, 256) : std::min(p.np, 128);
+  p.s_tiles = (l + p.st - 1) / p.st;
+  p.lp = p.s_tiles * p.st;
   const long long target = (long long)num_sms * (p.ws ? std::max(1, splits) : 4);
-  const int zparts = p.np > 128 ? p.np / 128 : 1;
-  long long kc = (target + (long long)p.s_tiles * zparts - 1) / ((long long)p.s_tiles * zparts);
+  const int zparts = p.np / p.npc;
+  // warp-specialised: whole waves (round down), the interleaved kernel: round up
+  const long long per = (long long)p.s_tiles * zparts;
+  long long kc = p.ws ? target / per : (target + per - 1) / per;
   const long long max_kc = (m_local + kKS - 1) / kKS;
   if (kc > max_kc) kc = max_kc;
   if (kc < 1) kc = 1;
@@ -474,15 +510,8 @@ cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long lo
     if (y1 <= y0) return cudaSuccess;
     cudaError_t e0 = ensure_tables();
     if (e0 != cudaSuccess) return e0;
-    CUtensorMap tm;
-    if (!make_tmap_2d(&tm, a, p.n, p.m_local, lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
-    const size_t smem = (size_t)kWsStages * (kWsATile + kWsOTile) * sizeof(double) + 1024;
-    cudaError_t e = cudaFuncSetAttribute(sketch_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0));
-    sketch_ws_kernel<<<grid, kWsThreads, smem, s>>>(tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
-                                                     partial, p.lp, p.np, check, y0, const_cast<DevStatus*>(st));
-    return cudaGetLastError();
+    if (p.npc == 128) return launch_ws<128, kST>(p, a, lda, m_global, row0, seed, partial, check, st, s, y0, y1);
+    return launch_ws<256, 32>(p, a, lda, m_global, row0, seed, partial, check, st, s, y0, y1);
   }
   switch (p.np) {
     case 8: return launch_sketch_t<8>(p, a, lda, m_global, row0, seed, partial, vec16, check, st, s, y0, y1);
