@@ -275,10 +275,10 @@ void allreduce(cqr_ctx* c, double* p, size_t count) {
 // Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
 void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g, int check = 0,
               Job* pj = nullptr) {
-  cqr::GramPlan p = cqr::gram_plan(m, n);
+  cqr::GramPlan p = cqr::gram_plan(m, n, cqr::gram_tma_ok(x, ldx, m, n));
   double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.workspace_doubles, 1));
   int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
-  const int key = p.np * 1000000 + p.wpc * 10000 + p.parts * 100 + p.maxt;
+  const int key = p.np * 1000000 + p.wpc * 10000 + p.parts * 100 + p.maxt + (p.tma ? 5000 : 0);
   if (c->tiles_key != key) {  // the table depends on (np, parts, maxt) only: upload once
     std::vector<int32_t> ht(p.tiles_bytes / sizeof(int32_t));
     cqr::gram_tiles(p, ht.data());

@@ -213,23 +213,33 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 // warps consume them behind full/empty mbarriers: no block barrier and no
 // cp.async issue work per chunk. Same tiles, same k order as gram_leaf_p_kernel:
 // bit-identical partials.
-constexpr int kGtStages = 4;
 constexpr int kGtMma = 12;
 constexpr int kGtThreads = (kGtMma + 1) * 32;
-constexpr int kGtChunk = 32 * 128;  // doubles per stage (8 boxes of 32 rows x 16 columns)
 
-template <bool CHECK>
+template <int NP, int ROWS>
+struct GtShape {
+  static constexpr int CHUNK = ROWS * NP;  // doubles per stage (NP/16 boxes of ROWS x 16)
+  static constexpr int BOX = ROWS * 16;
+  static constexpr int STAGES = CHUNK * 8 * 4 <= 200 * 1024 ? 4 : 3;
+  static constexpr size_t SMEM = (size_t)STAGES * CHUNK * sizeof(double) + 1024;
+};
+
+// Work item w = blockIdx.x + k * gridDim.x (gridDim.x a multiple of parts): part
+// w % parts (fixed per CTA: its warps' macro-tile lists), leaf leaf0 + w / parts.
+template <int NP, int MAXT, int ROWS, bool CHECK>
 __global__ void __launch_bounds__(kGtThreads, 1)
-    gram_leaf_tma_kernel(const __grid_constant__ CUtensorMap tmx, long long m, const int32_t* __restrict__ tiles,
-                         double* __restrict__ partial, int leaf0, int leaf1, DevStatus* st) {
-  constexpr int NP = 128, MAXT = 3;
+    gram_leaf_tma_kernel(const __grid_constant__ CUtensorMap tmx, long long m, int parts,
+                         const int32_t* __restrict__ tiles, double* __restrict__ partial, int leaf0, int leaf1,
+                         DevStatus* st) {
+  using S = GtShape<NP, ROWS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[kGtStages], empty[kGtStages];
+  __shared__ __align__(8) uint64_t full[S::STAGES], empty[S::STAGES];
   if (failed(st)) return;
   double* sm = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int part = blockIdx.x % parts;
   if (tid == 0) {
-    for (int s = 0; s < kGtStages; ++s) {
+    for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kGtMma);
     }
@@ -239,30 +249,32 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   __syncthreads();
   auto leaf_chunks = [&](int lf) {
     const long long rows = min((long long)kLeafRows, m - (long long)lf * kLeafRows);
-    return (int)((rows + 31) / 32);
+    return (int)((rows + ROWS - 1) / ROWS);
   };
   if (warp == kGtMma) {  // ---- producer
     if (lane == 0) {
       int it = 0;
-      for (int lf = leaf0 + blockIdx.x; lf < leaf1; lf += gridDim.x) {
+      for (int w = blockIdx.x;; w += gridDim.x) {
+        const int lf = leaf0 + w / parts;
+        if (lf >= leaf1) break;
         const int nch = leaf_chunks(lf);
         for (int c = 0; c < nch; ++c, ++it) {
-          const int s = it % kGtStages;
-          mbar_wait(&empty[s], ((it / kGtStages) & 1) ^ 1);
-          mbar_expect_tx(&full[s], kGtChunk * 8);
-          const int row = lf * kLeafRows + c * 32;
+          const int s = it % S::STAGES;
+          mbar_wait(&empty[s], ((it / S::STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], S::CHUNK * 8);
+          const int row = lf * kLeafRows + c * ROWS;
 #pragma unroll
-          for (int b = 0; b < 8; ++b) tma_load_2d(sm + s * kGtChunk + b * 512, &tmx, 16 * b, row, &full[s]);
+          for (int b = 0; b < NP / 16; ++b) tma_load_2d(sm + s * S::CHUNK + b * S::BOX, &tmx, 16 * b, row, &full[s]);
         }
       }
     }
     return;
   }
-  // ---- MMA warps: three 16x16 macro tiles each
+  // ---- MMA warps: MAXT 16x16 macro tiles each
   const int q = lane & 3, gr = lane >> 2;
   int mt[MAXT];
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t) mt[t] = tiles[warp * MAXT + t];
+  for (int t = 0; t < MAXT; ++t) mt[t] = tiles[(part * kGtMma + warp) * MAXT + t];
   double acc[MAXT][4][2];
 #pragma unroll
   for (int t = 0; t < MAXT; ++t)
@@ -271,17 +283,19 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   bool bad = false;
   // column group h (8 columns) of row r inside a stage: box h/2, 128B-swizzled 16-byte chunks
   auto at = [&](const double* base, int r, int h) {
-    return base[(h >> 1) * 512 + r * 16 + 2 * ((4 * (h & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
+    return base[(h >> 1) * S::BOX + r * 16 + 2 * ((4 * (h & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
   };
   int it = 0;
-  for (int lf = leaf0 + blockIdx.x; lf < leaf1; lf += gridDim.x) {
+  for (int w = blockIdx.x;; w += gridDim.x) {
+    const int lf = leaf0 + w / parts;
+    if (lf >= leaf1) break;
     const int nch = leaf_chunks(lf);
     for (int c = 0; c < nch; ++c, ++it) {
-      const int s = it % kGtStages;
-      mbar_wait(&full[s], (it / kGtStages) & 1);
-      const double* base = sm + s * kGtChunk;
+      const int s = it % S::STAGES;
+      mbar_wait(&full[s], (it / S::STAGES) & 1);
+      const double* base = sm + s * S::CHUNK;
 #pragma unroll 2
-      for (int k4 = 0; k4 < 8; ++k4) {
+      for (int k4 = 0; k4 < ROWS / 4; ++k4) {
         const int r = 4 * k4 + q;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
@@ -318,6 +332,23 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   if constexpr (CHECK) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
   }
+}
+
+template <int NP, int MAXT, int ROWS>
+cudaError_t launch_leaves_tma(const GramPlan& p, const CUtensorMap& tm, const int32_t* tiles, double* partial,
+                              int check, const DevStatus* st, cudaStream_t s, int leaf0, int leaf1, int num_sms) {
+  if (leaf1 < 0) leaf1 = p.leaves;
+  if (leaf1 <= leaf0) return cudaSuccess;
+  using S = GtShape<NP, ROWS>;
+  auto k = check ? gram_leaf_tma_kernel<NP, MAXT, ROWS, true> : gram_leaf_tma_kernel<NP, MAXT, ROWS, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+  if (e != cudaSuccess) return e;
+  const long long items = (long long)(leaf1 - leaf0) * p.parts;
+  const int slots = std::max(1, num_sms / p.parts) * p.parts;
+  const int grid = (int)std::min<long long>(items, slots);
+  k<<<(unsigned)grid, kGtThreads, S::SMEM, s>>>(tm, p.m, p.parts, tiles, partial, leaf0, leaf1,
+                                               const_cast<DevStatus*>(st));
+  return cudaGetLastError();
 }
 
 // The pairwise tree of kernels.hpp:42-57 in streaming form: after pushing leaf
@@ -419,7 +450,13 @@ cudaError_t launch_leaves_p(const GramPlan& p, const double* x, long long ldx, c
 
 }  // namespace
 
-GramPlan gram_plan(long long m, int n) {
+bool gram_tma_ok(const double* x, long long ldx, long long m, int n) {
+  static const bool off = std::getenv("CQR_GRAM_NO_TMA") != nullptr;  // tuning: the cp.async kernels
+  CUtensorMap probe;
+  return !off && n > 64 && m > 0 && make_tmap_2d(&probe, x, n, m, ldx, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+GramPlan gram_plan(long long m, int n, bool tma_ok) {
   GramPlan p;
   p.n = n;
   p.m = m;
@@ -428,7 +465,14 @@ GramPlan gram_plan(long long m, int n) {
   const int nm = p.np / 16;
   const int macros = nm * (nm + 1) / 2;
   static const bool legacy = std::getenv("CQR_GRAM_LEGACY") != nullptr;  // tuning: the per-leaf kernel
-  if (p.np == 128 && !legacy) {  // persistent: the 36 macro tiles divide evenly over 12 warps (measured: n = 64 is faster per leaf)
+  if (tma_ok && p.np >= 128) {  // TMA-fed: 12 DMMA warps, the macro tiles over `parts` CTAs per leaf
+    p.tma = 1;
+    p.persistent = 1;
+    p.wpc = kGtMma;
+    p.parts = p.np == 128 ? 1 : p.np == 256 ? 3 : 11;  // 36 / 136 / 528 macros: 3, 4, 4 per warp (13 warps: 128 regs)
+    p.maxt = (macros + p.wpc * p.parts - 1) / (p.wpc * p.parts);
+    p.ch = p.np == 512 ? 16 : 32;
+  } else if (p.np == 128 && !legacy) {  // persistent: the 36 macro tiles divide evenly over 12 warps (measured: n = 64 is faster per leaf)
     p.persistent = 1;
     p.wpc = p.np == 64 ? 10 : 12;
     p.parts = 1;
@@ -465,21 +509,15 @@ void gram_tiles(const GramPlan& p, int32_t* out) {
 cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
                                double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s, int leaf0,
                                int leaf1, int num_sms) {
-  if (p.persistent) {
-    static const bool no_tma = std::getenv("CQR_GRAM_NO_TMA") != nullptr;  // tuning: the cp.async kernel
+  if (p.tma) {
     CUtensorMap tm;
-    if (p.np == 128 && p.maxt == 3 && !no_tma &&
-        make_tmap_2d(&tm, x, p.n, p.m, ldx, 16, 32, CU_TENSOR_MAP_SWIZZLE_128B)) {
-      if (leaf1 < 0) leaf1 = p.leaves;
-      if (leaf1 <= leaf0) return cudaSuccess;
-      const size_t smem = (size_t)kGtStages * kGtChunk * sizeof(double) + 1024;
-      auto k = check ? gram_leaf_tma_kernel<true> : gram_leaf_tma_kernel<false>;
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      const int grid = std::min(leaf1 - leaf0, num_sms);
-      k<<<(unsigned)grid, kGtThreads, smem, s>>>(tm, p.m, tiles, partial, leaf0, leaf1, const_cast<DevStatus*>(st));
-      return cudaGetLastError();
-    }
+    if (!make_tmap_2d(&tm, x, p.n, p.m, ldx, 16, p.ch, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    if (p.np == 128) return launch_leaves_tma<128, 3, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 256) return launch_leaves_tma<256, 4, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    return cudaErrorInvalidValue;
+  }
+  if (p.persistent) {
     if (p.np == 128 && p.maxt == 3)
       return launch_leaves_p<128, 12, 3, 32>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 64 && p.maxt == 1)

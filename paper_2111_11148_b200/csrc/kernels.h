@@ -37,13 +37,15 @@ cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s);
 
 // ---- gram.cu ---------------------------------------------------------------------
 struct GramPlan {
-  int n = 0, np = 0, leaves = 0, parts = 0, maxt = 0, wpc = 0, ch = 0, persistent = 0;
+  int n = 0, np = 0, leaves = 0, parts = 0, maxt = 0, wpc = 0, ch = 0, persistent = 0, tma = 0;
   long long m = 0;
   size_t partial_doubles = 0;    // leaves * np * np
   size_t workspace_doubles = 0;  // partials + the per-group sums of the combine
   size_t tiles_bytes = 0;
 };
-GramPlan gram_plan(long long m, int n);
+GramPlan gram_plan(long long m, int n, bool tma_ok = false);
+// X is TMA-addressable for the TMA-fed leaf kernel (16-byte aligned base, even leading dimension)
+bool gram_tma_ok(const double* x, long long ldx, long long m, int n);
 // Host-side tile table for the plan (parts * wpc * maxt entries, packed I2 | J2<<16, -1 = none).
 void gram_tiles(const GramPlan& p, int32_t* out);
 // Leaf partials (1024-row leaves, kernels.hpp:20-38) -> partial[leaf][np*np] (upper tiles).
