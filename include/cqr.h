@@ -146,6 +146,9 @@ int cqr_comm_id_size(void);
  * same bytes to cqr_attach_comm. This replaces the reference's simulated
  * workers (parexec.cpp:64-75, engine.cpp:12-22) with one process per GPU. */
 int cqr_comm_make_id(void* id);
+/* An attached communicator switches the exchange steps on (sketch and Gram
+ * all-reduce, agreement on non-finite input), also for world == 1 (a one-rank
+ * NCCL communicator). */
 int cqr_attach_comm(cqr_ctx* ctx, int rank, int world, const void* id);
 int cqr_stream_handle(cqr_ctx* ctx, void** stream); /* cudaStream_t the context launches on */
 

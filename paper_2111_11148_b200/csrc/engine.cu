@@ -268,7 +268,7 @@ void wait_rows(Job& j, long long rows_end) {
 void wait_all(Job& j) { wait_rows(j, std::numeric_limits<long long>::max()); }
 
 void allreduce(cqr_ctx* c, double* p, size_t count) {
-  if (c->world <= 1 || c->local_only) return;
+  if (!c->comm || c->local_only) return;
   ckn(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->comm, c->stream), "ncclAllReduce");
 }
 
@@ -303,12 +303,12 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
       LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
                                         c->stream, 0, -1, c->num_sms));
     }
-    LAUNCH(c, cqr::launch_gram_combine(p, part, g, (c->world <= 1 || c->local_only) ? 1 : 0, c->status, c->stream));
+    LAUNCH(c, cqr::launch_gram_combine(p, part, g, (!c->comm || c->local_only) ? 1 : 0, c->status, c->stream));
     ++c->launches;
   } else {
     ck(cudaMemsetAsync(g, 0, sizeof(double) * n * n, c->stream), "memset");
   }
-  if (c->world > 1 && !c->local_only) {
+  if (c->comm && !c->local_only) {
     allreduce(c, g, (size_t)n * n);
     LAUNCH(c, cqr::launch_mirror_upper(g, n, c->status, c->stream));
   }
@@ -727,15 +727,15 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     reset_status(c);
     const bool gaussian = j.method == CQR_RQR_GAUSSIAN || j.cfg.strategy == CQR_GAUSSIAN;
     const bool family = j.method == CQR_CHOLQR || j.method == CQR_CHOLQR2 || j.method == CQR_SCHOLQR3;
-    j.check_first = (c->world == 1 && !j.precond && (family || gaussian)) ? 1 : 0;
+    j.check_first = (!c->comm && !j.precond && (family || gaussian)) ? 1 : 0;
     if (!j.check_first) {
       wait_all(j);
       check_finite(c, j.a, j.m_local, j.n, j.lda);
     }
-    if (c->world > 1) {
+    if (c->comm) {  // every rank takes the same path
       DevStatus s0 = read_status(c);
       int bad = s0.code != 0;
-      if (c->world > 1) {
+      {
         int* flag = dbuf<int>(c, B_DIAG, 1);
         ck(cudaMemcpyAsync(flag, &bad, sizeof(int), cudaMemcpyHostToDevice, c->stream), "flag");
         ckn(ncclAllReduce(flag, flag, 1, ncclInt, ncclMax, c->comm, c->stream), "allreduce flag");
@@ -860,11 +860,11 @@ int cqr_attach_comm(cqr_ctx* c, int rank, int world, const void* id) {
     }
     c->rank = rank;
     c->world = world;
-    if (world > 1) {
-      ncclUniqueId u;
-      std::memcpy(&u, id, sizeof(u));
-      ckn(ncclCommInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
-    }
+    // an attached communicator switches the collective paths on, also for world == 1
+    // (a one-rank NCCL communicator: the exchange steps run as on a multi-GPU job)
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    ckn(ncclCommInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
   });
 }
 
@@ -1239,7 +1239,7 @@ int cqr_residual_error_dev(cqr_ctx* c, const double* a, int64_t lda, const doubl
     ck(cudaMemcpyAsync(dr, r_host, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "R H2D");
     LAUNCH(c, cqr::launch_residual(a, lda, q, ldq, dr, m, (int)n, part, nb, o, c->stream));
     ++c->launches;
-    if (c->world > 1) allreduce(c, o, 2);
+    allreduce(c, o, 2);
     ck(cudaMemcpyAsync(c->scal_h, o, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
     *out = std::sqrt(c->scal_h[0]) / std::sqrt(c->scal_h[1]);

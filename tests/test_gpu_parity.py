@@ -19,6 +19,7 @@ import pytest
 from oracle import oracle as o
 from paper_2111_11148_b200 import _abi
 from paper_2111_11148_b200 import cholqr as G
+from paper_2111_11148_b200 import dist
 
 pytestmark = pytest.mark.gpu
 U = np.finfo(np.float64).eps
@@ -393,3 +394,26 @@ def test_orthonormalize_matches_reference_caller(orth):  # apps.cpp:166-196
             assert np.array_equal(q, ref)
     with pytest.raises(NotImplementedError):
         G.orthonormalize(y, G.Orth.HouseholderQr, seed, 0)
+
+
+def test_one_rank_nccl_collective_path_is_bit_identical():
+    # an attached communicator runs the multi-GPU exchange steps (NCCL all-reduce of the
+    # sketch and Gram partials, the agreement on non-finite input); with one rank every
+    # all-reduce is the identity, so the results equal the single-GPU path bit for bit
+    import torch
+
+    plain = G.Context(0)
+    coll = G.Context(0)
+    coll.attach_comm(0, 1, G.make_comm_id())
+    a = torch.as_tensor(o.synthesize(20000, 48, 1e6, 3), device="cuda")
+    for meth, cfg in [(_abi.RLU, G.SketchConfig(strategy=G.Strategy.Gaussian, seed=5)),
+                      (_abi.RQR, G.SketchConfig(seed=6)), (_abi.CHOLQR2, None)]:
+        res = []
+        for ctx in (plain, coll):
+            q, r, rep = dist.factor_sharded(ctx, meth, a, a.shape[0], 0, cfg)
+            res.append((q.cpu().numpy(), np.asarray(r)))
+        assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    bad = a.clone()
+    bad[7, 3] = float("nan")
+    with pytest.raises(ValueError):
+        dist.factor_sharded(coll, _abi.RLU, bad, bad.shape[0], 0, G.SketchConfig(strategy=G.Strategy.Gaussian))
