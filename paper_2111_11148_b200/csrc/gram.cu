@@ -372,8 +372,9 @@ __global__ void gram_combine_a_kernel(const double* __restrict__ partial, int le
                                       double* __restrict__ gsum, const DevStatus* st) {
   if (failed(st)) return;
   const int i = blockIdx.y;
-  const int j = i + blockIdx.x * blockDim.x + threadIdx.x;
-  const int grp = blockIdx.z;
+  const int xb = (n + 127) / 128;  // column blocks per row; grid.x = groups * xb (grid.z would cap at 65535)
+  const int grp = blockIdx.x / xb;
+  const int j = i + (blockIdx.x - grp * xb) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const long long stride = (long long)np * np;
   const int l0 = grp * kGroup, l1 = min(leaves, l0 + kGroup);
@@ -453,7 +454,7 @@ cudaError_t launch_leaves_p(const GramPlan& p, const double* x, long long ldx, c
 bool gram_tma_ok(const double* x, long long ldx, long long m, int n) {
   static const bool off = std::getenv("CQR_GRAM_NO_TMA") != nullptr;  // tuning: the cp.async kernels
   CUtensorMap probe;
-  return !off && n > 64 && m > 0 && make_tmap_2d(&probe, x, n, m, ldx, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
+  return !off && n > 64 && m > 0 && m < (1LL << 31) - 1024 && make_tmap_2d(&probe, x, n, m, ldx, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 GramPlan gram_plan(long long m, int n, bool tma_ok) {
@@ -548,7 +549,7 @@ cudaError_t launch_gram_combine(const GramPlan& p, double* partial, double* g, i
                                 const DevStatus* st, cudaStream_t s) {
   const int groups = (p.leaves + kGroup - 1) / kGroup;
   double* gsum = partial + p.partial_doubles;  // workspace after the leaf partials (gram_plan reserves it)
-  dim3 ga((unsigned)((p.n + 127) / 128), (unsigned)p.n, (unsigned)groups);
+  dim3 ga((unsigned)(((p.n + 127) / 128) * groups), (unsigned)p.n);
   gram_combine_a_kernel<<<ga, 128, 0, s>>>(partial, p.leaves, p.np, p.n, gsum, st);
   dim3 gb((unsigned)((p.n + 127) / 128), (unsigned)p.n);
   gram_combine_b_kernel<<<gb, 128, 0, s>>>(gsum, p.leaves, p.np, p.n, g, mirror, st);

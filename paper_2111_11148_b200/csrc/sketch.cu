@@ -465,7 +465,7 @@ void bm_tables_host(BmTables* t) {
 
 bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long row0, int n) {
   static const bool off = std::getenv("CQR_SKETCH_LEGACY") != nullptr;  // tuning: force the interleaved kernel
-  if (off || n <= 64 || n > 512 || (m_global & 1) || (row0 & 1)) return false;
+  if (off || n <= 64 || n > 512 || (m_global & 1) || (row0 & 1) || m_global > (1LL << 31) - 64) return false;
   CUtensorMap probe;
   return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B);
 }

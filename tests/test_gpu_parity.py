@@ -417,3 +417,26 @@ def test_one_rank_nccl_collective_path_is_bit_identical():
     bad[7, 3] = float("nan")
     with pytest.raises(ValueError):
         dist.factor_sharded(coll, _abi.RLU, bad, bad.shape[0], 0, G.SketchConfig(strategy=G.Strategy.Gaussian))
+
+
+@pytest.mark.slow
+def test_more_than_2_31_rows():
+    # 64-bit row indexing end to end (the TMA paths step aside above 2^31 rows):
+    # m = 2^31 + 1000 rows, n = 2, checked through the device diagnostics
+    import torch
+
+    free, _ = torch.cuda.mem_get_info()
+    m, n = (1 << 31) + 1000, 2
+    if free < 8 * m * n * 3 + (8 << 30):
+        pytest.skip("needs ~110 GB of free device memory")
+    ctx = G.Context(0)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
+    a[:, 1] += 0.5 * a[:, 0]
+    q = torch.empty_like(a)
+    for meth, cfg in [(_abi.CHOLQR2, None), (_abi.RQR_GAUSSIAN, G.SketchConfig(strategy=G.Strategy.Gaussian))]:
+        _, r, _ = dist.factor_sharded(ctx, meth, a, m, 0, cfg, q_out=q)
+        assert G.orthogonality_error_dev(q, ctx) < 1e-12
+        assert G.residual_error_dev(a, q, r, ctx) < 1e-14
+    del a, q
+    torch.cuda.empty_cache()
