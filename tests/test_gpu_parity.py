@@ -440,3 +440,32 @@ def test_more_than_2_31_rows():
         assert G.residual_error_dev(a, q, r, ctx) < 1e-14
     del a, q
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n", [128, 256])
+def test_strided_odd_inputs_use_the_fallback_kernels(n):
+    # an odd leading dimension and an odd row count: no TMA path applies (sketch, Gram and
+    # trisolve fall back to the cp.async / register kernels); Gram, Cholesky, LU and the
+    # trisolves are order-identical, so CholeskyQR2 and uniform-sketch rLU match the
+    # contiguous run and the oracle bit for bit; the Gaussian sketch only differs in its
+    # k-chunking (tolerance)
+    import torch
+
+    m = 30001
+    a = o.synthesize(m, n, 1e6, 4)
+    base = torch.zeros((m, n + 1), dtype=torch.float64, device="cuda")
+    base[:, :n] = torch.as_tensor(a, device="cuda")
+    a_s = base[:, :n]  # stride n + 1 (odd)
+    a_c = torch.as_tensor(a, device="cuda")
+    ctx = G.Context(0)
+    for meth, cfg in [(_abi.CHOLQR2, None), (_abi.RLU, G.SketchConfig(seed=3))]:
+        qs, rs, _ = dist.factor_sharded(ctx, meth, a_s, m, 0, cfg)
+        qc, rc, _ = dist.factor_sharded(ctx, meth, a_c, m, 0, cfg)
+        assert np.array_equal(qs.cpu().numpy(), qc.cpu().numpy()) and np.array_equal(rs, rc)
+        ref = o.factor(meth, a, None if cfg is None else cfg._c())
+        assert np.array_equal(qs.cpu().numpy(), ref.q) and np.array_equal(rs, ref.r)
+    cfg = G.SketchConfig(strategy=G.Strategy.Gaussian, seed=9)
+    qs, rs, _ = dist.factor_sharded(ctx, _abi.RQR_GAUSSIAN, a_s, m, 0, cfg)
+    ref = o.factor(_abi.RQR_GAUSSIAN, a, cfg._c())
+    assert relf(rs, ref.r) <= 1e-12
+    assert G.orthogonality_error_dev(qs, ctx) <= 1e-12
