@@ -465,7 +465,7 @@ void bm_tables_host(BmTables* t) {
 
 bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long row0, int n) {
   static const bool off = std::getenv("CQR_SKETCH_LEGACY") != nullptr;  // tuning: force the interleaved kernel
-  if (off || n <= 64 || n > 512 || (m_global & 1) || (row0 & 1) || m_global > (1LL << 31) - 64) return false;
+  if (off || n <= 32 || n > 512 || (m_global & 1) || (row0 & 1) || m_global > (1LL << 31) - 64) return false;
   CUtensorMap probe;
   return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B);
 }
@@ -479,8 +479,8 @@ SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok,
   // interleaved kernel: about 2 resident CTAs per SM over 2 waves; warp-specialised:
   // one CTA per SM, one wave (n = 128: 64 Omega rows x 128 columns per CTA; wider:
   // 32 Omega rows x 256 columns). Chunks are multiples of KS rows.
-  p.ws = ws_ok && p.np >= 128 ? 1 : 0;
-  p.st = p.ws && p.np > 128 ? 32 : kST;
+  p.ws = ws_ok && p.np >= 64 ? 1 : 0;
+  p.st = !p.ws ? kST : p.np == 64 ? 128 : p.np == 128 ? 64 : 32;  // Omega rows per CTA: DMMA work per draw
   p.npc = p.ws ? std::min(p.np, 256) : std::min(p.np, 128);
   p.s_tiles = (l + p.st - 1) / p.st;
   p.lp = p.s_tiles * p.st;
@@ -510,6 +510,7 @@ cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long lo
     if (y1 <= y0) return cudaSuccess;
     cudaError_t e0 = ensure_tables();
     if (e0 != cudaSuccess) return e0;
+    if (p.npc == 64) return launch_ws<64, 128>(p, a, lda, m_global, row0, seed, partial, check, st, s, y0, y1);
     if (p.npc == 128) return launch_ws<128, kST>(p, a, lda, m_global, row0, seed, partial, check, st, s, y0, y1);
     return launch_ws<256, 32>(p, a, lda, m_global, row0, seed, partial, check, st, s, y0, y1);
   }
