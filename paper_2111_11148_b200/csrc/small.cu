@@ -283,11 +283,25 @@ __global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restric
       const double d = P[jj * kLuLdp + jj];
       for (int r = jj + 1 + tid; r < pr; r += nt) P[r * kLuLdp + jj] = P[r * kLuLdp + jj] / d;
       __syncthreads();
-      // rank-1 update of the panel: warps over rows, lanes over the panel columns
-      for (int r = jj + 1 + warp; r < pr; r += nw) {
-        const double mult = P[r * kLuLdp + jj];
+      // rank-1 update of the panel: warps over rows (four per pass, every load issued before
+      // the stores so the passes are not serialised on possible aliasing), lanes over columns
+      {
         const int c = lane;
-        if (mult != 0.0 && c > jj && c < w) P[r * kLuLdp + c] = fma(-mult, P[jj * kLuLdp + c], P[r * kLuLdp + c]);
+        const double pc = (c > jj && c < w) ? P[jj * kLuLdp + c] : 0.0;
+        for (int rb = jj + 1 + warp; rb < pr; rb += 4 * nw) {
+          double mv[4], xv[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int r = rb + k * nw;
+            mv[k] = r < pr ? P[r * kLuLdp + jj] : 0.0;
+            xv[k] = (r < pr && c > jj && c < w) ? P[r * kLuLdp + c] : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int r = rb + k * nw;
+            if (r < pr && mv[k] != 0.0 && c > jj && c < w) P[r * kLuLdp + c] = fma(-mv[k], pc, xv[k]);
+          }
+        }
       }
       __syncthreads();
     }
