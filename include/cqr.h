@@ -162,6 +162,14 @@ int cqr_factor(cqr_ctx* ctx, int method, const double* a, int64_t m, int64_t n, 
                const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq,
                double* r, int64_t ldr, cqr_report* report);
 
+/* Host buffers, one rank of a multi-GPU job: rows [row0, row0 + m_local) of the
+ * m_global-row matrix (blocks ceil(b*m/p), cqr_block_offset); Q is this rank's
+ * rows, R the full factor (identical on every rank). Needs cqr_attach_comm;
+ * host-buffer counterpart of cqr_factor_dev (parexec::run_parallel,
+ * parexec.hpp:89-90). */
+int cqr_factor_sharded(cqr_ctx* ctx, int method, const double* a, int64_t m_local, int64_t m_global, int64_t row0,
+                       int64_t n, int64_t lda, const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q,
+                       int64_t ldq, double* r, int64_t ldr, cqr_report* report);
 /* Device buffers, row-block sharded when a communicator is attached: this
  * rank owns global rows [row0, row0 + m_local) of an m_global x n matrix
  * (blocks ceil(b*m/p), parexec.cpp:9-18). q may alias a (in-place, like the

@@ -189,6 +189,8 @@ def _lib():
                                  i64, P(_abi.Report)]),
             "cqr_factor_dev": (i32, [vp, i32, vp, i64, i64, i64, i64, i64, P(_abi.SketchCfg), P(_abi.Options),
                                      vp, i64, vp, i64, P(_abi.Report)]),
+            "cqr_factor_sharded": (i32, [vp, i32, vp, i64, i64, i64, i64, i64, P(_abi.SketchCfg), P(_abi.Options),
+                                         vp, i64, vp, i64, P(_abi.Report)]),
             "cqr_precond_factor": (i32, [vp, vp, i64, i64, i64, _abi.PRECOND_FN, vp, P(_abi.SketchCfg),
                                          P(_abi.Options), vp, i64, vp, i64, P(_abi.Report)]),
             "cqr_gram": (i32, [vp, vp, i64, i64, i64, vp]),

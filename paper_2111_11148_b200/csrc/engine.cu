@@ -900,12 +900,18 @@ int cqr_factor_dev(cqr_ctx* c, int method, const double* a, int64_t m_local, int
   return factor_dev_impl(c, j, r, ldr, report);
 }
 
-static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64_t n, int64_t lda,
-                       const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq, double* r,
-                       int64_t ldr, cqr_report* report, cqr_precond_fn fn, void* user) {
+// Host buffers: this rank's rows [row0, row0 + m) of an m_global-row matrix
+// (m_global == m, row0 == 0 for the unsharded calls).
+static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64_t m_global, int64_t row0, int64_t n,
+                       int64_t lda, const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq,
+                       double* r, int64_t ldr, cqr_report* report, cqr_precond_fn fn, void* user) {
   if (!c) return CQR_INVALID_ARGUMENT;
-  if (m < 1 || n < 1 || lda < n || ldq < n || (r && ldr < n)) {
-    c->err = "bad shape";
+  const bool sharded = m != m_global || row0 != 0;
+  if (m < 1 || n < 1 || lda < n || ldq < n || (r && ldr < n) || row0 < 0 || row0 + m > m_global ||
+      (sharded && !c->comm) || (!sharded && c->world > 1)) {
+    c->err = sharded && !c->comm     ? "sharded call without an attached communicator"
+             : !sharded && c->world > 1 ? "a multi-rank context takes its shard through cqr_factor_sharded"
+                                        : "bad shape";
     if (report) {
       std::memset(report, 0, sizeof(*report));
       report->status = CQR_INVALID_ARGUMENT;
@@ -945,8 +951,8 @@ static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64
     j.method = method;
     j.a = da;
     j.m_local = m;
-    j.m_global = m;
-    j.row0 = 0;
+    j.m_global = m_global;
+    j.row0 = row0;
     j.n = (int)n;
     j.lda = n;
     j.q = dq;
@@ -966,14 +972,21 @@ static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64
 int cqr_factor(cqr_ctx* c, int method, const double* a, int64_t m, int64_t n, int64_t lda,
                const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq, double* r, int64_t ldr,
                cqr_report* report) {
-  return factor_host(c, method, a, m, n, lda, cfg, opts, q, ldq, r, ldr, report, nullptr, nullptr);
+  return factor_host(c, method, a, m, m, 0, n, lda, cfg, opts, q, ldq, r, ldr, report, nullptr, nullptr);
+}
+
+int cqr_factor_sharded(cqr_ctx* c, int method, const double* a, int64_t m_local, int64_t m_global, int64_t row0,
+                       int64_t n, int64_t lda, const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q,
+                       int64_t ldq, double* r, int64_t ldr, cqr_report* report) {
+  return factor_host(c, method, a, m_local, m_global, row0, n, lda, cfg, opts, q, ldq, r, ldr, report, nullptr,
+                     nullptr);
 }
 
 int cqr_precond_factor(cqr_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, cqr_precond_fn precond,
                        void* user, const cqr_sketch_cfg* cfg, const cqr_options* opts, double* q, int64_t ldq,
                        double* r, int64_t ldr, cqr_report* report) {
   if (!precond) return CQR_INVALID_ARGUMENT;
-  return factor_host(c, CQR_RQR, a, m, n, lda, cfg, opts, q, ldq, r, ldr, report, precond, user);
+  return factor_host(c, CQR_RQR, a, m, m, 0, n, lda, cfg, opts, q, ldq, r, ldr, report, precond, user);
 }
 
 // ---- kernel-level entry points -------------------------------------------------------

@@ -57,3 +57,21 @@ def factor_sharded(ctx, method, a_local, m_global: int, row0: int, cfg: cq.Sketc
                                   q.stride(0), cq._ptr(r), n, C.byref(rep))
     ctx._check(st, rep.index)
     return q, (None if opts.r_less else r), rep
+
+
+def factor_sharded_host(ctx, method, a_local, m_global: int, row0: int, cfg: cq.SketchConfig | None = None,
+                        opts=None, q_out=None):
+    """cqr_factor_sharded: this rank's rows as a host (numpy, ideally pinned) buffer; the H2D of the
+    shard, the multi-GPU factorization and the D2H of Q_local happen inside. Returns (Q_local, R, report)."""
+    if opts is None:
+        opts = _abi.options()
+    cfg_c = (cfg or cq.SketchConfig())._c()
+    a_local = np.ascontiguousarray(a_local, dtype=np.float64)
+    m_local, n = a_local.shape
+    q = q_out if q_out is not None else np.empty_like(a_local)
+    r = np.zeros((n, n))
+    rep = _abi.Report()
+    st = cq._lib().cqr_factor_sharded(ctx.h, method, cq._ptr(a_local), m_local, m_global, row0, n, n,
+                                      C.byref(cfg_c), C.byref(opts), cq._ptr(q), n, cq._ptr(r), n, C.byref(rep))
+    ctx._check(st, rep.index)
+    return q, (None if opts.r_less else r), rep

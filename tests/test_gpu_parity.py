@@ -469,3 +469,18 @@ def test_strided_odd_inputs_use_the_fallback_kernels(n):
     ref = o.factor(_abi.RQR_GAUSSIAN, a, cfg._c())
     assert relf(rs, ref.r) <= 1e-12
     assert G.orthogonality_error_dev(qs, ctx) <= 1e-12
+
+
+def test_sharded_host_api_one_rank():
+    # cqr_factor_sharded (host buffers, one rank of a multi-GPU job) with a one-rank
+    # communicator equals cqr_factor bit for bit; without a communicator a real shard
+    # (m_local < m_global) is refused, as is the unsharded call on a multi-rank context
+    a = o.synthesize(12000, 40, 1e8, 8)
+    cfg = G.SketchConfig(strategy=G.Strategy.Gaussian, seed=11)
+    ref = G.rlu_cholesky_qr(a, cfg)
+    coll = G.Context(0)
+    coll.attach_comm(0, 1, G.make_comm_id())
+    q, r, _ = dist.factor_sharded_host(coll, _abi.RLU, a, a.shape[0], 0, cfg)
+    assert np.array_equal(q, ref.q) and np.array_equal(r, ref.r)
+    with pytest.raises(ValueError):
+        dist.factor_sharded_host(G.Context(0), _abi.RLU, a[:6000], a.shape[0], 0, cfg)
