@@ -560,6 +560,185 @@ __global__ void __launch_bounds__(kT) qr_kernel(const double* __restrict__ a1, i
 
 // 32x32 output tile per CTA (32x8 threads, 4 rows each); k chunks of 32 staged
 // in shared memory, ascending, so every element is the fma chain over k = 0..n-1.
+// Blocked Householder QR (compact WY) for sketches too large for shared memory
+// (e.g. c2: 512 x 256): the working matrix W (column-major) stays in the
+// L2-resident workspace; each 32-column panel is copied to shared memory and
+// factored there with the reflectors of qr_kernel (same beta / tau / v formulas,
+// fixed reduction trees), T of Q_panel = I - V T V^T is built from V^T V, and the
+// trailing columns get A2 -= V (T^T (V^T A2)) as two DMMA products. The result
+// differs from the column-by-column kernel only by rounding (tolerance parity,
+// like qr_kernel itself against the oracle).
+constexpr int kQrB = 32;
+constexpr int kQrT = 512;
+
+__global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restrict__ a1, int l, int n,
+                                                         double* __restrict__ r, double* W, DevStatus* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double scratch[33];
+  __shared__ double taus[kQrB];
+  __shared__ double T[kQrB][kQrB + 1];
+  __shared__ double s_tau, s_beta, s_denom;
+  __shared__ int s_zero;
+  if (failed(st)) return;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int ldr = l + 4;             // panel column stride (bank spread for the DMMA fragments)
+  double* Pn = smem;                 // kQrB columns of (l - j0) rows
+  double* Ys = smem + kQrB * ldr;    // kQrB x n (row stride n + 4): V^T A2, then T^T V^T A2
+  const int ldy = n + 4;
+  for (long long e = tid; e < (long long)l * n; e += nt) {
+    const int i = (int)(e / n), c = (int)(e % n);
+    W[(long long)c * l + i] = a1[e];
+  }
+  __syncthreads();
+  const double tol = 2.2250738585072014e-308 * 2.2250738585072014e-308;  // (smallest normal)^2
+  for (int j0 = 0; j0 < n; j0 += kQrB) {
+    const int b = min(kQrB, n - j0), rp = l - j0;  // panel width, panel rows
+    for (int e = tid; e < b * rp; e += nt) {
+      const int c = e / rp, i = e - (e / rp) * rp;
+      Pn[c * ldr + i] = W[(long long)(j0 + c) * l + j0 + i];
+    }
+    __syncthreads();
+    // ---- panel: Householder reflectors column by column (qr_kernel's arithmetic)
+    for (int jj = 0; jj < b; ++jj) {
+      double* col = Pn + jj * ldr;
+      double part = 0.0;
+      for (int i = jj + 1 + tid; i < rp; i += nt) part = fma(col[i], col[i], part);
+      const double tail = block_sum(part, scratch);
+      if (tid == 0) {
+        const double c0 = col[jj];
+        if (tail <= tol) {
+          s_zero = 1;
+          s_tau = 0.0;
+          s_beta = c0;
+          s_denom = 1.0;
+        } else {
+          s_zero = 0;
+          double beta = sqrt(c0 * c0 + tail);
+          if (c0 >= 0.0) beta = -beta;
+          s_beta = beta;
+          s_denom = c0 - beta;
+          s_tau = (beta - c0) / beta;
+        }
+        taus[jj] = s_tau;
+      }
+      __syncthreads();
+      const double denom = s_denom, tau = s_tau;
+      const int zero = s_zero;
+      for (int i = jj + 1 + tid; i < rp; i += nt) col[i] = zero ? 0.0 : col[i] / denom;
+      __syncthreads();
+      if (tid == 0) col[jj] = s_beta;
+      if (tau != 0.0) {  // warps own the remaining panel columns: dot, then axpy
+        for (int c = jj + 1 + warp; c < b; c += nw) {
+          double* cc = Pn + c * ldr;
+          double sdot = 0.0;
+          for (int i = jj + 1 + lane; i < rp; i += 32) sdot = fma(col[i], cc[i], sdot);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+          const double t = tau * (cc[jj] + sdot);
+          __syncwarp();
+          for (int i = jj + lane; i < rp; i += 32) cc[i] = (i == jj) ? cc[jj] - t : fma(-t, col[i], cc[i]);
+        }
+      }
+      __syncthreads();
+    }
+    // R rows of the panel back to W; V (unit diagonal, zeros above) stays in Pn
+    for (int e = tid; e < b * b; e += nt) {
+      const int c = e / b, i = e - (e / b) * b;
+      if (i <= c) W[(long long)(j0 + c) * l + j0 + i] = Pn[c * ldr + i];
+    }
+    __syncthreads();
+    for (int e = tid; e < b * rp; e += nt) {
+      const int c = e / rp, i = e - (e / rp) * rp;
+      if (i <= c) Pn[c * ldr + i] = i == c ? 1.0 : 0.0;
+    }
+    for (int e = tid; e < (kQrB - b) * rp; e += nt) Pn[(b + e / rp) * ldr + e % rp] = 0.0;  // short last panel
+    __syncthreads();
+    const int c1 = j0 + b;
+    if (c1 < n) {
+      // ---- T (upper triangular, kQrB x kQrB): T[k][k] = tau_k, T[0:k][k] = -tau_k T[0:k][0:k] (V^T v_k)[0:k]
+      for (int e = warp; e < kQrB * kQrB; e += nw) {  // G[i][k] = v_i . v_k for i < k (in T's lower half)
+        const int i = e / kQrB, k = e - (e / kQrB) * kQrB;
+        if (i >= k || k >= b) continue;
+        double sdot = 0.0;
+        for (int rr = k + lane; rr < rp; rr += 32) sdot = fma(Pn[i * ldr + rr], Pn[k * ldr + rr], sdot);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+        if (lane == 0) T[k][i] = sdot;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        for (int k = 0; k < kQrB; ++k) {
+          double v = 0.0;
+          if (k < b && lane < k) {
+            for (int jx = lane; jx < k; ++jx) v = fma(T[lane][jx], T[k][jx], v);
+            v *= -taus[k];
+          }
+          __syncwarp();
+          if (lane < k) T[lane][k] = k < b ? v : 0.0;
+          if (lane == k) T[k][k] = k < b ? taus[k] : 0.0;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      // ---- Y = V^T A2 (kQrB x n2, k over the panel rows) on DMMA
+      const int q = lane & 3, gr = lane >> 2;
+      const int n2 = n - c1, tcn = (n2 + 7) / 8;
+      for (int t = warp; t < (kQrB / 8) * tcn; t += nw) {
+        const int kt = t / tcn, ct = t - (t / tcn) * tcn;
+        const int cbase = c1 + ct * 8;
+        double y0 = 0.0, y1 = 0.0;
+        for (int r0 = 0; r0 < rp; r0 += 4) {
+          const int rr = r0 + q;
+          const double av = rr < rp ? Pn[(kt * 8 + gr) * ldr + rr] : 0.0;             // A = V^T: row k, col r
+          const int cb = cbase + gr;
+          const double bv = (rr < rp && cb < n) ? W[(long long)cb * l + j0 + rr] : 0.0;  // B = A2: row r, col c
+          dmma(y0, y1, av, bv);
+        }
+        const int cc = ct * 8 + 2 * q;
+        Ys[(kt * 8 + gr) * ldy + cc] = y0;
+        Ys[(kt * 8 + gr) * ldy + cc + 1] = y1;
+      }
+      __syncthreads();
+      // ---- Y <- T^T Y (in place, column by column of Y)
+      for (int c = tid; c < n2; c += nt) {  // k descending: z_k needs y_0..y_k, all still unwritten
+        for (int k = kQrB - 1; k >= 0; --k) {
+          double z = 0.0;
+          for (int i = 0; i <= k; ++i) z = fma(T[i][k], Ys[i * ldy + c], z);
+          Ys[k * ldy + c] = z;
+        }
+      }
+      __syncthreads();
+      // ---- A2 -= V Z on DMMA (rows of the panel range, trailing columns)
+      const int trt = (rp + 7) / 8;
+      for (int t = warp; t < trt * tcn; t += nw) {
+        const int rt = t / tcn, ct = t - (t / tcn) * tcn;
+        const int rowl = rt * 8 + gr, col = c1 + ct * 8 + 2 * q;
+        double c0v = (rowl < rp && col < n) ? W[(long long)col * l + j0 + rowl] : 0.0;
+        double c1v = (rowl < rp && col + 1 < n) ? W[(long long)(col + 1) * l + j0 + rowl] : 0.0;
+#pragma unroll
+        for (int k4 = 0; k4 < kQrB / 4; ++k4) {
+          const int kk = 4 * k4 + q;
+          const double av = rowl < rp ? -Pn[kk * ldr + rowl] : 0.0;  // A = -V: row r, col k
+          const int cz = ct * 8 + gr;
+          const double bv = cz < n2 ? Ys[kk * ldy + cz] : 0.0;          // B = Z: row k, col c
+          dmma(c0v, c1v, av, bv);
+        }
+        if (rowl < rp && col < n) W[(long long)col * l + j0 + rowl] = c0v;
+        if (rowl < rp && col + 1 < n) W[(long long)(col + 1) * l + j0 + rowl] = c1v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e / n, c = e % n;
+    r[e] = c >= i ? W[(long long)c * l + i] : 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += nt)  // normalize_r_sign (kernels.hpp:165-168)
+    if (r[(long long)i * n + i] < 0.0)
+      for (int c = i; c < n; ++c) r[(long long)i * n + c] = -r[(long long)i * n + c];
+}
+
 __global__ void triangular_product_kernel(const double* __restrict__ left, const double* __restrict__ right, int n,
                                           double* __restrict__ out, const DevStatus* st) {
   __shared__ double sl[32][33], sr[32][33];
@@ -659,6 +838,13 @@ cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work,
   if (n > 512) return cudaErrorInvalidValue;
   const size_t bytes = (size_t)l * n * sizeof(double);
   const int use_smem = bytes <= kSmemCap;
+  const size_t bsmem = ((size_t)kQrB * (l + 4) + (size_t)kQrB * (n + 4)) * sizeof(double);
+  if (!use_smem && bsmem <= 200 * 1024) {  // blocked: the panel and V^T A2 in shared memory
+    cudaError_t e = cudaFuncSetAttribute(qr_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+    if (e != cudaSuccess) return e;
+    qr_blocked_kernel<<<1, kQrT, bsmem, s>>>(a1, l, n, r, work, st);
+    return cudaGetLastError();
+  }
   return launch_small(qr_kernel, bytes, s, a1, l, n, r, work, use_smem, st);
 }
 

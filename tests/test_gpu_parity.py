@@ -185,7 +185,8 @@ def test_lu_known_and_singular():
         G.lu_u_factor(z)
 
 
-@pytest.mark.parametrize("l,n,seed", [(2, 1, 1), (40, 10, 2), (128, 64, 3), (256, 128, 4), (512, 256, 5)])
+@pytest.mark.parametrize("l,n,seed", [(2, 1, 1), (40, 10, 2), (128, 64, 3), (256, 128, 4), (512, 256, 5),
+                                      (700, 300, 6), (1000, 100, 7), (310, 290, 8)])
 def test_qr_r_tolerance(l, n, seed):
     a1 = o.gaussian_matrix(l, n, seed)
     # different reduction trees: R agrees to a small multiple of u*cond
