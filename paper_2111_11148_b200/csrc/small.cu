@@ -636,7 +636,20 @@ __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restri
           for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
           const double t = tau * (cc[jj] + sdot);
           __syncwarp();
-          for (int i = jj + lane; i < rp; i += 32) cc[i] = (i == jj) ? cc[jj] - t : fma(-t, col[i], cc[i]);
+          for (int i0 = jj; i0 < rp; i0 += 128) {  // four rows per lane and pass, loads ahead of the stores
+            double cv[4], xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + lane + 32 * u;
+              cv[u] = (i > jj && i < rp) ? col[i] : 0.0;
+              xv[u] = i < rp ? cc[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + lane + 32 * u;
+              if (i < rp) cc[i] = (i == jj) ? xv[u] - t : fma(-t, cv[u], xv[u]);
+            }
+          }
         }
       }
       __syncthreads();
@@ -687,12 +700,17 @@ __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restri
         const int kt = t / tcn, ct = t - (t / tcn) * tcn;
         const int cbase = c1 + ct * 8;
         double y0 = 0.0, y1 = 0.0;
-        for (int r0 = 0; r0 < rp; r0 += 4) {
-          const int rr = r0 + q;
-          const double av = rr < rp ? Pn[(kt * 8 + gr) * ldr + rr] : 0.0;             // A = V^T: row k, col r
-          const int cb = cbase + gr;
-          const double bv = (rr < rp && cb < n) ? W[(long long)cb * l + j0 + rr] : 0.0;  // B = A2: row r, col c
-          dmma(y0, y1, av, bv);
+        const int cb = cbase + gr;
+        for (int r0 = 0; r0 < rp; r0 += 32) {  // 8 k-steps per pass, every load issued before the chain
+          double av[8], bv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int rr = r0 + 4 * u + q;
+            av[u] = rr < rp ? Pn[(kt * 8 + gr) * ldr + rr] : 0.0;             // A = V^T: row k, col r
+            bv[u] = (rr < rp && cb < n) ? W[(long long)cb * l + j0 + rr] : 0.0;  // B = A2: row r, col c
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) dmma(y0, y1, av[u], bv[u]);
         }
         const int cc = ct * 8 + 2 * q;
         Ys[(kt * 8 + gr) * ldy + cc] = y0;
@@ -709,22 +727,36 @@ __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restri
       }
       __syncthreads();
       // ---- A2 -= V Z on DMMA (rows of the panel range, trailing columns)
-      const int trt = (rp + 7) / 8;
-      for (int t = warp; t < trt * tcn; t += nw) {
-        const int rt = t / tcn, ct = t - (t / tcn) * tcn;
-        const int rowl = rt * 8 + gr, col = c1 + ct * 8 + 2 * q;
-        double c0v = (rowl < rp && col < n) ? W[(long long)col * l + j0 + rowl] : 0.0;
-        double c1v = (rowl < rp && col + 1 < n) ? W[(long long)(col + 1) * l + j0 + rowl] : 0.0;
+      const int trt = (rp + 7) / 8, ntile = trt * tcn;
+      for (int t0 = warp; t0 < ntile; t0 += 2 * nw) {  // two tiles per pass: their global loads overlap
+        double c0v[2], c1v[2], av[2][kQrB / 4], bv[2][kQrB / 4];
+        int rowl[2], col[2];
 #pragma unroll
-        for (int k4 = 0; k4 < kQrB / 4; ++k4) {
-          const int kk = 4 * k4 + q;
-          const double av = rowl < rp ? -Pn[kk * ldr + rowl] : 0.0;  // A = -V: row r, col k
-          const int cz = ct * 8 + gr;
-          const double bv = cz < n2 ? Ys[kk * ldy + cz] : 0.0;          // B = Z: row k, col c
-          dmma(c0v, c1v, av, bv);
+        for (int h = 0; h < 2; ++h) {
+          const int t = t0 + h * nw;
+          const bool live = t < ntile;
+          const int rt = live ? t / tcn : 0, ct = live ? t - (t / tcn) * tcn : 0;
+          rowl[h] = live ? rt * 8 + gr : rp;
+          col[h] = c1 + ct * 8 + 2 * q;
+          c0v[h] = (rowl[h] < rp && col[h] < n) ? W[(long long)col[h] * l + j0 + rowl[h]] : 0.0;
+          c1v[h] = (rowl[h] < rp && col[h] + 1 < n) ? W[(long long)(col[h] + 1) * l + j0 + rowl[h]] : 0.0;
+#pragma unroll
+          for (int k4 = 0; k4 < kQrB / 4; ++k4) {
+            const int kk = 4 * k4 + q;
+            av[h][k4] = rowl[h] < rp ? -Pn[kk * ldr + rowl[h]] : 0.0;  // A = -V: row r, col k
+            const int cz = ct * 8 + gr;
+            bv[h][k4] = cz < n2 ? Ys[kk * ldy + cz] : 0.0;          // B = Z: row k, col c
+          }
         }
-        if (rowl < rp && col < n) W[(long long)col * l + j0 + rowl] = c0v;
-        if (rowl < rp && col + 1 < n) W[(long long)(col + 1) * l + j0 + rowl] = c1v;
+#pragma unroll
+        for (int k4 = 0; k4 < kQrB / 4; ++k4)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) dmma(c0v[h], c1v[h], av[h][k4], bv[h][k4]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (rowl[h] < rp && col[h] < n) W[(long long)col[h] * l + j0 + rowl[h]] = c0v[h];
+          if (rowl[h] < rp && col[h] + 1 < n) W[(long long)(col[h] + 1) * l + j0 + rowl[h]] = c1v[h];
+        }
       }
     }
     __syncthreads();
