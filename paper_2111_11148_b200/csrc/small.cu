@@ -16,6 +16,7 @@
 //  normalize_sign_kernel      engine.cpp:109-116 (R rows; Q columns via sgn).
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -369,6 +370,181 @@ __global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restric
   }
   for (int i = warp; i < n; i += nw)
     for (int c = lane; c < n; c += 32) u[(long long)i * n + c] = c >= i ? W[(long long)i * n + c] : 0.0;
+}
+
+// l <= 512: one thread per physical row, the panel's 32 columns of that row in
+// registers. Rows never move: partial pivoting is tracked with logical
+// positions (ties go to the smallest one: the reference's "first maximum" in its
+// swapped order), each thread updating its own position from the arg-max. The
+// current column is always x[0] (the row is shifted one place per step, so the
+// step loop stays rolled: no dynamic register indexing, a small I-cache
+// footprint). Per pivot step: one arg-max barrier, one barrier to publish the
+// pivot row, register fma updates; U rows go straight to the output.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restrict__ a1, int l, int n,
+                                                        double* __restrict__ u, double* W, DevStatus* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double prow[kLuPanel];
+  __shared__ double wb[2][NW];
+  __shared__ int wl[2][NW], wr[2][NW];
+  __shared__ int pv[kLuPanel];
+  if (failed(st)) return;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  double* P = smem;                                                    // multipliers: l x kLuLdp
+  int* lpS = reinterpret_cast<int*>(smem + (size_t)l * kLuLdp);        // logical positions after a panel
+  const bool mine = tid < l;
+  {  // W = A1, eight independent loads in flight per thread
+    const long long total = (long long)l * n;
+    for (long long e0 = tid; e0 < total; e0 += 8LL * nt) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = e0 + k * nt < total ? __ldg(a1 + e0 + k * nt) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (e0 + k * nt < total) W[e0 + k * nt] = v[k];
+    }
+  }
+  for (int i = warp; i < n; i += NW)
+    for (int c = lane; c < i; c += 32) u[(long long)i * n + c] = 0.0;
+  int my_lp = tid, buf = 0;
+  __syncthreads();
+  for (int j0 = 0; j0 < n; j0 += kLuPanel) {
+    const int w = min(kLuPanel, n - j0);
+    double x[kLuPanel];
+#pragma unroll
+    for (int c = 0; c < kLuPanel; ++c) x[c] = (mine && c < w) ? W[(long long)tid * n + j0 + c] : 0.0;
+#pragma unroll 1
+    for (int jj = 0; jj < w; ++jj) {
+      const int j = j0 + jj;
+      const bool act = mine && my_lp >= j;
+      double best = act ? fabs(x[0]) : -1.0;
+      int blp = act ? my_lp : 0x7fffffff, brow = tid;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, blp, o);
+        const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+        if (ob > best || (ob == best && ol < blp)) {
+          best = ob;
+          blp = ol;
+          brow = orow;
+        }
+      }
+      if (lane == 0) {
+        wb[buf][warp] = best;
+        wl[buf][warp] = blp;
+        wr[buf][warp] = brow;
+      }
+      __syncthreads();
+      {  // the NW warp winners, reduced by shuffles in every warp (all take the same decision)
+        const int k = lane % NW;
+        best = wb[buf][k];
+        blp = wl[buf][k];
+        brow = wr[buf][k];
+#pragma unroll
+        for (int o = NW / 2; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, blp, o);
+          const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+          if (ob > best || (ob == best && ol < blp)) {
+            best = ob;
+            blp = ol;
+            brow = orow;
+          }
+        }
+      }
+      buf ^= 1;
+      if (!(best > 0.0)) {  // exact zero pivot (kernels.hpp:235)
+        if (tid == 0) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, j);
+        return;
+      }
+      const int ps = brow;
+      if (tid == ps) {
+#pragma unroll
+        for (int c = 0; c < kLuPanel; ++c) {
+          prow[c] = x[c];
+          if (c < w - jj) u[(long long)j * n + j + c] = x[c];  // U row j, panel part
+        }
+        pv[jj] = ps;
+      }
+      __syncthreads();
+      if (act && tid != ps) {
+        const double mult = x[0] / prow[0];
+        P[tid * kLuLdp + jj] = mult;
+        if (mult != 0.0) {
+#pragma unroll
+          for (int c = 1; c < kLuPanel; ++c) x[c] = fma(-mult, prow[c], x[c]);
+        }
+      }
+      if (tid == ps)
+        my_lp = j;
+      else if (my_lp == j)
+        my_lp = blp;  // the row at position j takes the pivot's old position
+#pragma unroll
+      for (int c = 0; c < kLuPanel - 1; ++c) x[c] = x[c + 1];
+      x[kLuPanel - 1] = 0.0;
+    }
+    if (mine) lpS[tid] = my_lp;
+    __syncthreads();
+    const int c1 = j0 + w;
+    if (c1 < n) {
+      // U12 = L11^-1 A12 on the pivot rows: one thread per trailing column, fma chain over
+      // the panel's pivots in order, zero multipliers skipped
+      for (int c = c1 + tid; c < n; c += nt) {
+        double y[kLuPanel];
+#pragma unroll
+        for (int jj = 0; jj < kLuPanel; ++jj) y[jj] = jj < w ? W[(long long)pv[jj] * n + c] : 0.0;
+#pragma unroll
+        for (int jj = 1; jj < kLuPanel; ++jj) {
+          if (jj < w) {
+            const double* pr = P + pv[jj] * kLuLdp;
+#pragma unroll
+            for (int k = 0; k < jj; ++k) {
+              const double mult = pr[k];
+              if (mult != 0.0) y[jj] = fma(-mult, y[k], y[jj]);
+            }
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < kLuPanel; ++jj)
+          if (jj < w) u[(long long)(j0 + jj) * n + c] = y[jj];
+      }
+      __syncthreads();
+      // A22 += (-L21) U12 on DMMA for the rows still unpivoted (k = pivots in order)
+      const int q = lane & 3, gr = lane >> 2;
+      const int tr = (l + 7) / 8, tc = (n - c1 + 7) / 8;
+      for (int t = warp; t < tr * tc; t += NW) {
+        const int rt = t / tc, ct = t - (t / tc) * tc;
+        const int row = rt * 8 + gr, cc0 = c1 + ct * 8, col = cc0 + 2 * q;
+        const bool live = row < l && lpS[row] >= c1;
+        if (!__any_sync(0xffffffffu, live)) continue;
+        double c0v = (live && col < n) ? W[(long long)row * n + col] : 0.0;
+        double c1v = (live && col + 1 < n) ? W[(long long)row * n + col + 1] : 0.0;
+        double av[kLuPanel / 4], bv[kLuPanel / 4];
+#pragma unroll
+        for (int k4 = 0; k4 < kLuPanel / 4; ++k4) {
+          const int kk = 4 * k4 + q;
+          av[k4] = (row < l && kk < w) ? -P[row * kLuLdp + kk] : 0.0;  // A: row gr, k = q
+          const int bc = cc0 + gr;
+          bv[k4] = (kk < w && bc < n) ? u[(long long)(j0 + kk) * n + bc] : 0.0;  // B: k = q, col = gr
+        }
+#pragma unroll
+        for (int k4 = 0; k4 < kLuPanel / 4; ++k4) dmma(c0v, c1v, av[k4], bv[k4]);
+        if (live && col < n) W[(long long)row * n + col] = c0v;
+        if (live && col + 1 < n) W[(long long)row * n + col + 1] = c1v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int NW>
+cudaError_t launch_lu_rot(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
+  const size_t smem = (size_t)l * kLuLdp * sizeof(double) + (size_t)l * sizeof(int);
+  cudaError_t e = cudaFuncSetAttribute(lu_rot_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  lu_rot_kernel<NW><<<1, NW * 32, smem, s>>>(a1, l, n, u, work, st);
+  return cudaGetLastError();
 }
 
 // Blocked right-looking Cholesky (kernels.hpp:76-90 in the oracle's pinned
@@ -844,6 +1020,14 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
 }
 
 cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
+  static const bool legacy = std::getenv("CQR_LU_LEGACY") != nullptr;  // tuning: the swapping blocked kernel
+  if (!legacy && l <= 512 && (size_t)l * kLuLdp * sizeof(double) + (size_t)l * sizeof(int) <= 220 * 1024) {
+    // as few warps as rows need: the per-step barriers and arg-max dominate (8 vs 16 warps at
+    // l = 256: 276 vs 332 us)
+    if (l <= 128) return launch_lu_rot<4>(a1, l, n, u, work, st, s);
+    if (l <= 256) return launch_lu_rot<8>(a1, l, n, u, work, st, s);
+    return launch_lu_rot<16>(a1, l, n, u, work, st, s);
+  }
   {
     const bool fits = (size_t)l * kLuLdp * sizeof(double) <= 220 * 1024;
     const size_t smem = fits ? (size_t)l * kLuLdp * sizeof(double) : 0;
