@@ -403,7 +403,14 @@ __global__ void gram_combine_b_kernel(const double* __restrict__ gsum, int leave
   const double* p = gsum + (long long)i * np + j;
   double stk[40];
   int top = 0;
-  for (int k = 0; k < full; ++k) push_merge(stk, top, __ldg(p + (long long)k * stride), (unsigned)(k + 1));
+  for (int k0 = 0; k0 < full; k0 += 8) {  // eight loads in flight, merged in order
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = k0 + u < full ? __ldg(p + (long long)(k0 + u) * stride) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < full) push_merge(stk, top, v[u], (unsigned)(k0 + u + 1));
+  }
   if (groups > full) stk[top++] = __ldg(p + (long long)full * stride);
   double acc = stk[top - 1];
   for (int k = top - 2; k >= 0; --k) acc = stk[k] + acc;
