@@ -380,14 +380,14 @@ __global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restric
 // step loop stays rolled: no dynamic register indexing, a small I-cache
 // footprint). Per pivot step: one arg-max barrier, one barrier to publish the
 // pivot row, register fma updates; U rows go straight to the output.
-template <int NW>
+template <int NW, int PW>
 __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restrict__ a1, int l, int n,
                                                         double* __restrict__ u, double* W, DevStatus* st) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double prow[kLuPanel];
+  __shared__ double prow[PW];
   __shared__ double wb[2][NW];
   __shared__ int wl[2][NW], wr[2][NW];
-  __shared__ int pv[kLuPanel];
+  __shared__ int pv[PW];
   if (failed(st)) return;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   double* P = smem;                                                    // multipliers: l x kLuLdp
@@ -408,11 +408,11 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
     for (int c = lane; c < i; c += 32) u[(long long)i * n + c] = 0.0;
   int my_lp = tid, buf = 0;
   __syncthreads();
-  for (int j0 = 0; j0 < n; j0 += kLuPanel) {
-    const int w = min(kLuPanel, n - j0);
-    double x[kLuPanel];
+  for (int j0 = 0; j0 < n; j0 += PW) {
+    const int w = min(PW, n - j0);
+    double x[PW];
 #pragma unroll
-    for (int c = 0; c < kLuPanel; ++c) x[c] = (mine && c < w) ? W[(long long)tid * n + j0 + c] : 0.0;
+    for (int c = 0; c < PW; ++c) x[c] = (mine && c < w) ? W[(long long)tid * n + j0 + c] : 0.0;
 #pragma unroll 1
     for (int jj = 0; jj < w; ++jj) {
       const int j = j0 + jj;
@@ -437,12 +437,13 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       }
       __syncthreads();
       {  // the NW warp winners, reduced by shuffles in every warp (all take the same decision)
-        const int k = lane % NW;
-        best = wb[buf][k];
-        blp = wl[buf][k];
-        brow = wr[buf][k];
+        constexpr int NWP = NW <= 4 ? 4 : NW <= 8 ? 8 : NW <= 16 ? 16 : 32;  // power-of-two butterfly
+        const int k = lane % NWP;
+        best = k < NW ? wb[buf][k] : -1.0;
+        blp = k < NW ? wl[buf][k] : 0x7fffffff;
+        brow = k < NW ? wr[buf][k] : 0;
 #pragma unroll
-        for (int o = NW / 2; o > 0; o >>= 1) {
+        for (int o = NWP / 2; o > 0; o >>= 1) {
           const double ob = __shfl_xor_sync(0xffffffffu, best, o);
           const int ol = __shfl_xor_sync(0xffffffffu, blp, o);
           const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       const int ps = brow;
       if (tid == ps) {
 #pragma unroll
-        for (int c = 0; c < kLuPanel; ++c) {
+        for (int c = 0; c < PW; ++c) {
           prow[c] = x[c];
           if (c < w - jj) u[(long long)j * n + j + c] = x[c];  // U row j, panel part
         }
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
         P[tid * kLuLdp + jj] = mult;
         if (mult != 0.0) {
 #pragma unroll
-          for (int c = 1; c < kLuPanel; ++c) x[c] = fma(-mult, prow[c], x[c]);
+          for (int c = 1; c < PW; ++c) x[c] = fma(-mult, prow[c], x[c]);
         }
       }
       if (tid == ps)
@@ -481,8 +482,8 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       else if (my_lp == j)
         my_lp = blp;  // the row at position j takes the pivot's old position
 #pragma unroll
-      for (int c = 0; c < kLuPanel - 1; ++c) x[c] = x[c + 1];
-      x[kLuPanel - 1] = 0.0;
+      for (int c = 0; c < PW - 1; ++c) x[c] = x[c + 1];
+      x[PW - 1] = 0.0;
     }
     if (mine) lpS[tid] = my_lp;
     __syncthreads();
@@ -491,11 +492,11 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       // U12 = L11^-1 A12 on the pivot rows: one thread per trailing column, fma chain over
       // the panel's pivots in order, zero multipliers skipped
       for (int c = c1 + tid; c < n; c += nt) {
-        double y[kLuPanel];
+        double y[PW];
 #pragma unroll
-        for (int jj = 0; jj < kLuPanel; ++jj) y[jj] = jj < w ? W[(long long)pv[jj] * n + c] : 0.0;
+        for (int jj = 0; jj < PW; ++jj) y[jj] = jj < w ? W[(long long)pv[jj] * n + c] : 0.0;
 #pragma unroll
-        for (int jj = 1; jj < kLuPanel; ++jj) {
+        for (int jj = 1; jj < PW; ++jj) {
           if (jj < w) {
             const double* pr = P + pv[jj] * kLuLdp;
 #pragma unroll
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
           }
         }
 #pragma unroll
-        for (int jj = 0; jj < kLuPanel; ++jj)
+        for (int jj = 0; jj < PW; ++jj)
           if (jj < w) u[(long long)(j0 + jj) * n + c] = y[jj];
       }
       __syncthreads();
@@ -520,16 +521,16 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
         if (!__any_sync(0xffffffffu, live)) continue;
         double c0v = (live && col < n) ? W[(long long)row * n + col] : 0.0;
         double c1v = (live && col + 1 < n) ? W[(long long)row * n + col + 1] : 0.0;
-        double av[kLuPanel / 4], bv[kLuPanel / 4];
+        double av[PW / 4], bv[PW / 4];
 #pragma unroll
-        for (int k4 = 0; k4 < kLuPanel / 4; ++k4) {
+        for (int k4 = 0; k4 < PW / 4; ++k4) {
           const int kk = 4 * k4 + q;
           av[k4] = (row < l && kk < w) ? -P[row * kLuLdp + kk] : 0.0;  // A: row gr, k = q
           const int bc = cc0 + gr;
           bv[k4] = (kk < w && bc < n) ? u[(long long)(j0 + kk) * n + bc] : 0.0;  // B: k = q, col = gr
         }
 #pragma unroll
-        for (int k4 = 0; k4 < kLuPanel / 4; ++k4) dmma(c0v, c1v, av[k4], bv[k4]);
+        for (int k4 = 0; k4 < PW / 4; ++k4) dmma(c0v, c1v, av[k4], bv[k4]);
         if (live && col < n) W[(long long)row * n + col] = c0v;
         if (live && col + 1 < n) W[(long long)row * n + col + 1] = c1v;
       }
@@ -538,12 +539,12 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
   }
 }
 
-template <int NW>
+template <int NW, int PW>
 cudaError_t launch_lu_rot(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
   const size_t smem = (size_t)l * kLuLdp * sizeof(double) + (size_t)l * sizeof(int);
-  cudaError_t e = cudaFuncSetAttribute(lu_rot_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(lu_rot_kernel<NW, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  lu_rot_kernel<NW><<<1, NW * 32, smem, s>>>(a1, l, n, u, work, st);
+  lu_rot_kernel<NW, PW><<<1, NW * 32, smem, s>>>(a1, l, n, u, work, st);
   return cudaGetLastError();
 }
 
@@ -1024,10 +1025,12 @@ cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work,
   if (!legacy && l <= 512 && (size_t)l * kLuLdp * sizeof(double) + (size_t)l * sizeof(int) <= 220 * 1024) {
     // as few warps as rows need: the per-step barriers and arg-max dominate (8 vs 16 warps at
     // l = 256: 276 vs 332 us)
-    if (l <= 128) return launch_lu_rot<4>(a1, l, n, u, work, st, s);
-    if (l <= 256) return launch_lu_rot<8>(a1, l, n, u, work, st, s);
-    return launch_lu_rot<16>(a1, l, n, u, work, st, s);
+    if (l <= 128) return launch_lu_rot<4, kLuPanel>(a1, l, n, u, work, st, s);
+    if (l <= 256) return launch_lu_rot<8, kLuPanel>(a1, l, n, u, work, st, s);
+    return launch_lu_rot<16, kLuPanel>(a1, l, n, u, work, st, s);
   }
+  // taller sketches (c4: 768 x 512) keep the swapping kernel: 24 warps x 16-column panels measured slower
+  // (6.08 vs 4.95 ms)
   {
     const bool fits = (size_t)l * kLuLdp * sizeof(double) <= 220 * 1024;
     const size_t smem = fits ? (size_t)l * kLuLdp * sizeof(double) : 0;
