@@ -485,3 +485,54 @@ def test_sharded_host_api_one_rank():
     assert np.array_equal(q, ref.q) and np.array_equal(r, ref.r)
     with pytest.raises(ValueError):
         dist.factor_sharded_host(G.Context(0), _abi.RLU, a[:6000], a.shape[0], 0, cfg)
+
+
+def test_randomized_parity_sweep():
+    # 96 random shapes across every method and both sketch strategies, host buffers and
+    # strided device views; status (ok / breakdown / singular, with index) must match the
+    # oracle; bit-identical Q and R for the order-pinned methods, tolerances otherwise
+    import torch
+
+    rng = np.random.default_rng(2024)
+    exact = {_abi.CHOLQR, _abi.CHOLQR2, _abi.SCHOLQR3}
+    for case in range(96):
+        meth = int(rng.choice([_abi.CHOLQR, _abi.CHOLQR2, _abi.SCHOLQR3, _abi.RLU, _abi.RQR, _abi.RQR_GAUSSIAN]))
+        n = int(rng.integers(1, 131))
+        m = int(rng.integers(n, max(n + 1, 6000)))
+        kappa = float(10.0 ** rng.uniform(0, 9))
+        gauss = meth == _abi.RQR_GAUSSIAN or (meth == _abi.RLU and rng.random() < 0.5)
+        l = int(rng.integers(n, min(m, 3 * n) + 1))
+        seed = int(rng.integers(1, 1 << 30))
+        a = o.synthesize(m, n, kappa, seed)
+        cfg_c = _abi.sketch_cfg(strategy=_abi.GAUSSIAN if gauss else _abi.UNIFORM, size=l, seed=seed + 7)
+        cfg = G.SketchConfig(strategy=G.Strategy.Gaussian if gauss else G.Strategy.Uniform, size=l, seed=seed + 7)
+        try:
+            ref = o.factor(meth, a, cfg_c)
+            ref_err = None
+        except o.OracleError as e:
+            ref, ref_err = None, e
+        use_dev = rng.random() < 0.4
+        try:
+            if use_dev:  # strided device view (leading dimension n + 3)
+                base = torch.zeros((m, n + 3), dtype=torch.float64, device="cuda")
+                base[:, :n] = torch.as_tensor(a, device="cuda")
+                qd, r, _ = dist.factor_sharded(G.context(0), meth, base[:, :n], m, 0, cfg)
+                q = qd.cpu().numpy()
+            else:
+                f, _, _ = G._factor(meth, a, cfg, _abi.options())
+                q, r = f.q, f.r
+            err = None
+        except (G.CholeskyBreakdown, G.SingularTriangular) as e:
+            err = e
+        ctx_msg = f"case {case}: method {meth} m={m} n={n} l={l} kappa={kappa:.1e} gauss={gauss} dev={use_dev}"
+        if ref_err is not None:
+            assert err is not None, ctx_msg
+            idx = getattr(err, "pivot_index", getattr(err, "index", None))
+            assert idx == ref_err.index, ctx_msg
+            continue
+        if meth in exact or (meth == _abi.RLU and not gauss):
+            assert err is None and np.array_equal(q, ref.q) and np.array_equal(r, ref.r), ctx_msg
+        else:
+            assert err is None, ctx_msg
+            assert relf(r, ref.r) <= 1e-11, ctx_msg
+            assert o.orthogonality_error(q) <= max(2 * o.orthogonality_error(ref.q), 1e-11), ctx_msg
