@@ -536,3 +536,23 @@ def test_randomized_parity_sweep():
             assert err is None, ctx_msg
             assert relf(r, ref.r) <= 1e-11, ctx_msg
             assert o.orthogonality_error(q) <= max(2 * o.orthogonality_error(ref.q), 1e-11), ctx_msg
+
+
+def test_randomized_kernel_sweep():
+    # the kernel-level entry points at random shapes around every padding boundary
+    rng = np.random.default_rng(77)
+    widths = [1, 2, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 200, 255, 256, 257, 384, 511, 512]
+    for case in range(40):
+        n = int(rng.choice(widths))
+        m = int(rng.integers(n, n + 3000))
+        seed = int(rng.integers(1, 1 << 30))
+        x = o.gaussian_matrix(m, n, seed)
+        g = o.gram(x)
+        assert np.array_equal(G.gram(x), g), (case, m, n)
+        rr = o.cholesky_upper(g)
+        assert np.array_equal(G.cholesky_upper(g), rr), (case, n)
+        assert np.array_equal(G.right_trisolve(x, rr), o.right_trisolve(x, rr)), (case, m, n)
+        l = int(rng.integers(n, 2 * n + 2))
+        a1 = o.gaussian_matrix(l, n, seed + 1)
+        assert np.array_equal(G.lu_u_factor(a1), o.lu_u_factor(a1)), (case, l, n)
+        assert relf(G.qr_r_factor(a1), o.qr_r_factor(a1)) <= 1e-12, (case, l, n)
