@@ -61,8 +61,9 @@ def test_rng_gaussian_within_ulps():
         n = 200000
         gd = G.rng_gaussian(seed, 12345, n)
         go = o.gaussian_fill(seed, 12345, n)
-        # CUDA log/sincos vs glibc: |diff| <= 8 ulp of max(|g|, 1)
-        tol = 8 * U * np.maximum(np.abs(go), 1.0)
+        # table Box-Muller vs glibc: |diff| <= 16 ulp of max(|g|, 1) (1e7 draws: max 12.5, the
+        # absolute error of cos/sin near their zeros times r <= 8.6; tools/gpu/bm_acc.py)
+        tol = 16 * U * np.maximum(np.abs(go), 1.0)
         assert np.all(np.abs(gd - go) <= tol)
         assert np.mean(gd == go) > 0.5  # most draws are bit-identical
 
