@@ -41,11 +41,13 @@ __device__ __forceinline__ void gaussian_pair_fast(const BmTables& T, uint64_t s
                                                    double& g_odd) {
   const uint64_t b1 = mix64(seed + (2 * p + 1) * 0x9E3779B97F4A7C15ull);
   const uint64_t b2 = mix64(seed + (2 * p + 2) * 0x9E3779B97F4A7C15ull);
-  const double u1 = (double)((b1 >> 11) + 1) * 0x1.0p-53;
+  // u1 = N1 * 2^-53 with N1 = (b1 >> 11) + 1 in [1, 2^53]: the scaling is folded into the
+  // exponent below (N1's double has u1's mantissa bits, its exponent is 53 higher)
+  const double n1 = (double)((b1 >> 11) + 1);
   const double u2 = (double)(b2 >> 11) * 0x1.0p-53;
   // ---- log(u1)
-  const int hi = __double2hiint(u1), lo = __double2loint(u1);
-  int e = (hi >> 20) - 1023;
+  const int hi = __double2hiint(n1), lo = __double2loint(n1);
+  int e = (hi >> 20) - 1023 - 53;
   const int mh = hi & 0xFFFFF;
   const int i = mh >> 13;
   double f = __hiloint2double(mh | 0x3FF00000, lo);
