@@ -34,6 +34,29 @@ KAPPA = 1e14
 SEED = 1
 CPU_SAMPLE_ROWS = 100_000
 WORKLOAD = "c1: rLU-CholeskyQR fp64, m=1e6 rows/GPU, n=128, Gaussian sketch s=256, cond 1e14"
+# BASELINE.json configs (per-GPU shapes; c1 is the benchmark line, the others via --workload):
+# name -> (method name, m per GPU, n, sketch rows l, kappa or "two-segment", description)
+WORKLOADS = {
+    "c1": ("rlu", M_PER_GPU, N, 256, KAPPA, WORKLOAD),
+    "c2": ("rqr-gaussian", 4_000_000, 256, 512, 1e12,
+           "c2: rQR-CholeskyQR (Gaussian) fp64, m=4e6 rows/GPU, n=256, s=512, cond 1e12"),
+    "c3": ("rqr-gaussian", 4_194_304, 64, 128, 1e15,
+           "c3: rQR-CholeskyQR (Gaussian) fp64, m=4194304 rows/GPU, n=64, s=128, cond 1e15"),
+    "c4": ("rlu", 1_000_000, 512, 768, "two-segment",
+           "c4: rLU-CholeskyQR (Gaussian) fp64, m=1e6 rows/GPU, n=512, s=768, sigma 10^(-8i/255) then 1e-8"),
+}
+
+
+def workload_sigma(n, kappa):
+    import numpy as np
+
+    if kappa == "two-segment":  # BASELINE.json c4
+        s = np.full(n, 1e-8)
+        s[:256] = 10.0 ** (-8.0 * np.arange(256) / 255.0)
+        return s
+    from paper_2111_11148_b200 import cholqr as cq
+
+    return cq.geometric_sigma(n, kappa)
 
 
 def flops_rlu(m, n, l):
@@ -101,7 +124,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_input(m_local, n, rank, world, device, kappa=None, ctx=None):
+def make_input(m_local, n, rank, world, device, kappa=None, ctx=None, sigma=None):
     """Rows [rank*m_local, (rank+1)*m_local) of A = U diag(sigma) V^T, generated on
     the device by the library (matgen.cpp:21-46 restated: counter-RNG Gaussians,
     seeds derive(SEED, 0/1), orthonormalised across all ranks)."""
@@ -112,7 +135,7 @@ def make_input(m_local, n, rank, world, device, kappa=None, ctx=None):
 
         ctx = dist.make_context(device.index if hasattr(device, "index") else int(device), rank, world)
     k = KAPPA if kappa is None else kappa
-    return cq.synthesize_dev(m_local, n, k, SEED, device=ctx.device, m_global=m_local * world,
+    return cq.synthesize_dev(m_local, n, k, SEED, sigma=sigma, device=ctx.device, m_global=m_local * world,
                              row0=rank * m_local, ctx=ctx)
 
 
@@ -133,17 +156,18 @@ def run_ours(args):
     if world > 1:
         td.init_process_group("nccl", device_id=dev)
     ctx = dist.make_context(local, rank, world)
-    m_local, n = M_PER_GPU, N
+    mname, m_local, n, l_req, kap, wdesc = WORKLOADS[args.workload]
+    method = {v: k for k, v in _abi.METHOD_NAMES.items()}[mname]
     m_global = m_local * world
     row0 = rank * m_local
-    a = make_input(m_local, n, rank, world, dev, ctx=ctx)
+    a = make_input(m_local, n, rank, world, dev, ctx=ctx, sigma=workload_sigma(n, kap))
     q = torch.empty_like(a)
-    cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=RATE, seed=_seed_value())
+    cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, size=l_req, rate=RATE, seed=_seed_value())
     l = cfg.resolved_size(m_global, n)
     opts = _abi.options()
 
     def step():
-        return dist.factor_sharded(ctx, _abi.RLU, a, m_global, row0, cfg, opts, q_out=q)
+        return dist.factor_sharded(ctx, method, a, m_global, row0, cfg, opts, q_out=q)
 
     for _ in range(args.warmup):
         step()
@@ -191,10 +215,10 @@ def run_ours(args):
     def e2e_step():
         import ctypes as C
         if world == 1:
-            st = cq._lib().cqr_factor(ctx.h, _abi.RLU, C.c_void_p(an.ctypes.data), m_local, n, n, C.byref(cfg_c),
+            st = cq._lib().cqr_factor(ctx.h, method, C.c_void_p(an.ctypes.data), m_local, n, n, C.byref(cfg_c),
                                       C.byref(opts), C.c_void_p(qn.ctypes.data), n, cq._ptr(rh), n, C.byref(rep2))
         else:
-            st = cq._lib().cqr_factor_sharded(ctx.h, _abi.RLU, C.c_void_p(an.ctypes.data), m_local, m_global, row0,
+            st = cq._lib().cqr_factor_sharded(ctx.h, method, C.c_void_p(an.ctypes.data), m_local, m_global, row0,
                                               n, n, C.byref(cfg_c), C.byref(opts), C.c_void_p(qn.ctypes.data), n,
                                               cq._ptr(rh), n, C.byref(rep2))
         ctx._check(st, rep2.index)
@@ -224,19 +248,21 @@ def run_ours(args):
     roof = {"kernel": "sketch_ws_kernel (8 Box-Muller warps + 8 DMMA warps) + sketch_reduce (Sketch stage)",
             "bound": "tensor",
             "achieved": achieved, "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"],
-            "peak_src": pk["fp64_src"], "algorithmic": "2*l*m*n flops per launch (l=256, m=1e6, n=128); Omega "
-            "generation (l*m Gaussian draws) is extra work not counted", "traffic": _traffic()}
+            "peak_src": pk["fp64_src"], "algorithmic": f"2*l*m*n flops per launch (l={l}, m={m_local}, n={n}); "
+            "Omega generation (l*m Gaussian draws) is extra work not counted",
+            "traffic": _traffic() if args.workload == "c1" else None}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample(a, l, CPU_SAMPLE_ROWS)
+        cpu = cpu_baseline_sample(a, l, CPU_SAMPLE_ROWS, method, mname)
     stage_avg = {cq_name: float(v / args.steps) for cq_name, v in zip(_abi.STAGE_NAMES, stage_tot)}
     line = {"metric": "rQR/rLU-CholeskyQR fp64 TFLOP/s (ms/factorization in ms_per_step)", "value": value,
             "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: A = U diag(sigma) V^T generated on the device (matgen.cpp restated), sigma log-spaced 1..1e-14",
-            "config": {"workload": WORKLOAD, "method": "rlu", "sketch": "gaussian", "m_per_gpu": m_local,
-                       "m_global": m_global, "n": n, "l": l, "kappa": KAPPA,
-                       "l2": "inputs larger than L2 (1.02 GB per GPU vs 126 MB L2), no flush",
+            "data": "synthetic: A = U diag(sigma) V^T generated on the device (matgen.cpp restated), "
+                    + ("sigma log-spaced 1..1/kappa" if kap != "two-segment" else "c4 two-segment spectrum"),
+            "config": {"workload": wdesc, "method": mname, "sketch": "gaussian", "m_per_gpu": m_local,
+                       "m_global": m_global, "n": n, "l": l, "kappa": kap,
+                       "l2": f"inputs larger than L2 ({8 * m_local * n / 1e9:.2f} GB per GPU vs 126 MB L2), no flush",
                        "parallelism": f"row-block dp{world}"},
             "stage_ms": stage_avg, "clocks": clk.summary(), "gpu_launches": launches,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
@@ -255,7 +281,7 @@ def _traffic():
         return None
 
 
-def cpu_baseline_sample(a_dev, l, rows):
+def cpu_baseline_sample(a_dev, l, rows, method=None, mname="rlu"):
     """Oracle (CPU port of the reference) on the first `rows` rows of the same A."""
     import numpy as np
 
@@ -264,13 +290,13 @@ def cpu_baseline_sample(a_dev, l, rows):
 
     a = np.ascontiguousarray(a_dev[:rows].cpu().numpy())
     cores = os.cpu_count() or 1
-    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, rate=RATE, seed=_seed_value())
+    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, size=l, rate=RATE, seed=_seed_value())
     t0 = time.perf_counter()
-    o.factor(_abi.RLU, a, cfg, _abi.options(), workers=cores)
+    o.factor(_abi.RLU if method is None else method, a, cfg, _abi.options(), workers=cores)
     dt = time.perf_counter() - t0
     fl = flops_rlu(rows, a.shape[1], l)
     return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-            "sample": f"one rLU-CholeskyQR factorization of the first {rows} rows (n={a.shape[1]}, l={l}); "
+            "sample": f"one {mname} factorization of the first {rows} rows (n={a.shape[1]}, l={l}); "
                       f"{dt:.2f} s; sketch serial as in sketch.cpp:94-116, Gram/trisolve on {cores} workers"}
 
 
@@ -296,30 +322,31 @@ def run_reference(args):
     from oracle import oracle as o
     from paper_2111_11148_b200 import _abi
 
+    mname, _, n, l, kap, wdesc = WORKLOADS[args.workload]
+    method = {v: k for k, v in _abi.METHOD_NAMES.items()}[mname]
     rows = CPU_SAMPLE_ROWS
     rs = np.random.default_rng(SEED)
-    u, _ = np.linalg.qr(rs.standard_normal((rows, N)))
-    v, _ = np.linalg.qr(rs.standard_normal((N, N)))
-    sigma = KAPPA ** (-np.arange(N) / (N - 1))
+    u, _ = np.linalg.qr(rs.standard_normal((rows, n)))
+    v, _ = np.linalg.qr(rs.standard_normal((n, n)))
+    sigma = workload_sigma(n, kap)
     a = np.ascontiguousarray(u @ (sigma[:, None] * v.T))
     cores = os.cpu_count() or 1
-    l = int(np.ceil(RATE * N))
-    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, rate=RATE, seed=_seed_value())
+    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, size=l, rate=RATE, seed=_seed_value())
     for _ in range(args.warmup):
-        o.factor(_abi.RLU, a, cfg, _abi.options(), workers=cores)
+        o.factor(method, a, cfg, _abi.options(), workers=cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        o.factor(_abi.RLU, a, cfg, _abi.options(), workers=cores)
+        o.factor(method, a, cfg, _abi.options(), workers=cores)
     dt = (time.perf_counter() - t0) / args.steps
-    value = flops_rlu(rows, N, l) / dt / 1e12
+    value = flops_rlu(rows, n, l) / dt / 1e12
     line = {"impl": "reference", "metric": "rQR/rLU-CholeskyQR fp64 TFLOP/s (ms/factorization in ms_per_step)",
             "value": value, "unit": "TFLOP/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "method": "rlu", "sketch": "gaussian", "n": N, "l": l,
-                       "kappa": KAPPA, "sample_rows": rows},
+            "config": {"workload": wdesc, "method": mname, "sketch": "gaussian", "n": n, "l": l,
+                       "kappa": kap, "sample_rows": rows},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                             "sample": f"rLU-CholeskyQR of a {rows} x {N} sample per step (the reference is "
+                             "sample": f"{mname} of a {rows} x {n} sample per step (the reference is "
                                        "not buildable here: no Eigen); serial Gaussian sketch as the reference"},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -332,6 +359,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--workload", default="c1", choices=sorted(WORKLOADS),
+                    help="BASELINE.json config (c1, the benchmark line, by default)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
