@@ -329,7 +329,7 @@ void trisolve_dev(cqr_ctx* c, const double* in, long long ldi, double* out, long
   t.vec16 = (vec_ok(in, ldi, n) && vec_ok(out, ldo, n)) ? 1 : 0;
   t.num_sms = c->num_sms;
   t.status = c->status;
-  static const int variant = [] {  // CQR_TRISOLVE_VARIANT=1 selects the left-looking kernel (A/B runs)
+  static const int variant = [] {  // CQR_TRISOLVE_VARIANT=1 forces the register kernel (A/B runs)
     const char* v = std::getenv("CQR_TRISOLVE_VARIANT");
     return v ? std::atoi(v) : 0;
   }();

@@ -28,7 +28,7 @@ struct TrisolveArgs {
   int vec16;
   int num_sms;
   const DevStatus* status;
-  int variant = 0;  // 0: TMA kernel when eligible, else the register kernel; 1..7: fixed kernels (tuning)
+  int variant = 0;  // 0: the TMA kernel when eligible, else the register kernel; nonzero: the register kernel
 };
 cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s);
 // trisolve_tma.cu: the TMA-staged kernel (16-byte aligned bases, even leading dimensions, np >= 32)

@@ -1,15 +1,16 @@
-// trisolve.cu — tall right triangular solve X R = A (kernels.hpp:94-127).
+// trisolve.cu — tall right triangular solve X R = A (kernels.hpp:94-127): the
+// packed R, the dispatcher, and the register kernel used when A or X is not
+// TMA-addressable (the default kernel is trisolve_tma.cu).
 //
 // Reference recurrence, per row and column j: y_j = a_j; for k < j:
 // y_j = fma(-r_kj, x_k, y_j) (skipped when r_kj == 0); x_j = y_j / r_jj. A row's
 // result depends only on that row, so any row partition gives the same bits
 // (kernels.hpp:98-101).
 //
-// B200 mapping. Each warp owns a panel of RW = 8*MG rows staged in shared
-// memory; columns go in blocks J of 8:
-//  1. off-diagonal part, k < 8J: DMMA m8n8k4 with A = solved X columns (smem)
-//     and B = -R tiles (smem when they fit). DMMA accumulates as the
-//     sequential fma chain in k order (profiles/r01_fp64_probe.txt), so this is
+// B200 mapping (both kernels). A warp owns 32 rows; columns go in blocks J of 8:
+//  1. off-diagonal part, k < 8J: DMMA m8n8k4 with A = solved X columns and
+//     B = -R fragments (pack_r). DMMA accumulates as the sequential fma chain
+//     in k order (profiles/r01_fp64_probe.txt, r01_dmma_shapes.txt), so this is
 //     the reference's chain bit for bit (zero terms are not skipped: only the
 //     sign of an exact zero can differ);
 //  2. diagonal 8x8 block, one lane per row: the remaining k in [8J, j) as
@@ -100,126 +101,7 @@ __global__ void pack_status_kernel(const int* bad_min, int n, DevStatus* st) {
   if (*bad_min < n) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, *bad_min);
 }
 
-template <int NP, int MG, int WPC, bool BSMEM>
-__global__ void __launch_bounds__(WPC * 32) trisolve_kernel(const double* in, long long ldi, double* out,
-                                                            long long ldo, long long m, int n,
-                                                            const double* __restrict__ bpack,
-                                                            const double* __restrict__ dpack,
-                                                            int vec16,
-                                                            const DevStatus* st) {
-  constexpr int NT = NP / 8;
-  constexpr int RW = 8 * MG;
-  constexpr int LDX = NP + 4;
-  constexpr int NB = NT * (NT - 1) * 32;
-  constexpr int ND = NT * kDiagStride;
-  extern __shared__ __align__(16) double smem[];
-  if (failed(st)) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = lane & 3, gr = lane >> 2;
-  double* sD = smem;
-  const double* sB = bpack;
-  double* sX = smem + ND + (BSMEM ? NB : 0) + warp * RW * LDX;
-  for (int e = threadIdx.x; e < ND; e += WPC * 32) sD[e] = dpack[e];
-  if constexpr (BSMEM) {
-    double* s = smem + ND;
-    for (int e = threadIdx.x; e < NB; e += WPC * 32) s[e] = bpack[e];
-    sB = s;
-  }
-  __syncthreads();
-  const long long groups = (m + RW - 1) / RW;
-  for (long long grp = (long long)blockIdx.x * WPC + warp; grp < groups; grp += (long long)gridDim.x * WPC) {
-    const long long row0 = grp * RW;
-    const int rows = (int)min((long long)RW, m - row0);
-    // stage the panel (zero-padded columns and rows)
-    if (vec16) {
-      for (int r = 0; r < RW; ++r)
-        for (int c2 = lane; c2 < NP / 2; c2 += 32) {
-          double* d = sX + r * LDX + 2 * c2;
-          if (r < rows && 2 * c2 < n)
-            cp_async16(d, in + (row0 + r) * ldi + 2 * c2);
-          else
-            *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);
-        }
-    } else {
-      for (int r = 0; r < RW; ++r)
-        for (int c = lane; c < NP; c += 32) {
-          double* d = sX + r * LDX + c;
-          if (r < rows && c < n)
-            cp_async8(d, in + (row0 + r) * ldi + c);
-          else
-            *d = 0.0;
-        }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-#pragma unroll 1
-    for (int J = 0; J < NT; ++J) {
-      if (J > 0) {
-        double c[MG][2];
-#pragma unroll
-        for (int g = 0; g < MG; ++g) {
-          const double2 v = *reinterpret_cast<const double2*>(sX + (g * 8 + gr) * LDX + 8 * J + 2 * q);
-          c[g][0] = v.x;
-          c[g][1] = v.y;
-        }
-        const double* bj = sB + (long long)J * (J - 1) * 32 + lane;
-        const double* xa = sX + gr * LDX + q;
-#pragma unroll 4
-        for (int k4 = 0; k4 < 2 * J; ++k4) {
-          const double b = BSMEM ? bj[k4 * 32] : __ldg(bj + k4 * 32);
-#pragma unroll
-          for (int g = 0; g < MG; ++g) dmma(c[g][0], c[g][1], xa[g * 8 * LDX + 4 * k4], b);
-        }
-#pragma unroll
-        for (int g = 0; g < MG; ++g)
-          *reinterpret_cast<double2*>(sX + (g * 8 + gr) * LDX + 8 * J + 2 * q) = make_double2(c[g][0], c[g][1]);
-        __syncwarp();
-      }
-      // diagonal block: one lane per row
-      if (lane < RW) {
-        double* xr = sX + lane * LDX + 8 * J;
-        double y[8];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double2 v = *reinterpret_cast<const double2*>(xr + 2 * u);
-          y[2 * u] = v.x;
-          y[2 * u + 1] = v.y;
-        }
-        const double* D = sD + J * kDiagStride;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-#pragma unroll
-          for (int kk = 0; kk < j; ++kk) {
-            const double rr = D[kk * 8 + j];
-            if (rr != 0.0) y[j] = fma(-rr, y[kk], y[j]);
-          }
-          y[j] = fast_div(y[j], D[j * 8 + j], D[64 + j], D[72 + j] != 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(xr + 2 * u) = make_double2(y[2 * u], y[2 * u + 1]);
-      }
-      __syncwarp();
-    }
-    // write the solved panel (coalesced rows)
-    if (vec16) {
-      for (int r = 0; r < rows; ++r)
-        for (int c2 = lane; 2 * c2 < n; c2 += 32) {
-          double2 v = *reinterpret_cast<const double2*>(sX + r * LDX + 2 * c2);
-          *reinterpret_cast<double2*>(out + (row0 + r) * ldo + 2 * c2) = v;
-        }
-    } else {
-      for (int r = 0; r < rows; ++r)
-        for (int c = lane; c < n; c += 32) {
-          double v = sX[r * LDX + c];
-          out[(row0 + r) * ldo + c] = v;
-        }
-    }
-    __syncwarp();
-  }
-}
-
-// Super-block kernel (the default). A warp owns 32 rows (4 DMMA row groups;
+// Register kernel (the fallback when A or X is not TMA-addressable). A warp owns 32 rows (4 DMMA row groups;
 // one lane per row in the scalar part, so all 32 lanes work). Columns go in
 // passes of 64 (8 blocks of 8), the pass held in DMMA accumulator registers:
 //  1. left-looking: contributions of all columns solved in earlier passes,
@@ -458,23 +340,6 @@ cudaError_t launch_trisolve_sb_t(const TrisolveArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int NP, int MG, int WPC, bool BSMEM>
-cudaError_t launch_trisolve_t(const TrisolveArgs& a, cudaStream_t s) {
-  constexpr int NT = NP / 8;
-  const size_t smem =
-      (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * (NP + 4)) * sizeof(double);
-  auto k = trisolve_kernel<NP, MG, WPC, BSMEM>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const long long groups = (a.m + 8 * MG - 1) / (8 * MG);
-  long long grid = (groups + WPC - 1) / WPC;
-  if (grid > a.num_sms) grid = a.num_sms;
-  if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, WPC * 32, smem, s>>>(a.in, a.ldi, a.out, a.ldo, a.m, a.n, a.bpack, a.dpack, a.vec16,
-                                           a.status);
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 int trisolve_np(int n) {
@@ -516,33 +381,9 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   const int nt = np / 8;
   a.bpack = a.pack;
   a.dpack = a.pack + (size_t)nt * (nt - 1) * 32;
-  if ((a.variant == 0 || a.variant >= 8) && trisolve_tma_eligible(a, np)) {
+  if (a.variant == 0 && trisolve_tma_eligible(a, np)) {
     const cudaError_t e = launch_trisolve_tma(a, np, s);
     if (e != cudaErrorNotSupported) return e;
-  }
-  if (a.variant == 2) {  // 32-column passes, 16 warps
-    switch (np) {
-      case 64: return launch_trisolve_sb_t<64, 16, true, 4>(a, s);
-      case 128: return launch_trisolve_sb_t<128, 16, true, 4>(a, s);
-      case 256: return launch_trisolve_sb_t<256, 16, false, 4>(a, s);
-    }
-  }
-  if (a.variant == 3) {  // 64-column passes, 8 warps
-    switch (np) {
-      case 64: return launch_trisolve_sb_t<64, 8, true, 8>(a, s);
-      case 128: return launch_trisolve_sb_t<128, 8, true, 8>(a, s);
-      case 256: return launch_trisolve_sb_t<256, 8, false, 8>(a, s);
-    }
-  }
-  if (a.variant == 1) {  // left-looking (smem panel), kept for comparison
-    switch (np) {
-      case 8: return launch_trisolve_t<8, 2, 16, true>(a, s);
-      case 16: return launch_trisolve_t<16, 2, 16, true>(a, s);
-      case 32: return launch_trisolve_t<32, 2, 16, true>(a, s);
-      case 64: return launch_trisolve_t<64, 2, 16, true>(a, s);
-      case 128: return launch_trisolve_t<128, 2, 8, true>(a, s);
-      case 256: return launch_trisolve_t<256, 2, 5, false>(a, s);
-    }
   }
   // register kernel (best measured configuration per width)
   switch (np) {

@@ -321,18 +321,6 @@ bool trisolve_tma_eligible(const TrisolveArgs& a, int np) {
 }
 
 cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s) {
-  if (a.variant == 8) {  // tuning: 16 warps, R tiles through L1
-    switch (np) {
-      case 64: return launch_t<64, 16, false>(a, s);
-      case 128: return launch_t<128, 16, false>(a, s);
-    }
-  }
-  if (a.variant == 9) {  // tuning: 12 warps, R tiles through L1
-    switch (np) {
-      case 64: return launch_t<64, 12, false>(a, s);
-      case 128: return launch_t<128, 12, false>(a, s);
-    }
-  }
   switch (np) {
     case 32: return launch_t<32, 16, true>(a, s);
     case 64: return launch_t<64, 12, true>(a, s);
