@@ -217,6 +217,10 @@ int cqr_sample_rows_uniform(cqr_ctx* ctx, const double* a, int64_t m, int64_t n,
 /* rng::gaussian_matrix / bits_at on the device (rng.hpp:29-92), for checks. */
 int cqr_rng_bits(cqr_ctx* ctx, uint64_t seed, uint64_t k0, int64_t count, uint64_t* out);
 int cqr_rng_gaussian(cqr_ctx* ctx, uint64_t seed, uint64_t k0, int64_t count, double* out);
+/* The Box-Muller step of rng.hpp:47-55 on given counter bits (host arrays):
+ * bits[2i] -> u1 = ((bits[2i] >> 11) + 1) 2^-53, bits[2i+1] -> u2 = (bits[2i+1] >> 11) 2^-53;
+ * out[2i] = sqrt(-2 ln u1) cos(2 pi u2), out[2i+1] = ... sin(2 pi u2). For edge-case checks. */
+int cqr_box_muller_bits(cqr_ctx* ctx, const uint64_t* bits, int64_t pairs, double* out);
 
 /* ---- diagnostics on the device (diagnostics.cpp:10-28) ------------------ */
 int cqr_orthogonality_error_dev(cqr_ctx* ctx, const double* q, int64_t m, int64_t n, int64_t ldq,

@@ -205,6 +205,7 @@ def _lib():
             "cqr_sample_rows_uniform": (i32, [vp, vp, i64, i64, i64, i64, u64, i32, vp, vp]),
             "cqr_rng_bits": (i32, [vp, u64, u64, i64, vp]),
             "cqr_rng_gaussian": (i32, [vp, u64, u64, i64, vp]),
+            "cqr_box_muller_bits": (i32, [vp, vp, i64, vp]),
             "cqr_orthogonality_error_dev": (i32, [vp, vp, i64, i64, i64, pd]),
             "cqr_residual_error_dev": (i32, [vp, vp, i64, vp, i64, vp, i64, i64, pd]),
             "cqr_synthesize_dev": (i32, [vp, i64, i64, i64, i64, vp, u64, vp, i64]),
@@ -637,6 +638,17 @@ def rng_gaussian(seed, k0, count, ctx=None):
     ctx = ctx or context()
     out = np.empty(count)
     ctx._check(_lib().cqr_rng_gaussian(ctx.h, seed & (2**64 - 1), k0, count, _ptr(out)))
+    return out
+
+
+def box_muller_bits(bits, ctx=None):
+    """Box-Muller step (rng.hpp:47-55) of the device draws on given counter bits:
+    bits[2i] -> u1, bits[2i+1] -> u2; returns [r cos a, r sin a] per pair."""
+    ctx = ctx or context()
+    bits = np.ascontiguousarray(bits, dtype=np.uint64)
+    assert bits.size % 2 == 0
+    out = np.empty(bits.size)
+    ctx._check(_lib().cqr_box_muller_bits(ctx.h, _ptr(bits), bits.size // 2, _ptr(out)))
     return out
 
 

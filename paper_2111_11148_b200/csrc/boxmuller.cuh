@@ -4,16 +4,24 @@
 // CUDA's log/sqrt/sincos carry special-case branches, which split basic
 // blocks and keep the scheduler from interleaving the draws with the DMMA
 // stream. These versions are straight-line for the arguments that occur
-// (u1 in (0,1], a in [0, 2*pi)) and accurate to a few ulp in absolute terms
-// (1e7 draws against glibc: max 12.5 ulp of max(|g|, 1) -- the absolute error of
-// cos/sin near their zeros times r <= 8.6 -- and 70.7% bit-identical):
-//  * log: u1 = 2^e f, f renormalised to [sqrt(2)/2, sqrt(2)), 128-entry table
-//    of inv_i = RN(1/c_i) and -log(inv_i) (hi+lo, built in long double), r =
-//    f*inv_i - 1 (one fma), log1p(r) by a degree-7 polynomial (|r| < 2^-7.9);
+// (u1 in (0,1], a in [0, 2*pi)) and stay within 3 ulp of max(|g|, 1) of the
+// oracle (tools/gpu/bm_acc.py, 1e7 draws; tests/test_gpu_parity.py also drives
+// the edge bits: u1 -> 1, u1 -> 0, quadrant and table boundaries of u2):
+//  * log: u1 = 2^e f, f renormalised to [sqrt(2)/2, sqrt(2)), table points
+//    c_i = 1 + i/256 (i = -75..106, rounded from the mantissa bits) with
+//    inv_i = RN(1/c_i) and -log(inv_i) (hi+lo, long double), r = f*inv_i - 1
+//    (one fma, |r| < 2^-8.5), log1p(r) by a degree-6 polynomial. c_0 = 1
+//    exactly, so for u1 -> 1 the result is log1p(f - 1) with f - 1 exact: full
+//    relative accuracy of ln u1 (and of r = sqrt(-2 ln u1)) down to u1 = 1 - 2^-53;
 //  * sqrt: rsqrt.approx + one Newton step + one residual correction;
-//  * sincos: 64-entry table of sin/cos(2*pi*i/64), 3-part Cody-Waite
-//    reduction, degree-9/8 polynomials on |d| <= pi/64.
-// Tables live in shared memory (BmTables, ~4 KB), filled from __constant__.
+//  * sincos: sin/cos(2*pi*k/256) from a one-quadrant table (65 entries, quadrant
+//    rotation by sign/swap on the integer pipe), k = round(256 u2) from the integer
+//    counter bits, 3-part Cody-Waite reduction, degree-5/6 polynomials on |d| <= pi/256.
+// The FP64 pipe is shared with the sketch's DMMA stream, which holds it whenever it
+// has work (tools/probe/pipe_prio.cu): the draws' FP64 instructions mostly run in
+// its gaps, so exact power-of-two scalings and the table indices go through the
+// integer pipe, and P pairs are drawn side by side for instruction-level parallelism.
+// Tables live in shared memory (BmTables, 4.9 KB), filled from __constant__.
 #pragma once
 
 #include <cstdint>
@@ -22,13 +30,26 @@
 
 namespace cqr {
 
+constexpr int kBmLogLo = -75, kBmLogHi = 106;  // log table points c_i = 1 + i/256
+constexpr int kBmLog = kBmLogHi - kBmLogLo + 1;
+constexpr int kBmTrig = 256;  // table points 2 pi k / 256 over [0, 2 pi)
 struct BmTables {
-  double inv[128];
-  double lhi[128];
-  double llo[128];
-  double s[66];
-  double c[66];
+  double inv[kBmLog];
+  double lhi[kBmLog];
+  double llo[kBmLog];
+  double q[kBmTrig / 4 + 1];  // sin(2 pi m / 256), m = 0..64 (one quadrant; the others by symmetry)
 };
+
+// sin and cos of 2 pi k / 256: k = 64 q + m, rotate the first-quadrant pair by q quarter turns
+__device__ __forceinline__ void bm_table_sincos(const BmTables& T, int k, double& S, double& C) {
+  const int q = k >> 6, m = k & 63;
+  const double s0 = T.q[m], c0 = T.q[64 - m];
+  const bool swap = q & 1;
+  const long long sb = __double_as_longlong(swap ? c0 : s0), cb = __double_as_longlong(swap ? s0 : c0);
+  const long long sneg = (long long)(q >> 1) << 63, cneg = (long long)((q ^ (q >> 1)) & 1) << 63;
+  S = __longlong_as_double(sb ^ sneg);
+  C = __longlong_as_double(cb ^ cneg);
+}
 
 __device__ __forceinline__ double rsqrt_approx(double x) {
   double y;
@@ -36,67 +57,111 @@ __device__ __forceinline__ double rsqrt_approx(double x) {
   return y;
 }
 
-// Both outputs of Box-Muller pair p (counters 2p -> cos, 2p+1 -> sin).
+#define CQR_BM_EACH _Pragma("unroll") for (int j = 0; j < P; ++j)
+
+// Box-Muller on raw counter bits: b1 -> u1 = ((b1 >> 11) + 1) 2^-53, b2 -> u2 =
+// (b2 >> 11) 2^-53; g_even = r cos(a), g_odd = r sin(a). The pairs are independent;
+// every step is issued for all P of them before the next one (P-way ILP).
+template <int P>
+__device__ __forceinline__ void box_muller_bits(const BmTables& T, const uint64_t (&b1)[P], const uint64_t (&b2)[P],
+                                                double (&g_even)[P], double (&g_odd)[P]) {
+  double n1[P], a[P], fk[P];
+  int k[P];
+  CQR_BM_EACH {
+    // u1 = N1 * 2^-53 with N1 = (b1 >> 11) + 1 in [1, 2^53]: the scaling is folded into the
+    // exponent below (N1's double has u1's mantissa bits, its exponent is 53 higher)
+    n1[j] = (double)((b1[j] >> 11) + 1);
+    // a = RN(2 pi) * u2 with u2 = N2 * 2^-53: the power-of-two scaling commutes with the
+    // rounding (a is 0 or >= 2^-51), so one multiply by RN(2 pi) * 2^-53 gives the same a
+    const uint64_t n2 = b2[j] >> 11;
+    a[j] = (double)n2 * 0x1.921fb54442d18p-51;
+    // table point k = round(256 u2) in [0, 256] (k = 256 reduces with 2 pi and reads entry 0)
+    const int kk = (int)((n2 + (1ull << 44)) >> 45);
+    k[j] = kk & (kBmTrig - 1);
+    fk[j] = (double)kk;
+  }
+  // ---- log(u1) = e ln 2 - log(inv_i) + log1p(f inv_i - 1)
+  int e[P], ti[P];
+  double r[P], r2[P], pl[P];
+  CQR_BM_EACH {
+    const int hi = __double2hiint(n1[j]), lo = __double2loint(n1[j]);
+    const int mh = hi & 0xFFFFF;  // top 20 of the 52 mantissa bits m of f0 = 1 + m 2^-52
+    const bool up = mh >= (213 << 11);  // f0 >= 1 + 106.5/256: use f = f0/2, e + 1
+    // i = round((f - 1) * 256): round(m / 2^44) below, round(m / 2^45) - 128 above
+    const int i = up ? ((mh + (1 << 12)) >> 13) - 128 : (mh + (1 << 11)) >> 12;
+    ti[j] = i - kBmLogLo;
+    e[j] = (hi >> 20) - 1023 - 53 + (up ? 1 : 0);
+    const double f = __hiloint2double(mh | (up ? 0x3FE00000 : 0x3FF00000), lo);  // [0.708, 1.416)
+    r[j] = fma(f, T.inv[ti[j]], -1.0);
+  }
+  CQR_BM_EACH r2[j] = r[j] * r[j];
+  CQR_BM_EACH pl[j] = fma(-1.0 / 6.0, r[j], 1.0 / 5.0);
+  CQR_BM_EACH pl[j] = fma(pl[j], r[j], -1.0 / 4.0);
+  CQR_BM_EACH pl[j] = fma(pl[j], r[j], 1.0 / 3.0);
+  CQR_BM_EACH pl[j] = fma(pl[j], r[j], -0.5);
+  double L[P];
+  CQR_BM_EACH {
+    const double l1p = fma(r2[j], pl[j], r[j]);
+    const double ed = (double)e[j];
+    const double ln2_hi = 0x1.62e42fefa3800p-1, ln2_lo = 0x1.ef35793c76730p-45;
+    L[j] = fma(ed, ln2_hi, T.lhi[ti[j]]) + (fma(ed, ln2_lo, T.llo[ti[j]]) + l1p);
+  }
+  // ---- sincos(a): d = a - k * 2 pi / 256 (three parts; k * part 1 and k * part 2 are exact)
+  double d[P];
+  CQR_BM_EACH {
+    d[j] = fma(-fk[j], 0x1.921fb54400000p-6, a[j]);
+    d[j] = fma(-fk[j], 0x1.0b4611a600000p-40, d[j]);
+    d[j] = fma(-fk[j], 0x1.3198a2e037073p-75, d[j]);
+  }
+  // ---- sqrt(-2 L): L is 0 or a normal number (|L| >= 2^-54), so x = -2 L is a sign flip
+  // plus one on the exponent, and -x/2 is L itself
+  double x[P], y[P];
+  CQR_BM_EACH {
+    const long long Lb = __double_as_longlong(L[j]);
+    x[j] = (Lb << 1) == 0 ? 0.0 : __longlong_as_double((Lb ^ (1ll << 63)) + (1ll << 52));
+    y[j] = rsqrt_approx(x[j]);
+  }
+  double d2[P], sp[P], cp[P];
+  CQR_BM_EACH d2[j] = d[j] * d[j];
+  CQR_BM_EACH y[j] = y[j] * fma(L[j], y[j] * y[j], 1.5);  // one Newton step (a second one changed no draw in 1e7)
+  // sin d = d + d^3 (-1/6 + d^2/120) (next term <= 8.6e-18); cos d to d^6 (next term <= 1.3e-20)
+  CQR_BM_EACH sp[j] = fma(d2[j], 1.0 / 120.0, -1.0 / 6.0);
+  CQR_BM_EACH cp[j] = fma(d2[j], -1.0 / 720.0, 1.0 / 24.0);
+  CQR_BM_EACH cp[j] = fma(cp[j], d2[j], -0.5);
+  CQR_BM_EACH {
+    double s = x[j] * y[j];
+    const double hy = __longlong_as_double(__double_as_longlong(y[j]) - (1ll << 52));  // y / 2, y normal
+    s = fma(hy, fma(-s, s, x[j]), s);
+    const double rad = __double_as_longlong(x[j]) > 0 ? s : 0.0;
+    const double sn = fma(d[j] * d2[j], sp[j], d[j]);
+    const double cs = fma(cp[j], d2[j], 1.0);
+    double S, C;
+    bm_table_sincos(T, k[j], S, C);
+    g_even[j] = rad * fma(C, cs, -(S * sn));
+    g_odd[j] = rad * fma(S, cs, C * sn);
+  }
+}
+
+// Both outputs of Box-Muller pairs p[0..P) (counters 2p -> cos, 2p+1 -> sin; rng.hpp:47-55).
+template <int P>
+__device__ __forceinline__ void gaussian_pairs_fast(const BmTables& T, uint64_t seed, const uint64_t (&p)[P],
+                                                    double (&g_even)[P], double (&g_odd)[P]) {
+  uint64_t b1[P], b2[P];
+  CQR_BM_EACH {
+    b1[j] = mix64(seed + (2 * p[j] + 1) * 0x9E3779B97F4A7C15ull);
+    b2[j] = mix64(seed + (2 * p[j] + 2) * 0x9E3779B97F4A7C15ull);
+  }
+  box_muller_bits<P>(T, b1, b2, g_even, g_odd);
+}
+#undef CQR_BM_EACH
+
 __device__ __forceinline__ void gaussian_pair_fast(const BmTables& T, uint64_t seed, uint64_t p, double& g_even,
                                                    double& g_odd) {
-  const uint64_t b1 = mix64(seed + (2 * p + 1) * 0x9E3779B97F4A7C15ull);
-  const uint64_t b2 = mix64(seed + (2 * p + 2) * 0x9E3779B97F4A7C15ull);
-  // u1 = N1 * 2^-53 with N1 = (b1 >> 11) + 1 in [1, 2^53]: the scaling is folded into the
-  // exponent below (N1's double has u1's mantissa bits, its exponent is 53 higher)
-  const double n1 = (double)((b1 >> 11) + 1);
-  const double u2 = (double)(b2 >> 11) * 0x1.0p-53;
-  // ---- log(u1)
-  const int hi = __double2hiint(n1), lo = __double2loint(n1);
-  int e = (hi >> 20) - 1023 - 53;
-  const int mh = hi & 0xFFFFF;
-  const int i = mh >> 13;
-  double f = __hiloint2double(mh | 0x3FF00000, lo);
-  const bool up = i >= 53;
-  f = up ? f * 0.5 : f;
-  e += up ? 1 : 0;
-  const double r = fma(f, T.inv[i], -1.0);
-  const double r2 = r * r;
-  double pl = 1.0 / 7.0;
-  pl = fma(pl, r, -1.0 / 6.0);
-  pl = fma(pl, r, 1.0 / 5.0);
-  pl = fma(pl, r, -1.0 / 4.0);
-  pl = fma(pl, r, 1.0 / 3.0);
-  pl = fma(pl, r, -0.5);
-  const double l1p = fma(r2, pl, r);
-  const double ed = (double)e;
-  const double ln2_hi = 0x1.62e42fefa3800p-1, ln2_lo = 0x1.ef35793c76730p-45;
-  const double L = fma(ed, ln2_hi, T.lhi[i]) + (fma(ed, ln2_lo, T.llo[i]) + l1p);
-  // ---- sqrt(-2 L)
-  const double x = -2.0 * L;
-  double y = rsqrt_approx(x);
-  y = y * fma(-0.5 * x, y * y, 1.5);  // one Newton step: a second one changed no draw in 1e7 (tools/gpu/bm_acc.py)
-  double s = x * y;
-  s = fma(0.5 * y, fma(-s, s, x), s);
-  const double rad = (x > 0.0) ? s : 0.0;
-  // ---- sincos(a), a = RN(2 pi) * u2
-  const double a = 6.283185307179586 * u2;
-  const double t = fma(a, 10.185916357881302, 0x1.8p52);  // a * 64/(2 pi) + rounding constant
-  const int k = __double2loint(t) & 127;
-  const double fk = t - 0x1.8p52;
-  double d = fma(-fk, 0x1.921fb54400000p-4, a);  // 2 pi / 64, three parts
-  d = fma(-fk, 0x1.0b4611a600000p-38, d);
-  d = fma(-fk, 0x1.3198a2e037073p-73, d);
-  const double d2 = d * d;
-  double sp = 1.0 / 362880.0;
-  sp = fma(sp, d2, -1.0 / 5040.0);
-  sp = fma(sp, d2, 1.0 / 120.0);
-  sp = fma(sp, d2, -1.0 / 6.0);
-  const double sn = fma(sp * d2, d, d);
-  double cp = 1.0 / 40320.0;
-  cp = fma(cp, d2, -1.0 / 720.0);
-  cp = fma(cp, d2, 1.0 / 24.0);
-  cp = fma(cp, d2, -0.5);
-  const double cs = fma(cp, d2, 1.0);
-  const double S = T.s[k], C = T.c[k];
-  const double ca = fma(C, cs, -(S * sn));
-  const double sa = fma(S, cs, C * sn);
-  g_even = rad * ca;
-  g_odd = rad * sa;
+  const uint64_t pp[1] = {p};
+  double ge[1], go[1];
+  gaussian_pairs_fast<1>(T, seed, pp, ge, go);
+  g_even = ge[0];
+  g_odd = go[0];
 }
 
 // Host: fill the tables (long double arithmetic) and upload to the device copy.

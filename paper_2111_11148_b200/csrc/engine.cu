@@ -1225,6 +1225,20 @@ int cqr_rng_gaussian(cqr_ctx* c, uint64_t seed, uint64_t k0, int64_t count, doub
   });
 }
 
+int cqr_box_muller_bits(cqr_ctx* c, const uint64_t* bits, int64_t pairs, double* out) {
+  if (!c || pairs < 0 || (pairs > 0 && (!bits || !out))) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const size_t cnt = (size_t)std::max<int64_t>(2 * pairs, 1);
+    uint64_t* db = dbuf<uint64_t>(c, B_SYN, cnt);
+    double* d = dbuf<double>(c, B_X, cnt);
+    ck(cudaMemcpyAsync(db, bits, sizeof(uint64_t) * 2 * pairs, cudaMemcpyHostToDevice, c->stream), "H2D");
+    LAUNCH(c, cqr::launch_box_muller_bits(db, pairs, d, c->stream));
+    ck(cudaMemcpyAsync(out, d, sizeof(double) * 2 * pairs, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
 int cqr_orthogonality_error_dev(cqr_ctx* c, const double* q, int64_t m, int64_t n, int64_t ldq, double* out) {
   if (!c || m < n || n < 1 || n > 512) return CQR_INVALID_ARGUMENT;
   return guarded(c, [&] {

@@ -88,6 +88,7 @@ cudaError_t launch_gather_rows(const double* a, long long lda, long long m_local
                                double* a1, long long* idx_out, const DevStatus* st, cudaStream_t s);
 cudaError_t launch_rng_bits(uint64_t seed, uint64_t k0, long long count, uint64_t* out, cudaStream_t s);
 cudaError_t launch_rng_gaussian(uint64_t seed, uint64_t k0, long long count, double* out, cudaStream_t s);
+cudaError_t launch_box_muller_bits(const uint64_t* bits, long long pairs, double* out, cudaStream_t s);
 
 // ---- small.cu (single-CTA factorizations, all on device) ------------------------------
 // kernels.hpp:76-90 (+ G += shift*I, engine.cpp:85; theory shift from trace(G)).

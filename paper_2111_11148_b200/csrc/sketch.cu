@@ -192,30 +192,45 @@ __global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const double* __res
 // columns, one box per MMA warp), and 8 MMA warps consume the stages behind
 // full/empty mbarriers. Per-element arithmetic and k order are those of
 // sketch_kernel<128, true>: the partials are bit-identical.
+// The DMMA stream holds the FP64 pipe whenever it has work (tools/probe/pipe_prio.cu:
+// a DFMA chain next to 8 DMMA warps advances only when they stall), so the draws'
+// FP64 instructions run in its gaps and in the windows where the ring runs dry
+// (per-warp timeline: -DCQR_WS_TRACE + tools/gpu/ws_trace.py). Each generator
+// thread draws its ILP pairs side by side (box_muller_bits<P>): 2.66 -> 2.55 ms at
+// c1; constant draws (-DCQR_WS_FAKEGEN) bound the kernel at 1.89 ms.
 #ifndef CQR_WS_STAGES
 #define CQR_WS_STAGES 3
 #endif
 #ifndef CQR_WS_GEN
 #define CQR_WS_GEN 8
 #endif
-#ifndef CQR_WS_UNROLL
-#define CQR_WS_UNROLL 4
-#endif
 constexpr int kWsStages = CQR_WS_STAGES;
 constexpr int kWsGen = CQR_WS_GEN;
-constexpr int kWsUnroll = CQR_WS_UNROLL;
-constexpr int kWsMma = 8;
+#ifndef CQR_WS_ILP
+#define CQR_WS_ILP 4
+#endif
+constexpr int kWsIlp = CQR_WS_ILP;
+#ifndef CQR_WS_MMA
+#define CQR_WS_MMA 8
+#endif
+constexpr int kWsMma = CQR_WS_MMA;
 constexpr int kWsThreads = (kWsGen + kWsMma) * 32;
 
 // NPC columns of A per CTA (128, or 256 for wider A with 32 Omega rows per CTA so
 // that each drawn Omega entry feeds twice the DMMA work), ST Omega rows per CTA.
+#ifdef CQR_WS_TRACE  // probe: per-warp step timeline of CTA 0 (read with cqr_debug_trace)
+constexpr int kTraceSteps = 64;
+__device__ long long g_trace[16 * kTraceSteps * 2];
+#endif
+
 template <int NPC, int ST>
 struct WsShape {
   static constexpr int ATILE = kKS * NPC;       // doubles per A stage (NPC/16 boxes of 32 x 16)
   static constexpr int OTILE = ST * (kKS + 4);  // doubles per Omega stage (stride 36)
-  static constexpr int NGW = NPC / 64;          // 8-column groups per MMA warp
+  static constexpr int NGW = NPC / (8 * kWsMma);  // 8-column groups per MMA warp
   static constexpr int MGW = ST / 8;            // 8-row groups per MMA warp
   static constexpr int PAIRS = ST * kKS / 2 / (kWsGen * 32);  // Box-Muller pairs per generator thread per step
+  static constexpr int ILP = PAIRS < kWsIlp ? PAIRS : kWsIlp;  // pairs drawn side by side
   static constexpr size_t SMEM = (size_t)kWsStages * (ATILE + OTILE) * sizeof(double) + 1024;
 };
 
@@ -260,6 +275,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int stp = 0; stp < nsteps; ++stp) {
       const int s = stp % kWsStages;
       mbar_wait(&empty[s], ((stp / kWsStages) & 1) ^ 1);
+#ifdef CQR_WS_TRACE
+      if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && stp < kTraceSteps) g_trace[(warp * kTraceSteps + stp) * 2] = clock64();
+#endif
       const long long kb = k_begin + (long long)stp * kKS;
       if (gt == 0) {
         mbar_expect_tx(&full[s], S::ATILE * 8);
@@ -269,15 +287,32 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       }
       double* Om = sO + s * S::OTILE;
 #pragma unroll
-      for (int u = 0; u < S::PAIRS; ++u) {
-        const int e = gt + kWsGen * 32 * u;
-        const int i = e >> 4, pp = e & 15;
-        const unsigned long long c_lo = (unsigned long long)(s0 + i) * (unsigned long long)m_global + row0 + kb;
-        double ge, go;
-        gaussian_pair_fast(T, seed, (c_lo >> 1) + pp, ge, go);
-        const bool live = s0 + i < l;
-        *reinterpret_cast<double2*>(Om + i * LDO + 2 * pp) = make_double2(live ? ge : 0.0, live ? go : 0.0);
+      for (int u0 = 0; u0 < S::PAIRS; u0 += S::ILP) {
+        uint64_t pc[S::ILP];
+        double ge[S::ILP], go[S::ILP];
+#pragma unroll
+        for (int j = 0; j < S::ILP; ++j) {
+          const int e = gt + kWsGen * 32 * (u0 + j);
+          const unsigned long long c_lo = (unsigned long long)(s0 + (e >> 4)) * (unsigned long long)m_global + row0 + kb;
+          pc[j] = (c_lo >> 1) + (e & 15);
+        }
+#ifdef CQR_WS_FAKEGEN  // probe: constant draws (the MMA-side bound of this kernel)
+#pragma unroll
+        for (int j = 0; j < S::ILP; ++j) ge[j] = (double)(pc[j] & 255) * 0x1.0p-8, go[j] = 0.5;
+#else
+        gaussian_pairs_fast<S::ILP>(T, seed, pc, ge, go);
+#endif
+#pragma unroll
+        for (int j = 0; j < S::ILP; ++j) {
+          const int e = gt + kWsGen * 32 * (u0 + j);
+          const int i = e >> 4, pp = e & 15;
+          const bool live = s0 + i < l;
+          *reinterpret_cast<double2*>(Om + i * LDO + 2 * pp) = make_double2(live ? ge[j] : 0.0, live ? go[j] : 0.0);
+        }
       }
+#ifdef CQR_WS_TRACE
+      if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && stp < kTraceSteps) g_trace[(warp * kTraceSteps + stp) * 2 + 1] = clock64();
+#endif
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
     }
     return;
@@ -293,6 +328,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   for (int stp = 0; stp < nsteps; ++stp) {
     const int s = stp % kWsStages;
     mbar_wait(&full[s], (stp / kWsStages) & 1);
+#ifdef CQR_WS_TRACE
+    if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && stp < kTraceSteps) g_trace[(warp * kTraceSteps + stp) * 2] = clock64();
+#endif
     const double* Om = sO + s * S::OTILE + gr * LDO + q;
     const double* As = sA + s * S::ATILE;
 #pragma unroll
@@ -313,6 +351,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         for (int h = 0; h < S::NGW; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
     }
     __syncwarp();
+#ifdef CQR_WS_TRACE
+    if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && stp < kTraceSteps) g_trace[(warp * kTraceSteps + stp) * 2 + 1] = clock64();
+#endif
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
   }
   if (check && __any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
@@ -445,22 +486,23 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
 
 }  // namespace
 
+#ifdef CQR_WS_TRACE
+extern "C" int cqr_debug_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
+}
+#endif
+
 void bm_tables_host(BmTables* t) {
-  for (int i = 0; i < 128; ++i) {
-    long double c = 1.0L + ((long double)i + 0.5L) / 128.0L;
-    if (i >= 53) c *= 0.5L;
+  for (int i = 0; i < kBmLog; ++i) {
+    const long double c = 1.0L + (long double)(i + kBmLogLo) / 256.0L;  // exact; c = 1 at i = -kBmLogLo
     const double inv = (double)(1.0L / c);
-    const long double v = -logl((long double)inv);
+    const long double v = 0.0L - logl((long double)inv);  // +0 for inv = 1
     t->inv[i] = inv;
     t->lhi[i] = (double)v;
     t->llo[i] = (double)(v - (long double)t->lhi[i]);
   }
   const long double two_pi = 6.283185307179586476925286766559005768L;
-  for (int k = 0; k < 66; ++k) {
-    const long double ang = two_pi * (long double)k / 64.0L;
-    t->s[k] = (double)sinl(ang);
-    t->c[k] = (double)cosl(ang);
-  }
+  for (int m = 0; m <= kBmTrig / 4; ++m) t->q[m] = (double)sinl(two_pi * (long double)m / kBmTrig);
 }
 
 bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long row0, int n) {
@@ -544,6 +586,33 @@ cudaError_t launch_gather_rows(const double* a, long long lda, long long m_local
 
 cudaError_t launch_rng_bits(uint64_t seed, uint64_t k0, long long count, uint64_t* out, cudaStream_t s) {
   rng_bits_kernel<<<256, 256, 0, s>>>(seed, k0, count, out);
+  return cudaGetLastError();
+}
+
+// Box-Muller on given counter bits (bits[2i] -> u1, bits[2i+1] -> u2): out[2i] = r cos a,
+// out[2i+1] = r sin a. Drives the edge cases (u1 -> 1, table and quadrant boundaries) in tests.
+__global__ void box_muller_bits_kernel(const uint64_t* __restrict__ bits, long long pairs, double* __restrict__ out) {
+  __shared__ BmTables T;
+  {
+    const double* src = reinterpret_cast<const double*>(&c_bm);
+    double* dst = reinterpret_cast<double*>(&T);
+    for (int e = threadIdx.x; e < (int)(sizeof(BmTables) / sizeof(double)); e += blockDim.x) dst[e] = src[e];
+  }
+  __syncthreads();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < pairs;
+       e += (long long)gridDim.x * blockDim.x) {
+    const uint64_t b1[1] = {bits[2 * e]}, b2[1] = {bits[2 * e + 1]};
+    double ge[1], go[1];
+    box_muller_bits<1>(T, b1, b2, ge, go);
+    out[2 * e] = ge[0];
+    out[2 * e + 1] = go[0];
+  }
+}
+
+cudaError_t launch_box_muller_bits(const uint64_t* bits, long long pairs, double* out, cudaStream_t s) {
+  cudaError_t e = ensure_tables();
+  if (e != cudaSuccess) return e;
+  box_muller_bits_kernel<<<148, 256, 0, s>>>(bits, pairs, out);
   return cudaGetLastError();
 }
 

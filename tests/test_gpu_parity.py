@@ -68,6 +68,55 @@ def test_rng_gaussian_within_ulps():
         assert np.mean(gd == go) > 0.5  # most draws are bit-identical
 
 
+def _box_muller_edge_bits():
+    """Counter bits that put u1 and u2 on the edges of the draw's table reduction."""
+    rng = np.random.default_rng(5)
+    n1 = [2**53 - j for j in range(256)] + list(range(1, 257))
+    for k in range(1, 54):  # exponent boundaries of u1
+        n1 += [2**k - 1, 2**k, min(2**k + 1, 2**53)]
+    for e in (0, 1, 5, 30, 52):  # table rounding points and the sqrt(2) split, mantissa-relative
+        base = 2**e
+        for t in list(range(0, 257, 7)) + [212, 213, 214]:
+            c = base + (t * base) // 512
+            n1 += [max(1, c - 1), c, c + 1]
+    n1 += [int(v) for v in rng.integers(1, 2**53, 4000, dtype=np.int64)]
+    n2 = [0, 1, 2, 2**53 - 1, 2**53 - 2]
+    for k in range(0, 257):  # table points of a, incl. the quadrant boundaries
+        c = k * 2**45
+        n2 += [v for v in (c - 2**44, c - 1, c, c + 1, c + 2**44 - 1) if 0 <= v < 2**53]
+    n2 = np.array(n2 + [int(v) for v in rng.integers(0, 2**53, 4000 - len(n2) % 4000, dtype=np.int64)], dtype=np.uint64)
+    n1 = np.array([min(max(v, 1), 2**53) for v in n1], dtype=np.uint64)
+    npairs = max(len(n1), len(n2))
+    n1 = np.resize(n1, npairs)
+    n2 = np.resize(rng.permutation(n2), npairs)
+    low = rng.integers(0, 2**11, (2, npairs), dtype=np.uint64)
+    bits = np.empty(2 * npairs, dtype=np.uint64)
+    bits[0::2] = ((n1 - np.uint64(1)) << np.uint64(11)) | low[0]
+    bits[1::2] = (n2 << np.uint64(11)) | low[1]
+    return bits
+
+
+def test_box_muller_edge_bits():
+    import math
+    bits = _box_muller_edge_bits()
+    got = G.box_muller_bits(bits)
+    worst_abs = worst_rad = 0.0
+    for i in range(bits.size // 2):
+        u1 = float((int(bits[2 * i]) >> 11) + 1) * 2.0**-53
+        u2 = float(int(bits[2 * i + 1]) >> 11) * 2.0**-53
+        r = math.sqrt(-2.0 * math.log(u1))
+        a = 2.0 * math.pi * u2
+        ref = (r * math.cos(a), r * math.sin(a))  # rng.hpp:52-54 with glibc, as the oracle
+        for g, gr in zip(got[2 * i:2 * i + 2], ref):
+            worst_abs = max(worst_abs, abs(g - gr) / (U * max(abs(gr), 1.0)))
+        if r > 0:  # the radius keeps full relative accuracy, also for u1 -> 1 (tiny r)
+            worst_rad = max(worst_rad, abs(math.hypot(*got[2 * i:2 * i + 2]) - r) / (U * r))
+        else:
+            assert got[2 * i] == 0.0 and got[2 * i + 1] == 0.0
+    assert worst_abs <= 16, worst_abs
+    assert worst_rad <= 8, worst_rad
+
+
 # ---------------- kernels -------------------------------------------------------------
 @pytest.mark.parametrize("m,n,seed", [(3, 3, 0), (50, 10, 7), (2500, 6, 11), (3000, 12, 2), (5000, 64, 3),
                                       (4113, 128, 4), (2048, 1, 5), (20000, 33, 6), (9000, 200, 7),

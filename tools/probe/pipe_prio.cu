@@ -1,0 +1,76 @@
+// Does a DMMA stream starve DFMA chains of other warps on the same SM sub-partition?
+// One CTA per SM: MMA warps (16 independent DMMA chains each) run a fixed number of steps;
+// side warps run `chain` independent DFMA chains of fixed length. Each warp records its own
+// elapsed clocks; we print how long the side warps took alone vs next to the MMA stream.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipe_prio pipe_prio.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int CH>
+__global__ void __launch_bounds__(512, 1) k(double* out, long long* cyc, int mma_warps, int steps, int len) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t0 = clock64();
+  if (warp < mma_warps) {
+    double acc[16][2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = threadIdx.x + i;
+    const double a = 1.0 + threadIdx.x * 1e-9, b = 1e-3;
+    for (int s = 0; s < steps; ++s) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dmma(acc[i][0], acc[i][1], a, b);
+    }
+    double t = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t += acc[i][0] + acc[i][1];
+    if (t == 1234.5) out[0] = t;
+  } else if (warp >= 8) {
+    double x[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = 1.0 + threadIdx.x * 1e-7 + i * 1e-3;
+    for (int it = 0; it < len; ++it) {
+#pragma unroll
+      for (int i = 0; i < CH; ++i) x[i] = fma(x[i], 0.999999, 1e-7);
+    }
+    double t = 0;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) t += x[i];
+    if (t == 1234.5) out[0] = t;
+  }
+  const long long t1 = clock64();
+  if (lane == 0 && blockIdx.x == 0) cyc[warp] = t1 - t0;
+}
+
+int main() {
+  double* out;
+  long long* cyc;
+  cudaMalloc(&out, 8);
+  cudaMalloc(&cyc, 16 * 8);
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, 0);
+  const int sms = p.multiProcessorCount;
+  for (int ch : {1, 4, 8}) {
+    for (int mw : {0, 4, 8}) {
+      long long h[16] = {};
+      const int len = 20000, steps = mw ? 4000 : 0;
+      cudaMemset(cyc, 0, 128);
+      if (ch == 1) k<1><<<sms, 512>>>(out, cyc, mw, steps, len);
+      if (ch == 4) k<4><<<sms, 512>>>(out, cyc, mw, steps, len);
+      if (ch == 8) k<8><<<sms, 512>>>(out, cyc, mw, steps, len);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, cyc, 128, cudaMemcpyDeviceToHost);
+      long long mma = 0, side = 0;
+      for (int w = 0; w < 8; ++w) mma = h[w] > mma ? h[w] : mma;
+      for (int w = 8; w < 16; ++w) side = h[w] > side ? h[w] : side;
+      printf("chains %d, %d MMA warps: MMA warps %lld clk, side warps %lld clk (%.2f clk per dependent DFMA step)\n",
+             ch, mw, mma, side, (double)side / len);
+    }
+  }
+  return 0;
+}
