@@ -153,6 +153,17 @@ __device__ __forceinline__ void gaussian_pairs_fast(const BmTables& T, uint64_t 
   }
   box_muller_bits<P>(T, b1, b2, g_even, g_odd);
 }
+// Same, from each pair's first counter word z = seed + (2p + 1) G (the second is z + G).
+template <int P>
+__device__ __forceinline__ void gaussian_pairs_z(const BmTables& T, const uint64_t (&z)[P], double (&g_even)[P],
+                                                 double (&g_odd)[P]) {
+  uint64_t b1[P], b2[P];
+  CQR_BM_EACH {
+    b1[j] = mix64(z[j]);
+    b2[j] = mix64(z[j] + 0x9E3779B97F4A7C15ull);
+  }
+  box_muller_bits<P>(T, b1, b2, g_even, g_odd);
+}
 #undef CQR_BM_EACH
 
 __device__ __forceinline__ void gaussian_pair_fast(const BmTables& T, uint64_t seed, uint64_t p, double& g_even,

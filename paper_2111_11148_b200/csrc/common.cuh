@@ -50,6 +50,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // ---- counter RNG (rng.hpp:18-55), bit-exact on the integer part ------------------
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;  // counter stride (rng.hpp:29)
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;

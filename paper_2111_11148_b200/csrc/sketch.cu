@@ -272,6 +272,16 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   if (warp >= kWsMma) {
     // ---- generator warps: Omega tiles + the A tile's TMA
     const int gt = tid - kWsMma * 32;
+    // Counter state of each of this thread's pairs: pair p = (c >> 1) + pp with c = (s0 + i) m_global
+    // + row0 + k (even: m_global, row0 and the chunk starts are even), so from one step to the next
+    // p grows by kKS/2 and the pair's first counter word seed + (2p + 1) G by kKS G.
+    uint64_t z[S::PAIRS];
+#pragma unroll
+    for (int u = 0; u < S::PAIRS; ++u) {
+      const int e = gt + kWsGen * 32 * u;
+      const unsigned long long c0 = (unsigned long long)(s0 + (e >> 4)) * (unsigned long long)m_global + row0 + k_begin;
+      z[u] = seed + (2 * ((c0 >> 1) + (e & 15)) + 1) * kGolden;
+    }
     for (int stp = 0; stp < nsteps; ++stp) {
       const int s = stp % kWsStages;
       mbar_wait(&empty[s], ((stp / kWsStages) & 1) ^ 1);
@@ -288,19 +298,18 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       double* Om = sO + s * S::OTILE;
 #pragma unroll
       for (int u0 = 0; u0 < S::PAIRS; u0 += S::ILP) {
-        uint64_t pc[S::ILP];
+        uint64_t zz[S::ILP];
         double ge[S::ILP], go[S::ILP];
 #pragma unroll
         for (int j = 0; j < S::ILP; ++j) {
-          const int e = gt + kWsGen * 32 * (u0 + j);
-          const unsigned long long c_lo = (unsigned long long)(s0 + (e >> 4)) * (unsigned long long)m_global + row0 + kb;
-          pc[j] = (c_lo >> 1) + (e & 15);
+          zz[j] = z[u0 + j];
+          z[u0 + j] += (uint64_t)kKS * kGolden;
         }
 #ifdef CQR_WS_FAKEGEN  // probe: constant draws (the MMA-side bound of this kernel)
 #pragma unroll
-        for (int j = 0; j < S::ILP; ++j) ge[j] = (double)(pc[j] & 255) * 0x1.0p-8, go[j] = 0.5;
+        for (int j = 0; j < S::ILP; ++j) ge[j] = (double)(zz[j] & 255) * 0x1.0p-8, go[j] = 0.5;
 #else
-        gaussian_pairs_fast<S::ILP>(T, seed, pc, ge, go);
+        gaussian_pairs_z<S::ILP>(T, zz, ge, go);
 #endif
 #pragma unroll
         for (int j = 0; j < S::ILP; ++j) {
@@ -333,6 +342,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #endif
     const double* Om = sO + s * S::OTILE + gr * LDO + q;
     const double* As = sA + s * S::ATILE;
+#ifdef CQR_WS_NOMMA  // probe: generator-only throughput (the MMA warps just cycle the ring)
+    if (nsteps > 0) {
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      continue;
+    }
+#endif
 #pragma unroll
     for (int k4 = 0; k4 < kKS / 4; ++k4) {
       const int r = 4 * k4 + q;

@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   if (lane == 0 && grp < groups) issue_in(0, grp);
   for (; grp < groups; grp += gstride) {
     const int row0 = (int)(grp * kRW);
+    // warps of this CTA with a group in this round (the others have left the loop)
+    const int nact_thr = (int)min((long long)WPC, groups - (grp - warp)) * 32;
 #pragma unroll 1
     for (int P = 0; P < NPASS; ++P) {
       const int c0 = 8 * W * P;
@@ -182,6 +184,9 @@ __global__ void __launch_bounds__(WPC * 32, 1)
         for (int g = 0; g < 4; ++g)
           *reinterpret_cast<double2*>(tile + swz64(8 * g + gr, q)) = make_double2(acc[g][0][0], acc[g][0][1]);
         __syncwarp();
+#ifdef CQR_TRI_SYNC
+        asm volatile("bar.sync 1, %0;" ::"r"(nact_thr) : "memory");
+#endif
         {
           const double* D = sD + J * kDiagStride;
           double y[8];
@@ -230,6 +235,9 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           for (int u = 0; u < 4; ++u)
             *reinterpret_cast<double2*>(tile + swz64(lane, u)) = make_double2(y[2 * u], y[2 * u + 1]);
         }
+#ifdef CQR_TRI_SYNC
+        asm volatile("bar.sync 1, %0;" ::"r"(nact_thr) : "memory");
+#endif
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
