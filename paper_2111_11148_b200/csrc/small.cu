@@ -372,6 +372,45 @@ __global__ void __launch_bounds__(512) lu_blocked_kernel(const double* __restric
     for (int c = lane; c < n; c += 32) u[(long long)i * n + c] = c >= i ? W[(long long)i * n + c] : 0.0;
 }
 
+__device__ __forceinline__ double div_rn(double y, double d, double inv) {
+  // correctly rounded y / d from inv = RN(1/d), one Markstein correction (see trisolve_common.cuh)
+  const double ay = fabs(y);
+  if (!(ay >= 0x1p-400 && ay <= 0x1p+400) || !(fabs(d) >= 0x1p-500 && fabs(d) <= 0x1p+500)) return y / d;
+  const double q0 = y * inv;
+  const double r = fma(-q0, d, y);
+  return fma(r, inv, q0);
+}
+
+// Arg-max of (|x| as its bit pattern (hi, lo), then the smallest logical position) over a warp's
+// lanes; lanes with cand false take no part. Fast path: one redux.sync on the high word when it
+// is unique and non-zero; otherwise the full key. Returns the winning lane (-1 if no candidate).
+__device__ __forceinline__ int warp_argmax_key(bool cand, unsigned hi, unsigned lo, unsigned pos) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const unsigned mhi = __reduce_max_sync(kFull, cand ? hi : 0u);
+  const unsigned top = __ballot_sync(kFull, cand && hi == mhi);
+  if (mhi != 0u && __popc(top) == 1) return __ffs(top) - 1;
+  const bool c1 = cand && hi == mhi;
+  const unsigned mlo = __reduce_max_sync(kFull, c1 ? lo : 0u);
+  const bool c2 = c1 && lo == mlo;
+  const unsigned mpos = __reduce_min_sync(kFull, c2 ? pos : 0xffffffffu);
+  return __ffs(__ballot_sync(kFull, c2 && pos == mpos)) - 1;
+}
+
+#ifdef CQR_LU_TRACE  // probe: clock64 marks of thread 0 (read with cqr_debug_lu_trace, tools/gpu/lu_trace.py)
+__device__ long long g_lu_trace[1024];
+#define LU_MARK(i) \
+  {                                          \
+    if (threadIdx.x == 0) g_lu_trace[i] = clock64(); \
+  }
+#else
+#define LU_MARK(i) \
+  {}
+#endif
+#ifndef CQR_LU_UNROLL
+#define CQR_LU_UNROLL 4
+#endif
+constexpr int kLuUnroll = CQR_LU_UNROLL;
+
 // l <= 512: one thread per physical row, the panel's 32 columns of that row in
 // registers. Rows never move: partial pivoting is tracked with logical
 // positions (ties go to the smallest one: the reference's "first maximum" in its
@@ -384,9 +423,10 @@ template <int NW, int PW>
 __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restrict__ a1, int l, int n,
                                                         double* __restrict__ u, double* W, DevStatus* st) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double prow[PW];
-  __shared__ double wb[2][NW];
-  __shared__ int wl[2][NW], wr[2][NW];
+  __shared__ __align__(16) double cv[2][NW][PW];  // each warp winner's panel row, double-buffered
+  __shared__ double cinv[2][NW];                  // and RN(1 / its current element)
+  __shared__ unsigned chi[2][NW], clo[2][NW], clp[2][NW];
+  __shared__ int crow[2][NW];
   __shared__ int pv[PW];
   if (failed(st)) return;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
@@ -408,85 +448,81 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
     for (int c = lane; c < i; c += 32) u[(long long)i * n + c] = 0.0;
   int my_lp = tid, buf = 0;
   __syncthreads();
+  LU_MARK(0)
   for (int j0 = 0; j0 < n; j0 += PW) {
     const int w = min(PW, n - j0);
+    LU_MARK(1 + 4 * (j0 / PW))
     double x[PW];
 #pragma unroll
     for (int c = 0; c < PW; ++c) x[c] = (mine && c < w) ? W[(long long)tid * n + j0 + c] : 0.0;
+    // kLuUnroll pivot steps per iteration with the current column x[o] (compile-time u), then
+    // one rotation by kLuUnroll: the rolled loop keeps the code small, the unroll divides the
+    // register moves of the rotation
 #pragma unroll 1
-    for (int jj = 0; jj < w; ++jj) {
-      const int j = j0 + jj;
-      const bool act = mine && my_lp >= j;
-      double best = act ? fabs(x[0]) : -1.0;
-      int blp = act ? my_lp : 0x7fffffff, brow = tid;
+    for (int jb = 0; jb < w; jb += kLuUnroll) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, blp, o);
-        const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
-        if (ob > best || (ob == best && ol < blp)) {
-          best = ob;
-          blp = ol;
-          brow = orow;
-        }
-      }
-      if (lane == 0) {
-        wb[buf][warp] = best;
-        wl[buf][warp] = blp;
-        wr[buf][warp] = brow;
-      }
-      __syncthreads();
-      {  // the NW warp winners, reduced by shuffles in every warp (all take the same decision)
-        constexpr int NWP = NW <= 4 ? 4 : NW <= 8 ? 8 : NW <= 16 ? 16 : 32;  // power-of-two butterfly
-        const int k = lane % NWP;
-        best = k < NW ? wb[buf][k] : -1.0;
-        blp = k < NW ? wl[buf][k] : 0x7fffffff;
-        brow = k < NW ? wr[buf][k] : 0;
+      for (int o = 0; o < kLuUnroll; ++o) {
+        const int jj = jb + o;
+        if (jj >= w) break;
+        const int j = j0 + jj;
+        LU_MARK(100 + j)
+        const bool act = mine && my_lp >= j;
+        {  // this warp's arg-max; its winner publishes key, row (from x[o] on) and RN(1/x[o])
+          const double ax = fabs(x[o]);
+          const unsigned khi = (unsigned)__double2hiint(ax), klo = (unsigned)__double2loint(ax);
+          const int wl = warp_argmax_key(act, khi, klo, (unsigned)my_lp);
+          if (lane == (wl < 0 ? 0 : wl)) {
 #pragma unroll
-        for (int o = NWP / 2; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int ol = __shfl_xor_sync(0xffffffffu, blp, o);
-          const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
-          if (ob > best || (ob == best && ol < blp)) {
-            best = ob;
-            blp = ol;
-            brow = orow;
+            for (int c = o; c < PW; c += 2)
+              *reinterpret_cast<double2*>(&cv[buf][warp][c - o]) = make_double2(x[c], c + 1 < PW ? x[c + 1] : 0.0);
+            cinv[buf][warp] = wl < 0 ? 0.0 : __drcp_rn(x[o]);
+            chi[buf][warp] = wl < 0 ? 0u : khi;
+            clo[buf][warp] = wl < 0 ? 0u : klo;
+            clp[buf][warp] = wl < 0 ? 0xffffffffu : (unsigned)my_lp;
+            crow[buf][warp] = tid;
           }
         }
-      }
-      buf ^= 1;
-      if (!(best > 0.0)) {  // exact zero pivot (kernels.hpp:235)
-        if (tid == 0) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, j);
-        return;
-      }
-      const int ps = brow;
-      if (tid == ps) {
-#pragma unroll
-        for (int c = 0; c < PW; ++c) {
-          prow[c] = x[c];
-          if (c < w - jj) u[(long long)j * n + j + c] = x[c];  // U row j, panel part
+        if (j < 32) LU_MARK(300 + 8 * j)
+        __syncthreads();
+        if (j < 32) LU_MARK(301 + 8 * j)
+        // the NW slots, reduced the same way in every warp (all take the same decision)
+        const bool in = lane < NW;
+        const unsigned ghi = in ? chi[buf][lane] : 0u, glo = in ? clo[buf][lane] : 0u;
+        const unsigned glp = in ? clp[buf][lane] : 0xffffffffu;
+        const int ww = warp_argmax_key(in && glp != 0xffffffffu, ghi, glo, glp);
+        if (ww < 0 || (chi[buf][ww] | clo[buf][ww]) == 0u) {  // exact zero pivot (kernels.hpp:235)
+          if (tid == 0) set_status(st, 2 /*CQR_SINGULAR_TRIANGULAR*/, j);
+          return;
         }
-        pv[jj] = ps;
-      }
-      __syncthreads();
-      if (act && tid != ps) {
-        const double mult = x[0] / prow[0];
-        P[tid * kLuLdp + jj] = mult;
-        if (mult != 0.0) {
-#pragma unroll
-          for (int c = 1; c < PW; ++c) x[c] = fma(-mult, prow[c], x[c]);
+        const double* prow = cv[buf][ww];
+        const int ps = crow[buf][ww], blp = (int)clp[buf][ww];
+        const double pinv = cinv[buf][ww];
+        buf ^= 1;
+        if (j < 32) LU_MARK(302 + 8 * j)
+        if (warp == 0) {  // U row j, panel part
+          if (lane < w - jj) u[(long long)j * n + j + lane] = prow[lane];
+          if (lane == 0) pv[jj] = ps;
         }
-      }
-      if (tid == ps)
-        my_lp = j;
-      else if (my_lp == j)
-        my_lp = blp;  // the row at position j takes the pivot's old position
+        if (act && tid != ps) {
+          const double mult = div_rn(x[o], prow[0], pinv);
+          P[tid * kLuLdp + jj] = mult;
+          if (mult != 0.0) {
 #pragma unroll
-      for (int c = 0; c < PW - 1; ++c) x[c] = x[c + 1];
-      x[PW - 1] = 0.0;
+            for (int c = o + 1; c < PW; ++c) x[c] = fma(-mult, prow[c - o], x[c]);
+          }
+        }
+        if (j < 32) LU_MARK(303 + 8 * j)
+        if (tid == ps)
+          my_lp = j;
+        else if (my_lp == j)
+          my_lp = blp;  // the row at position j takes the pivot's old position
+      }
+#pragma unroll
+      for (int c = 0; c < PW; ++c) x[c] = c + kLuUnroll < PW ? x[c + kLuUnroll] : 0.0;
     }
     if (mine) lpS[tid] = my_lp;
     __syncthreads();
+    LU_MARK(2 + 4 * (j0 / PW))
     const int c1 = j0 + w;
     if (c1 < n) {
       // U12 = L11^-1 A12 on the pivot rows: one thread per trailing column, fma chain over
@@ -511,6 +547,7 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
           if (jj < w) u[(long long)(j0 + jj) * n + c] = y[jj];
       }
       __syncthreads();
+      LU_MARK(4 + 4 * (j0 / PW))
       // A22 += (-L21) U12 on DMMA for the rows still unpivoted (k = pivots in order)
       const int q = lane & 3, gr = lane >> 2;
       const int tr = (l + 7) / 8, tc = (n - c1 + 7) / 8;
@@ -536,6 +573,7 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       }
     }
     __syncthreads();
+    LU_MARK(3 + 4 * (j0 / PW))
   }
 }
 
@@ -556,15 +594,6 @@ cudaError_t launch_lu_rot(const double* a1, int l, int n, double* u, double* wor
 // ascending order on DMMA. S lives in the L2-resident global workspace, the
 // panel rows in shared memory.
 constexpr int kChPanel = 32;
-
-__device__ __forceinline__ double div_rn(double y, double d, double inv) {
-  // correctly rounded y / d from inv = RN(1/d), one Markstein correction (see trisolve_common.cuh)
-  const double ay = fabs(y);
-  if (!(ay >= 0x1p-400 && ay <= 0x1p+400) || !(fabs(d) >= 0x1p-500 && fabs(d) <= 0x1p+500)) return y / d;
-  const double q0 = y * inv;
-  const double r = fma(-q0, d, y);
-  return fma(r, inv, q0);
-}
 
 __global__ void __launch_bounds__(512) cholesky_blocked_kernel(const double* __restrict__ g, int n,
                                                                double* __restrict__ r, double* S, int shift_mode,
@@ -1080,3 +1109,9 @@ cudaError_t launch_normalize_sign(double* r, int n, double* sgn, const DevStatus
 }
 
 }  // namespace cqr
+
+#ifdef CQR_LU_TRACE
+extern "C" int cqr_debug_lu_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, cqr::g_lu_trace, sizeof(cqr::g_lu_trace));
+}
+#endif

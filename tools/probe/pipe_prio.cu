@@ -13,22 +13,22 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int CH>
+template <int CH, int MCH = 16>
 __global__ void __launch_bounds__(512, 1) k(double* out, long long* cyc, int mma_warps, int steps, int len) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t0 = clock64();
   if (warp < mma_warps) {
-    double acc[16][2];
+    double acc[MCH][2];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = threadIdx.x + i;
+    for (int i = 0; i < MCH; ++i) acc[i][0] = acc[i][1] = threadIdx.x + i;
     const double a = 1.0 + threadIdx.x * 1e-9, b = 1e-3;
-    for (int s = 0; s < steps; ++s) {
+    for (int s = 0; s < steps * 16 / MCH; ++s) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) dmma(acc[i][0], acc[i][1], a, b);
+      for (int i = 0; i < MCH; ++i) dmma(acc[i][0], acc[i][1], a, b);
     }
     double t = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) t += acc[i][0] + acc[i][1];
+    for (int i = 0; i < MCH; ++i) t += acc[i][0] + acc[i][1];
     if (t == 1234.5) out[0] = t;
   } else if (warp >= 8) {
     double x[CH];
@@ -71,6 +71,23 @@ int main() {
       printf("chains %d, %d MMA warps: MMA warps %lld clk, side warps %lld clk (%.2f clk per dependent DFMA step)\n",
              ch, mw, mma, side, (double)side / len);
     }
+  }
+  // MMA warps with fewer independent DMMA chains: does the side chain get the pipe sooner?
+  for (int mch : {2, 4, 8, 16}) {
+    long long h[16] = {};
+    const int len = 20000, steps = 4000;
+    cudaMemset(cyc, 0, 128);
+    if (mch == 2) k<1, 2><<<sms, 512>>>(out, cyc, 8, steps, len);
+    if (mch == 4) k<1, 4><<<sms, 512>>>(out, cyc, 8, steps, len);
+    if (mch == 8) k<1, 8><<<sms, 512>>>(out, cyc, 8, steps, len);
+    if (mch == 16) k<1, 16><<<sms, 512>>>(out, cyc, 8, steps, len);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, cyc, 128, cudaMemcpyDeviceToHost);
+    long long mma = 0, side = 0;
+    for (int w = 0; w < 8; ++w) mma = h[w] > mma ? h[w] : mma;
+    for (int w = 8; w < 16; ++w) side = h[w] > side ? h[w] : side;
+    printf("8 MMA warps x %2d DMMA chains: MMA warps %lld clk (%.1f%% of 2.05M), side chain %.2f clk per DFMA step\n", mch,
+           mma, 2.05e6 / mma * 100, (double)side / len);
   }
   return 0;
 }
