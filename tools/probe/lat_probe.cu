@@ -1,76 +1,51 @@
-// Dependent-issue latency (SM cycles) of the warp primitives the small factorizations use:
-// redux.sync max (u32), shfl.sync, vote.ballot, an LDS round trip, DFMA, DMUL, __drcp_rn, IEEE division.
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o lat_probe lat_probe.cu
+// Latency probe: dependent-chain latency of DMMA, DFMA, DDIV, shfl, and the
+// Markstein division sequence (one warp, clock64 around long chains).
+#include <cstdio>
+#include <cstdint>
 #include <cuda_runtime.h>
 
-#include <cstdio>
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
 
-__global__ void k(long long* cyc, unsigned* outu, double* outd, int iters) {
-  __shared__ unsigned sm[64];
-  const int lane = threadIdx.x & 31;
-  sm[lane] = lane;
-  __syncwarp();
-  unsigned v = lane * 7 + 1;
-  double d = 1.0 + lane * 1e-3;
-  long long t0, t1;
-  // redux
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) v = __reduce_max_sync(0xffffffffu, v + lane) & 0xffff;
-  t1 = clock64();
-  if (lane == 0) cyc[0] = t1 - t0;
-  // shfl
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) v = __shfl_xor_sync(0xffffffffu, v, 1) + 1;
-  t1 = clock64();
-  if (lane == 0) cyc[1] = t1 - t0;
-  // ballot
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) v = __ballot_sync(0xffffffffu, (v >> lane) & 1) + lane;
-  t1 = clock64();
-  if (lane == 0) cyc[2] = t1 - t0;
-  // lds
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) v = sm[v & 31];
-  t1 = clock64();
-  if (lane == 0) cyc[3] = t1 - t0;
-  // dfma
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) d = fma(d, 0.999999, 1e-7);
-  t1 = clock64();
-  if (lane == 0) cyc[4] = t1 - t0;
-  // drcp
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) d = __drcp_rn(d) + 0.5;
-  t1 = clock64();
-  if (lane == 0) cyc[5] = t1 - t0;
-  // div
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) d = 1.5 / d + 0.25;
-  t1 = clock64();
-  if (lane == 0) cyc[6] = t1 - t0;
-  // fabs + compare + select chain (DADD for fabs?)
-  t0 = clock64();
-  for (int i = 0; i < iters; ++i) d = fabs(d - 2.0) + 0.5;
-  t1 = clock64();
-  if (lane == 0) cyc[7] = t1 - t0;
-  outu[threadIdx.x] = v;
-  outd[threadIdx.x] = d;
+__global__ void k(double* out, long long* cyc, int iters, double x, double d) {
+  double c0 = threadIdx.x, c1 = 1.0, a = x, b = x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) dmma(c0, c1, a, b);
+  long long t1 = clock64();
+  double f = threadIdx.x;
+  for (int i = 0; i < iters; ++i) f = fma(f, x, d);
+  long long t2 = clock64();
+  double q = threadIdx.x + 1.0;
+  for (int i = 0; i < iters; ++i) q = q / d;
+  long long t3 = clock64();
+  double s = threadIdx.x;
+  for (int i = 0; i < iters; ++i) s = __shfl_sync(0xffffffffu, s, (threadIdx.x + 1) & 31) * x;
+  long long t4 = clock64();
+  const double inv = 1.0 / d;
+  double y = threadIdx.x + 1.0;
+  for (int i = 0; i < iters; ++i) {
+    double q0 = y * inv;
+    double r = fma(-q0, d, y);
+    double q1 = fma(r, inv, q0);
+    r = fma(-q1, d, y);
+    y = fma(r, inv, q1);
+  }
+  long long t5 = clock64();
+  out[threadIdx.x] = c0 + c1 + f + q + s + y;
+  if (threadIdx.x == 0) {
+    cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = t3 - t2; cyc[3] = t4 - t3; cyc[4] = t5 - t4;
+  }
 }
 
 int main() {
-  long long* cyc;
-  unsigned* ou;
-  double* od;
-  cudaMalloc(&cyc, 8 * 16);
-  cudaMalloc(&ou, 4 * 32);
-  cudaMalloc(&od, 8 * 32);
-  const int iters = 4096;
-  k<<<1, 32>>>(cyc, ou, od, iters);
-  k<<<1, 32>>>(cyc, ou, od, iters);
-  long long h[8];
-  cudaMemcpy(h, cyc, 64, cudaMemcpyDeviceToHost);
-  const char* names[] = {"redux.max+iadd", "shfl+iadd", "ballot+iadd", "lds (dependent)", "dfma", "drcp_rn+dadd",
-                         "ieee div+dadd", "dadd+fabs(dadd)"};
-  for (int i = 0; i < 8; ++i) printf("%-18s %6.1f cycles per iteration\n", names[i], (double)h[i] / iters);
+  double* o; long long* c; cudaMalloc(&o, 1024); cudaMalloc(&c, 64);
+  const int it = 4096;
+  k<<<1, 32>>>(o, c, it, 1.0000001, 1.0000003);
+  k<<<1, 32>>>(o, c, it, 1.0000001, 1.0000003);
+  long long h[5]; cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
+  const char* nm[5] = {"DMMA chain", "DFMA chain", "DDIV chain", "SHFL+DMUL chain", "Markstein div (5 ops) chain"};
+  for (int i = 0; i < 5; ++i) printf("%-28s %.1f cycles/op\n", nm[i], (double)h[i] / it);
   return 0;
 }

@@ -13,9 +13,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int CH, int MCH = 16>
+template <int CH, int MCH = 16, int SIDE_DMMA = 0, bool SWAP = false>
 __global__ void __launch_bounds__(512, 1) k(double* out, long long* cyc, int mma_warps, int steps, int len) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = SWAP ? ((threadIdx.x >> 5) ^ 8) : (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const long long t0 = clock64();
   if (warp < mma_warps) {
     double acc[MCH][2];
@@ -34,10 +34,17 @@ __global__ void __launch_bounds__(512, 1) k(double* out, long long* cyc, int mma
     double x[CH];
 #pragma unroll
     for (int i = 0; i < CH; ++i) x[i] = 1.0 + threadIdx.x * 1e-7 + i * 1e-3;
+    double sacc[SIDE_DMMA > 0 ? SIDE_DMMA : 1][2];
+#pragma unroll
+    for (int i = 0; i < (SIDE_DMMA > 0 ? SIDE_DMMA : 1); ++i) sacc[i][0] = sacc[i][1] = i;
     for (int it = 0; it < len; ++it) {
 #pragma unroll
       for (int i = 0; i < CH; ++i) x[i] = fma(x[i], 0.999999, 1e-7);
+#pragma unroll
+      for (int i = 0; i < SIDE_DMMA; ++i) dmma(sacc[i][0], sacc[i][1], x[0], 1e-3);
     }
+#pragma unroll
+    for (int i = 0; i < (SIDE_DMMA > 0 ? SIDE_DMMA : 1); ++i) x[0] += sacc[i][0] + sacc[i][1];
     double t = 0;
 #pragma unroll
     for (int i = 0; i < CH; ++i) t += x[i];
@@ -71,6 +78,34 @@ int main() {
       printf("chains %d, %d MMA warps: MMA warps %lld clk, side warps %lld clk (%.2f clk per dependent DFMA step)\n",
              ch, mw, mma, side, (double)side / len);
     }
+  }
+  // side warps that also issue DMMAs (on independent accumulators) between their dependent DFMAs
+  for (int sd : {0, 1, 2, 4}) {
+    long long h[16] = {};
+    const int len = 20000, steps = 4000;
+    cudaMemset(cyc, 0, 128);
+    if (sd == 0) k<1, 16, 0><<<sms, 512>>>(out, cyc, 8, steps, len);
+    if (sd == 1) k<1, 16, 1><<<sms, 512>>>(out, cyc, 8, steps, len);
+    if (sd == 2) k<1, 16, 2><<<sms, 512>>>(out, cyc, 8, steps, len);
+    if (sd == 4) k<1, 16, 4><<<sms, 512>>>(out, cyc, 8, steps, len);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, cyc, 128, cudaMemcpyDeviceToHost);
+    long long mma = 0, side = 0;
+    for (int w = 0; w < 8; ++w) mma = h[w] > mma ? h[w] : mma;
+    for (int w = 8; w < 16; ++w) side = h[w] > side ? h[w] : side;
+    printf("side warps with %d DMMA per DFMA step: MMA warps %lld clk, side %.2f clk per step\n", sd, mma,
+           (double)side / len);
+  }
+  {  // MMA warps on the high hardware warp ids
+    long long h[16] = {};
+    cudaMemset(cyc, 0, 128);
+    k<1, 16, 0, true><<<sms, 512>>>(out, cyc, 8, 4000, 20000);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, cyc, 128, cudaMemcpyDeviceToHost);
+    long long mma = 0, side = 0;
+    for (int w = 0; w < 8; ++w) mma = h[w] > mma ? h[w] : mma;
+    for (int w = 8; w < 16; ++w) side = h[w] > side ? h[w] : side;
+    printf("MMA warps on hardware warps 8-15: MMA %lld clk, side %.2f clk per DFMA step\n", mma, (double)side / 20000);
   }
   // MMA warps with fewer independent DMMA chains: does the side chain get the pipe sooner?
   for (int mch : {2, 4, 8, 16}) {
