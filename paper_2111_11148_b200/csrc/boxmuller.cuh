@@ -43,13 +43,21 @@ struct BmTables {
 // sin and cos of 2 pi k / 256: k = 64 q + m, rotate the first-quadrant pair by q quarter turns
 __device__ __forceinline__ void bm_table_sincos(const BmTables& T, int k, double& S, double& C) {
   const int q = k >> 6, m = k & 63;
-  const double s0 = T.q[m], c0 = T.q[64 - m];
-  const bool swap = q & 1;
-  const long long sb = __double_as_longlong(swap ? c0 : s0), cb = __double_as_longlong(swap ? s0 : c0);
+  const bool swap = q & 1;  // odd quarter turns exchange sin and cos: swap the table index
+  const long long sb = __double_as_longlong(T.q[swap ? 64 - m : m]), cb = __double_as_longlong(T.q[swap ? m : 64 - m]);
   const long long sneg = (long long)(q >> 1) << 63, cneg = (long long)((q ^ (q >> 1)) & 1) << 63;
   S = __longlong_as_double(sb ^ sneg);
   C = __longlong_as_double(cb ^ cneg);
 }
+
+// Polynomial and reduction constants in the constant bank: DFMA takes a c[][] operand
+// directly, where an immediate double costs two register moves per use.
+__constant__ double kBmK[] = {
+    -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,                           // 0-4: log1p
+    0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45,                                   // 5-6: ln 2 hi, lo
+    0x1.921fb54400000p-6, 0x1.0b4611a600000p-40, 0x1.3198a2e037073p-75,          // 7-9: 2 pi / 256, 3 parts
+    1.5, 1.0 / 120.0, -1.0 / 720.0, 1.0 / 24.0, 1.0, 0x1.921fb54442d18p-51, -1.0  // 10-16
+};
 
 __device__ __forceinline__ double rsqrt_approx(double x) {
   double y;
@@ -74,7 +82,7 @@ __device__ __forceinline__ void box_muller_bits(const BmTables& T, const uint64_
     // a = RN(2 pi) * u2 with u2 = N2 * 2^-53: the power-of-two scaling commutes with the
     // rounding (a is 0 or >= 2^-51), so one multiply by RN(2 pi) * 2^-53 gives the same a
     const uint64_t n2 = b2[j] >> 11;
-    a[j] = (double)n2 * 0x1.921fb54442d18p-51;
+    a[j] = (double)n2 * kBmK[15];
     // table point k = round(256 u2) in [0, 256] (k = 256 reduces with 2 pi and reads entry 0)
     const int kk = (int)((n2 + (1ull << 44)) >> 45);
     k[j] = kk & (kBmTrig - 1);
@@ -92,49 +100,48 @@ __device__ __forceinline__ void box_muller_bits(const BmTables& T, const uint64_
     ti[j] = i - kBmLogLo;
     e[j] = (hi >> 20) - 1023 - 53 + (up ? 1 : 0);
     const double f = __hiloint2double(mh | (up ? 0x3FE00000 : 0x3FF00000), lo);  // [0.708, 1.416)
-    r[j] = fma(f, T.inv[ti[j]], -1.0);
+    r[j] = fma(f, T.inv[ti[j]], kBmK[16]);
   }
   CQR_BM_EACH r2[j] = r[j] * r[j];
-  CQR_BM_EACH pl[j] = fma(-1.0 / 6.0, r[j], 1.0 / 5.0);
-  CQR_BM_EACH pl[j] = fma(pl[j], r[j], -1.0 / 4.0);
-  CQR_BM_EACH pl[j] = fma(pl[j], r[j], 1.0 / 3.0);
-  CQR_BM_EACH pl[j] = fma(pl[j], r[j], -0.5);
+  CQR_BM_EACH pl[j] = fma(r[j], kBmK[0], kBmK[1]);
+  CQR_BM_EACH pl[j] = fma(pl[j], r[j], kBmK[2]);
+  CQR_BM_EACH pl[j] = fma(pl[j], r[j], kBmK[3]);
+  CQR_BM_EACH pl[j] = fma(pl[j], r[j], kBmK[4]);
   double L[P];
   CQR_BM_EACH {
     const double l1p = fma(r2[j], pl[j], r[j]);
     const double ed = (double)e[j];
-    const double ln2_hi = 0x1.62e42fefa3800p-1, ln2_lo = 0x1.ef35793c76730p-45;
-    L[j] = fma(ed, ln2_hi, T.lhi[ti[j]]) + (fma(ed, ln2_lo, T.llo[ti[j]]) + l1p);
+    L[j] = fma(ed, kBmK[5], T.lhi[ti[j]]) + (fma(ed, kBmK[6], T.llo[ti[j]]) + l1p);
   }
   // ---- sincos(a): d = a - k * 2 pi / 256 (three parts; k * part 1 and k * part 2 are exact)
   double d[P];
   CQR_BM_EACH {
-    d[j] = fma(-fk[j], 0x1.921fb54400000p-6, a[j]);
-    d[j] = fma(-fk[j], 0x1.0b4611a600000p-40, d[j]);
-    d[j] = fma(-fk[j], 0x1.3198a2e037073p-75, d[j]);
+    d[j] = fma(-fk[j], kBmK[7], a[j]);
+    d[j] = fma(-fk[j], kBmK[8], d[j]);
+    d[j] = fma(-fk[j], kBmK[9], d[j]);
   }
-  // ---- sqrt(-2 L): L is 0 or a normal number (|L| >= 2^-54), so x = -2 L is a sign flip
-  // plus one on the exponent, and -x/2 is L itself
+  // ---- sqrt(-2 L): L is +0 (never -0: its high part is +0 whenever the sum can vanish) or a
+  // normal number (|L| >= 2^-54), so x = -2 L is a sign flip plus one on the exponent, and -x/2
+  // is L itself; L = +0 maps to x = -2^-1022, which the x > 0 test below sends to r = 0
   double x[P], y[P];
   CQR_BM_EACH {
-    const long long Lb = __double_as_longlong(L[j]);
-    x[j] = (Lb << 1) == 0 ? 0.0 : __longlong_as_double((Lb ^ (1ll << 63)) + (1ll << 52));
+    x[j] = __longlong_as_double((__double_as_longlong(L[j]) ^ (1ll << 63)) + (1ll << 52));
     y[j] = rsqrt_approx(x[j]);
   }
   double d2[P], sp[P], cp[P];
   CQR_BM_EACH d2[j] = d[j] * d[j];
-  CQR_BM_EACH y[j] = y[j] * fma(L[j], y[j] * y[j], 1.5);  // one Newton step (a second one changed no draw in 1e7)
+  CQR_BM_EACH y[j] = y[j] * fma(L[j], y[j] * y[j], kBmK[10]);  // one Newton step (a second one changed no draw in 1e7)
   // sin d = d + d^3 (-1/6 + d^2/120) (next term <= 8.6e-18); cos d to d^6 (next term <= 1.3e-20)
-  CQR_BM_EACH sp[j] = fma(d2[j], 1.0 / 120.0, -1.0 / 6.0);
-  CQR_BM_EACH cp[j] = fma(d2[j], -1.0 / 720.0, 1.0 / 24.0);
-  CQR_BM_EACH cp[j] = fma(cp[j], d2[j], -0.5);
+  CQR_BM_EACH sp[j] = fma(d2[j], kBmK[11], kBmK[0]);
+  CQR_BM_EACH cp[j] = fma(d2[j], kBmK[12], kBmK[13]);
+  CQR_BM_EACH cp[j] = fma(cp[j], d2[j], kBmK[4]);
   CQR_BM_EACH {
     double s = x[j] * y[j];
     const double hy = __longlong_as_double(__double_as_longlong(y[j]) - (1ll << 52));  // y / 2, y normal
     s = fma(hy, fma(-s, s, x[j]), s);
     const double rad = __double_as_longlong(x[j]) > 0 ? s : 0.0;
     const double sn = fma(d[j] * d2[j], sp[j], d[j]);
-    const double cs = fma(cp[j], d2[j], 1.0);
+    const double cs = fma(cp[j], d2[j], kBmK[14]);
     double S, C;
     bm_table_sincos(T, k[j], S, C);
     g_even[j] = rad * fma(C, cs, -(S * sn));

@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     // Counter state of each of this thread's pairs: pair p = (c >> 1) + pp with c = (s0 + i) m_global
     // + row0 + k (even: m_global, row0 and the chunk starts are even), so from one step to the next
     // p grows by kKS/2 and the pair's first counter word seed + (2p + 1) G by kKS G.
+    const bool all_live = s0 + ST <= l;
     uint64_t z[S::PAIRS];
 #pragma unroll
     for (int u = 0; u < S::PAIRS; ++u) {
@@ -315,8 +316,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         for (int j = 0; j < S::ILP; ++j) {
           const int e = gt + kWsGen * 32 * (u0 + j);
           const int i = e >> 4, pp = e & 15;
-          const bool live = s0 + i < l;
-          *reinterpret_cast<double2*>(Om + i * LDO + 2 * pp) = make_double2(live ? ge[j] : 0.0, live ? go[j] : 0.0);
+          if (!all_live && s0 + i >= l) ge[j] = go[j] = 0.0;  // Omega rows past l (last s-tile only)
+          *reinterpret_cast<double2*>(Om + i * LDO + 2 * pp) = make_double2(ge[j], go[j]);
         }
       }
 #ifdef CQR_WS_TRACE
