@@ -238,7 +238,7 @@ template <int NPC, int ST>
 __global__ void __launch_bounds__(kWsThreads, 1)
     sketch_ws_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global, long long row0,
                      int l, uint64_t seed, long long rows_per_chunk, double* __restrict__ partial, int lp,
-                     int np_total, int check, int y0, DevStatus* st) {
+                     int np_total, int check, int y0, int tma3, DevStatus* st) {
   using S = WsShape<NPC, ST>;
   constexpr int LDO = kKS + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -292,9 +292,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       const long long kb = k_begin + (long long)stp * kKS;
       if (gt == 0) {
         mbar_expect_tx(&full[s], S::ATILE * 8);
+        if (tma3) {  // all NPC/16 column boxes in one 3-D load
+          tma_load_3d(sA + s * S::ATILE, &tma_a, 0, (int)kb, col0 / 16, &full[s]);
+        } else {
 #pragma unroll
-        for (int b = 0; b < NPC / 16; ++b)
-          tma_load_2d(sA + s * S::ATILE + b * (kKS * 16), &tma_a, col0 + 16 * b, (int)kb, &full[s]);
+          for (int b = 0; b < NPC / 16; ++b)
+            tma_load_2d(sA + s * S::ATILE + b * (kKS * 16), &tma_a, col0 + 16 * b, (int)kb, &full[s]);
+        }
       }
       double* Om = sO + s * S::OTILE;
 #pragma unroll
@@ -391,14 +395,19 @@ cudaError_t launch_ws(const SketchPlan& p, const double* a, long long lda, long 
                       uint64_t seed, double* partial, int check, const DevStatus* st, cudaStream_t s, int y0,
                       int y1) {
   CUtensorMap tm;
-  if (!make_tmap_2d(&tm, a, p.n, p.m_local, lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  static const bool no3d = std::getenv("CQR_SKETCH_TMA2D") != nullptr;  // tuning: per-box 2-D loads
+  const int tma3 = !no3d && p.n % 16 == 0 && p.np % NPC == 0 &&
+                   make_tmap_colblocks(&tm, a, p.n, p.m_local, lda, kKS, NPC / 16, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!tma3 && !make_tmap_2d(&tm, a, p.n, p.m_local, lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
   auto k = sketch_ws_kernel<NPC, ST>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsShape<NPC, ST>::SMEM);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NPC));
   k<<<grid, kWsThreads, WsShape<NPC, ST>::SMEM, s>>>(tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
-                                                      partial, p.lp, p.np, check, y0, const_cast<DevStatus*>(st));
+                                                      partial, p.lp, p.np, check, y0, tma3,
+                                                      const_cast<DevStatus*>(st));
   return cudaGetLastError();
 }
 

@@ -45,6 +45,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// global -> shared, 3-D box (c0 fastest)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 // shared -> global, bulk async-group completion
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -70,5 +78,10 @@ __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy
 // entry point is unavailable or the layout is not TMA-addressable.
 bool make_tmap_2d(CUtensorMap* map, const double* base, long long cols, long long rows, long long ld, int box_cols,
                   int box_rows, CUtensorMapSwizzle swizzle);
+// Host: the same matrix seen as (16 columns) x rows x (cols/16 column blocks), so that one 3-D box
+// {16, box_rows, box_blocks} lands as box_blocks consecutive 2-D {16, box_rows} boxes (one TMA
+// instruction instead of box_blocks). Requires cols % 16 == 0 (no column tail to zero-fill).
+bool make_tmap_colblocks(CUtensorMap* map, const double* base, long long cols, long long rows, long long ld,
+                         int box_rows, int box_blocks, CUtensorMapSwizzle swizzle);
 
 }  // namespace cqr
