@@ -13,6 +13,7 @@ import json
 import math
 import os
 
+import ctypes as C
 import numpy as np
 import pytest
 
@@ -385,6 +386,34 @@ def test_r_less_and_non_finite():
     for meth in (_abi.CHOLQR2, _abi.SCHOLQR3, _abi.RQR_GAUSSIAN, _abi.RLU, _abi.RQR):
         with pytest.raises(ValueError):
             G._factor(meth, c, G.SketchConfig(seed=3), _abi.options())
+
+
+def test_invalid_arguments_match_reference():
+    """engine.cpp:215-224 / errors.hpp:86-93: m < n, empty, p out of range and non-finite input are
+    invalid arguments on every method; ragged leading dimensions are rejected at the C-ABI."""
+    for shape in ((3, 5), (0, 4), (4, 0)):
+        a = np.ones(shape)
+        for meth in (_abi.CHOLQR, _abi.CHOLQR2, _abi.SCHOLQR3, _abi.RQR, _abi.RLU, _abi.RQR_GAUSSIAN):
+            with pytest.raises(ValueError):
+                G._factor(meth, a, G.SketchConfig(seed=1), _abi.options())
+    a = o.synthesize(500, 8, 1e3, 5)
+    for p in (0, 501):
+        with pytest.raises(ValueError):
+            G.run_parallel(_abi.CHOLQR2, a, p)
+    # lda < n, ldq < n through the C entry point itself
+    ctx = G.context()
+    q = np.empty_like(a)
+    r = np.empty((8, 8))
+    rep = _abi.Report()
+    lib = G._lib()
+    cfg, opt = _abi.sketch_cfg(seed=1), _abi.options()
+    for lda, ldq in ((7, 8), (8, 7)):
+        st = lib.cqr_factor(ctx.h, _abi.CHOLQR, G._ptr(a), 500, 8, lda, C.byref(cfg), C.byref(opt), G._ptr(q), ldq,
+                            G._ptr(r), 8, C.byref(rep))
+        assert st == 3 and rep.status == 3  # CQR_INVALID_ARGUMENT
+    # a valid call on the same context still works afterwards
+    f = G.cholesky_qr2(a)
+    assert o.orthogonality_error(f.q) <= 1e-13
 
 
 def test_diagnostics_cond_x():  # test_cholqr.cpp:154-171 (20 of the 100 trials)
