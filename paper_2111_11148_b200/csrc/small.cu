@@ -600,8 +600,7 @@ __global__ void __launch_bounds__(512) cholesky_blocked_kernel(const double* __r
                                                                double shift_value, double theory_coef,
                                                                double* shift_out, DevStatus* st) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double s_d, s_inv;
-  __shared__ int s_bad;
+  __shared__ double s_pd[kChPanel];  // the panel's pivots, stored after the panel
   if (failed(st)) return;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int ldp = n + 1;
@@ -625,24 +624,20 @@ __global__ void __launch_bounds__(512) cholesky_blocked_kernel(const double* __r
     for (int rr = warp; rr < w; rr += nw)
       for (int c = j0 + rr + lane; c < n; c += 32) Pn[rr * ldp + c] = S[(long long)(j0 + rr) * n + c];
     __syncthreads();
+    // Two barriers per step: every thread takes the pivot square root and RN(1/d) itself (no
+    // single-thread section and no barrier to publish them), divides its entry of row i, then
+    // the remaining panel rows are updated with the divided row. The pivots go to the diagonal
+    // once the panel is done.
     for (int ii = 0; ii < w; ++ii) {
       const int i = j0 + ii;
       double* Pi = Pn + ii * ldp;
-      if (tid == 0) {
-        const double sii = Pi[i];
-        if (!(sii > 0.0)) {
-          s_bad = 1;
-          set_status(st, 1 /*CQR_CHOLESKY_BREAKDOWN*/, i);
-        } else {
-          s_bad = 0;
-          s_d = sqrt(sii);
-          s_inv = 1.0 / s_d;
-          Pi[i] = s_d;
-        }
+      const double sii = Pi[i];
+      if (!(sii > 0.0)) {  // kernels.hpp:84 (NaN included); every thread sees the same sii
+        if (tid == 0) set_status(st, 1 /*CQR_CHOLESKY_BREAKDOWN*/, i);
+        return;
       }
-      __syncthreads();
-      if (s_bad) return;
-      const double d = s_d, inv = s_inv;
+      const double d = sqrt(sii), inv = __drcp_rn(d);
+      if (tid == 0) s_pd[ii] = d;  // the diagonal entry is stored after the panel (Pi[i] is still being read)
       for (int c = i + 1 + tid; c < n; c += nt) Pi[c] = div_rn(Pi[c], d, inv);
       __syncthreads();
       // update the remaining panel rows a in (i, j0+w), columns b >= a
@@ -654,6 +649,8 @@ __global__ void __launch_bounds__(512) cholesky_blocked_kernel(const double* __r
       }
       __syncthreads();
     }
+    if (tid < w) Pn[tid * ldp + j0 + tid] = s_pd[tid];
+    __syncthreads();
     // panel rows of R back to S
     for (int rr = warp; rr < w; rr += nw)
       for (int c = j0 + rr + lane; c < n; c += 32) S[(long long)(j0 + rr) * n + c] = Pn[rr * ldp + c];
