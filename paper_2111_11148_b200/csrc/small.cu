@@ -410,6 +410,10 @@ __device__ long long g_lu_trace[1024];
 #define CQR_LU_UNROLL 4
 #endif
 constexpr int kLuUnroll = CQR_LU_UNROLL;
+#ifndef CQR_LU_ROWTILES
+#define CQR_LU_ROWTILES 8
+#endif
+constexpr int kLuRowTilesMax = CQR_LU_ROWTILES;
 
 // l <= 512: one thread per physical row, the panel's 32 columns of that row in
 // registers. Rows never move: partial pivoting is tracked with logical
@@ -548,28 +552,45 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       }
       __syncthreads();
       LU_MARK(4 + 4 * (j0 / PW))
-      // A22 += (-L21) U12 on DMMA for the rows still unpivoted (k = pivots in order)
+      // A22 += (-L21) U12 on DMMA for the rows still unpivoted (k = pivots in order). A work item
+      // is one 8-column strip x kLuRowTiles row tiles: the strip's B fragments (U12) are loaded
+      // once, then every tile's loads are issued before the interleaved DMMA chains.
       const int q = lane & 3, gr = lane >> 2;
-      const int tr = (l + 7) / 8, tc = (n - c1 + 7) / 8;
-      for (int t = warp; t < tr * tc; t += NW) {
-        const int rt = t / tc, ct = t - (t / tc) * tc;
-        const int row = rt * 8 + gr, cc0 = c1 + ct * 8, col = cc0 + 2 * q;
-        const bool live = row < l && lpS[row] >= c1;
-        if (!__any_sync(0xffffffffu, live)) continue;
-        double c0v = (live && col < n) ? W[(long long)row * n + col] : 0.0;
-        double c1v = (live && col + 1 < n) ? W[(long long)row * n + col + 1] : 0.0;
-        double av[PW / 4], bv[PW / 4];
+      constexpr int kLuRowTiles = NW >= 16 ? 1 : kLuRowTilesMax;  // 512 threads: 128 registers
+      const int tr = (l + 7) / 8, tc = (n - c1 + 7) / 8, nrc = (tr + kLuRowTiles - 1) / kLuRowTiles;
+      for (int it = warp; it < tc * nrc; it += NW) {
+        const int ct = it % tc, rc = it / tc;
+        const int cc0 = c1 + ct * 8, col = cc0 + 2 * q, bc = cc0 + gr;
+        double bv[PW / 4];
 #pragma unroll
         for (int k4 = 0; k4 < PW / 4; ++k4) {
           const int kk = 4 * k4 + q;
-          av[k4] = (row < l && kk < w) ? -P[row * kLuLdp + kk] : 0.0;  // A: row gr, k = q
-          const int bc = cc0 + gr;
           bv[k4] = (kk < w && bc < n) ? u[(long long)(j0 + kk) * n + bc] : 0.0;  // B: k = q, col = gr
         }
+        double c0v[kLuRowTiles], c1v[kLuRowTiles], av[kLuRowTiles][PW / 4];
+        bool live[kLuRowTiles];
+        int row[kLuRowTiles];
 #pragma unroll
-        for (int k4 = 0; k4 < PW / 4; ++k4) dmma(c0v, c1v, av[k4], bv[k4]);
-        if (live && col < n) W[(long long)row * n + col] = c0v;
-        if (live && col + 1 < n) W[(long long)row * n + col + 1] = c1v;
+        for (int r = 0; r < kLuRowTiles; ++r) {
+          row[r] = (rc * kLuRowTiles + r) * 8 + gr;
+          live[r] = row[r] < l && lpS[row[r]] >= c1;
+          c0v[r] = (live[r] && col < n) ? W[(long long)row[r] * n + col] : 0.0;
+          c1v[r] = (live[r] && col + 1 < n) ? W[(long long)row[r] * n + col + 1] : 0.0;
+#pragma unroll
+          for (int k4 = 0; k4 < PW / 4; ++k4) {
+            const int kk = 4 * k4 + q;
+            av[r][k4] = (row[r] < l && kk < w) ? -P[row[r] * kLuLdp + kk] : 0.0;  // A: row gr, k = q
+          }
+        }
+#pragma unroll
+        for (int k4 = 0; k4 < PW / 4; ++k4)
+#pragma unroll
+          for (int r = 0; r < kLuRowTiles; ++r) dmma(c0v[r], c1v[r], av[r][k4], bv[k4]);
+#pragma unroll
+        for (int r = 0; r < kLuRowTiles; ++r) {
+          if (live[r] && col < n) W[(long long)row[r] * n + col] = c0v[r];
+          if (live[r] && col + 1 < n) W[(long long)row[r] * n + col + 1] = c1v[r];
+        }
       }
     }
     __syncthreads();
