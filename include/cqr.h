@@ -243,6 +243,34 @@ int64_t cqr_block_offset(int64_t m, int p, int b);
 int cqr_comm_model(int method, int p, int64_t n, int64_t l, int* rounds_min, int* rounds_max,
                    double* volume_min, double* volume_max);
 
+/* Sharded Gram whose result does not depend on the rank count (the reference's
+ * parallel_gram splits global 1024-row leaves over workers and combines them in one
+ * fixed tree, engine.cpp:24-39; test_parexec.cpp:47-56 asserts bitwise identity
+ * across p). Rank b of p owns rows [row0, row1) = parexec.cpp:13-15; a leaf
+ * straddling a block boundary is one fma chain continued across ranks (head: from
+ * rank b-1, tail: to rank b+1, span: both, inside one leaf); owned leaves [lo, hi)
+ * are combined into the pairwise-tree nodes listed; every rank all-gathers the nodes
+ * and evaluates the rest of the tree. Used by every multi-rank factorization whose
+ * shards are the standard partition. Host-only (no GPU needed). */
+typedef struct {
+  int64_t row0, row1;
+  int head, tail, span;
+  int64_t head_end, tail_start; /* head rows [row0, head_end), tail rows [tail_start, row1) */
+  int64_t full0, full1;         /* rows of the leaves complete on this rank */
+  int64_t lo, hi;               /* owned global leaves */
+  int nodes;
+  int64_t node_start[64], node_count[64];
+} cqr_gram_shard;
+int cqr_gram_shard_plan(int64_t m, int p, int b, cqr_gram_shard* out);
+/* Postfix program of the tree top over gathered slots b*K + k (op -1 = left + right).
+ * Returns its length (negative: -length when cap is too small); *slots_per_rank = K. */
+int cqr_gram_tree_program(int64_t m, int p, int* prog, int cap, int* slots_per_rank);
+/* The p-rank protocol run rank by rank on this one device (the exchanges become
+ * device copies): G of the device matrix x (m x n) as p ranks would compute it.
+ * Test entry for the multi-rank arithmetic on a one-GPU box. */
+int cqr_gram_sharded_sim(cqr_ctx* ctx, const double* x, int64_t m, int64_t n, int64_t ldx, int p,
+                         double* g_dev);
+
 /* Number of kernels this library launched since the context was created
  * (evidence for the bench's gpu_launches count). */
 int64_t cqr_launch_count(const cqr_ctx* ctx);

@@ -1007,6 +1007,20 @@ int orc_gram(const double* x, int64_t m, int64_t n, int64_t ldx, int workers, do
   return guarded([&] { store(gram(x, m, n, ldx, workers), g); });
 }
 
+// One leaf chain continued over `rows` rows from init (n x n, upper used; NULL = +0):
+// the part of a 1024-row leaf (kernels.hpp:28-38) that one row block holds.
+void orc_gram_chain(const double* x, int64_t ldx, int64_t rows, int64_t n, const double* init, double* out) {
+  if (init)
+    std::memcpy(out, init, sizeof(double) * static_cast<size_t>(n * n));
+  else
+    std::fill(out, out + n * n, 0.0);
+  for (int64_t k = 0; k < rows; ++k) {
+    const double* xr = x + k * ldx;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = i; j < n; ++j) out[i * n + j] = std::fma(xr[i], xr[j], out[i * n + j]);
+  }
+}
+
 void orc_gram_tree_combine(double* slots, int64_t count, int64_t len, double* out) {
   std::vector<double> s(slots, slots + count * len);
   gram_tree_combine(s, count, len);

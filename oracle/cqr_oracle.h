@@ -57,6 +57,7 @@ int orc_sketch_gaussian_shard(const double* a, int64_t m_local, int64_t m_global
 int orc_gram(const double* x, int64_t m, int64_t n, int64_t ldx, int workers, double* g);
 /* Leaf partials + tree, exposed so the tree rule can be tested alone. */
 void orc_gram_tree_combine(double* slots, int64_t count, int64_t len, double* out);
+void orc_gram_chain(const double* x, int64_t ldx, int64_t rows, int64_t n, const double* init, double* out);
 void orc_gram_stack_combine(const double* slots, int64_t count, int64_t len, double* out);
 int orc_cholesky_upper(const double* g, int64_t n, double* r, int64_t* pivot);
 int orc_trisolve_inplace(double* x, int64_t m, int64_t n, int64_t ldx, const double* r,

@@ -46,6 +46,7 @@ def lib():
             "orc_sketch_gaussian_shard": (i32, [pd, i64, i64, i64, i64, i64, u64, pd]),
             "orc_gram": (i32, [pd, i64, i64, i64, i32, pd]),
             "orc_gram_tree_combine": (None, [pd, i64, i64, pd]),
+            "orc_gram_chain": (None, [pd, i64, i64, i64, pd, pd]),
             "orc_gram_stack_combine": (None, [pd, i64, i64, pd]),
             "orc_cholesky_upper": (i32, [pd, i64, pd, pi64]),
             "orc_trisolve_inplace": (i32, [pd, i64, i64, i64, pd, i32, pi64]),
@@ -182,6 +183,16 @@ def gram(x, workers=1):
     g = np.empty((n, n))
     _check(lib().orc_gram(_pd(x), m, n, n, workers, _pd(g)))
     return g
+
+
+def gram_chain(x, init=None):
+    """fma chain over the rows of x continued from init (upper triangle, +0 if None)."""
+    x = _f64(x)
+    rows, n = x.shape
+    out = np.zeros((n, n))
+    ip = _pd(_f64(init)) if init is not None else None
+    lib().orc_gram_chain(_pd(x), n, rows, n, ip, _pd(out))
+    return out
 
 
 def tree_combine(slots):

@@ -75,6 +75,19 @@ class Report(C.Structure):
     ]
 
 
+class GramShard(C.Structure):
+    """cqr_gram_shard: rank b's part of the rank-count-independent Gram."""
+    _fields_ = [
+        ("row0", C.c_int64), ("row1", C.c_int64),
+        ("head", C.c_int32), ("tail", C.c_int32), ("span", C.c_int32),
+        ("head_end", C.c_int64), ("tail_start", C.c_int64),
+        ("full0", C.c_int64), ("full1", C.c_int64),
+        ("lo", C.c_int64), ("hi", C.c_int64),
+        ("nodes", C.c_int32),
+        ("node_start", C.c_int64 * 64), ("node_count", C.c_int64 * 64),
+    ]
+
+
 PRECOND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_int64,
                          C.POINTER(C.c_double), C.POINTER(C.c_int64))
 

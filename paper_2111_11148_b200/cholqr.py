@@ -195,6 +195,9 @@ def _lib():
                                          P(_abi.Options), vp, i64, vp, i64, P(_abi.Report)]),
             "cqr_gram": (i32, [vp, vp, i64, i64, i64, vp]),
             "cqr_gram_dev": (i32, [vp, vp, i64, i64, i64, vp]),
+            "cqr_gram_sharded_sim": (i32, [vp, vp, i64, i64, i64, i32, vp]),
+            "cqr_gram_shard_plan": (i32, [i64, i32, i32, P(_abi.GramShard)]),
+            "cqr_gram_tree_program": (i32, [i64, i32, P(C.c_int), i32, P(C.c_int)]),
             "cqr_cholesky_upper": (i32, [vp, vp, i64, vp, pi64]),
             "cqr_trisolve_inplace": (i32, [vp, vp, i64, i64, i64, vp, pi64]),
             "cqr_trisolve_inplace_dev": (i32, [vp, vp, i64, i64, i64, vp, pi64]),
@@ -505,6 +508,20 @@ def gram(x, ctx=None):
         raise ValueError("gram: matrix must have rows >= cols")
     g = np.empty((n, n))
     ctx._check(_lib().cqr_gram(ctx.h, _ptr(x), m, n, n, _ptr(g)))
+    return g
+
+
+def gram_sharded_sim(x, p, ctx=None):
+    """G of a CUDA matrix as p ranks of the rank-count-independent sharded Gram
+    compute it (cqr_gram_sharded_sim: the multi-rank protocol on one device)."""
+    import torch
+
+    ctx = ctx or context(x.device.index)
+    m, n = x.shape
+    g = torch.empty((n, n), dtype=torch.float64, device=x.device)
+    torch.cuda.current_stream(x.device).synchronize()
+    ctx._check(_lib().cqr_gram_sharded_sim(ctx.h, C.c_void_p(x.data_ptr()), m, n, x.stride(0), p,
+                                            C.c_void_p(g.data_ptr())))
     return g
 
 

@@ -23,6 +23,7 @@
 
 #include "../../include/cqr.h"
 #include "common.cuh"
+#include "gram_shard.h"
 #include "kernels.h"
 
 using cqr::DevStatus;
@@ -48,7 +49,7 @@ struct cqr_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   std::string err;
-  DevBuf bufs[24];
+  DevBuf bufs[32];
   DevStatus* status = nullptr;   // device
   DevStatus* status_h = nullptr;  // pinned host
   double* scal_h = nullptr;       // pinned host scalars
@@ -68,7 +69,7 @@ namespace {
 
 enum BufId {
   B_A1 = 0, B_SKPART, B_GPART, B_GTILES, B_G, B_RT, B_RH, B_R, B_RTMP, B_SGN, B_PACK1, B_PACK2, B_WORK,
-  B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X, B_SYN, B_SYNV
+  B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X, B_SYN, B_SYNV, B_SHPART, B_SHSLOT, B_SHALL, B_SHTAB, B_SHHT
 };
 
 struct Fail {
@@ -253,6 +254,7 @@ struct Job {
   long long ldq_host = 0;
   std::vector<long long> bounds;  // chunk row boundaries, bounds.front() = 0, bounds.back() = m
   int waited = 0;                 // H2D chunks the compute stream already waits on
+  int det = 0;  // every rank holds its standard row block: the rank-count-independent Gram (gram_shard.cu)
 };
 
 bool pipelined(const Job& j) { return j.a_host != nullptr; }
@@ -272,11 +274,7 @@ void allreduce(cqr_ctx* c, double* p, size_t count) {
   ckn(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->comm, c->stream), "ncclAllReduce");
 }
 
-// Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
-void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g, int check = 0,
-              Job* pj = nullptr) {
-  cqr::GramPlan p = cqr::gram_plan(m, n, cqr::gram_tma_ok(x, ldx, m, n));
-  double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.workspace_doubles, 1));
+const int32_t* gram_tiles_dev(cqr_ctx* c, const cqr::GramPlan& p) {
   int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
   const int key = p.np * 1000000 + p.wpc * 10000 + p.parts * 100 + p.maxt + (p.tma ? 5000 : 0);
   if (c->tiles_key != key) {  // the table depends on (np, parts, maxt) only: upload once
@@ -286,6 +284,141 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
     ck(cudaMemcpy(tiles, ht.data(), p.tiles_bytes, cudaMemcpyHostToDevice), "tiles H2D");
     c->tiles_key = key;
   }
+  return tiles;
+}
+
+// ---- rank-count-independent sharded Gram (gram_shard.cu) ------------------------------
+struct ShardWs {
+  double *part, *gsum, *slots, *all, *ht;  // ht: 3 np x np chain buffers (head in, tail out, spare)
+  int* tab;
+  int np, K;
+};
+
+ShardWs shard_ws(cqr_ctx* c, long long m, int p, int n, int K) {
+  ShardWs w;
+  w.np = cqr::gram_plan(1024, n).np;
+  w.K = K;
+  long long owned = 0;
+  for (int b = 0; b < p; ++b) {
+    const cqr::ShardGram g = cqr::shard_gram_plan(m, p, b);
+    owned = std::max(owned, g.hi - g.lo);
+  }
+  const size_t np2 = (size_t)w.np * w.np;
+  const size_t groups = (size_t)(owned + 15) / 16 + (size_t)K;
+  w.part = dbuf<double>(c, B_SHPART, (size_t)(owned + 1) * np2 + groups * np2);
+  w.gsum = w.part + (size_t)(owned + 1) * np2;
+  w.slots = dbuf<double>(c, B_SHSLOT, (size_t)K * n * n);
+  w.all = dbuf<double>(c, B_SHALL, (size_t)p * K * n * n);
+  w.ht = dbuf<double>(c, B_SHHT, 3 * np2);
+  w.tab = dbuf<int>(c, B_SHTAB, 65536);
+  return w;
+}
+
+// tail rows -> out (a chain from +0), unless the rank lies inside one leaf
+void shard_tail(cqr_ctx* c, const cqr::ShardGram& sg, const double* x, long long ldx, int n, int np, double* out,
+                int check) {
+  if (sg.tail && !sg.span)
+    LAUNCH(c, cqr::launch_gram_chain(x + (sg.tail_start - sg.r0) * ldx, ldx, sg.r1 - sg.tail_start, n, np, nullptr,
+                                     out, check, c->status, c->stream));
+}
+
+// the head chain (continued from head_in), the complete leaves, and the owned nodes -> slots
+void shard_body(cqr_ctx* c, const cqr::ShardGram& sg, const double* x, long long ldx, int n, const ShardWs& w,
+                const double* head_in, double* span_out, double* slots, int check) {
+  const size_t np2 = (size_t)w.np * w.np;
+  if (sg.span) {
+    LAUNCH(c, cqr::launch_gram_chain(x, ldx, sg.r1 - sg.r0, n, w.np, head_in, span_out, check, c->status,
+                                     c->stream));
+    return;
+  }
+  if (sg.head)
+    LAUNCH(c, cqr::launch_gram_chain(x, ldx, sg.head_end - sg.r0, n, w.np, head_in, w.part, check, c->status,
+                                     c->stream));
+  if (sg.full1 > sg.full0) {
+    const double* xf = x + (sg.full0 - sg.r0) * ldx;
+    const long long mf = sg.full1 - sg.full0;
+    cqr::GramPlan p = cqr::gram_plan(mf, n, cqr::gram_tma_ok(xf, ldx, mf, n));
+    const int32_t* tiles = gram_tiles_dev(c, p);
+    LAUNCH(c, cqr::launch_gram_leaves(p, xf, ldx, tiles, w.part + (sg.head ? np2 : 0), vec_ok(xf, ldx, n) ? 1 : 0,
+                                      check, c->status, c->stream, 0, -1, c->num_sms));
+  }
+  std::vector<int> ta, tb;
+  const int groups = (int)cqr::gram_nodes_tables(sg, ta, tb);
+  const int nodes = (int)tb.size() / 3;
+  if (nodes == 0) return;
+  ta.insert(ta.end(), tb.begin(), tb.end());
+  if (ta.size() > 65536) throw Fail{CQR_INVALID_ARGUMENT, -1, "sharded Gram: node table too large"};
+  ck(cudaMemcpyAsync(w.tab, ta.data(), ta.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "node table");
+  LAUNCH(c, cqr::launch_gram_nodes(w.part, w.np, n, w.tab, groups, w.tab + 2 * groups, nodes, w.gsum, slots,
+                                   c->status, c->stream));
+}
+
+void shard_top(cqr_ctx* c, long long m, int p, int n, const ShardWs& w, double* g) {
+  int K = 0;
+  const std::vector<int> prog = cqr::tree_program(m, p, &K);
+  if (prog.size() > 65536) throw Fail{CQR_INVALID_ARGUMENT, -1, "sharded Gram: program too large"};
+  ck(cudaMemcpyAsync(w.tab, prog.data(), prog.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "program");
+  LAUNCH(c, cqr::launch_gram_program(w.all, n, w.tab, (int)prog.size(), g, c->status, c->stream));
+}
+
+int shard_slots(long long m, int p) {
+  int K = 0;
+  cqr::tree_program(m, p, &K);
+  return K;
+}
+
+// This rank's part over NCCL: tails to the next rank, heads from the previous, nodes all-gathered.
+void gram_det(cqr_ctx* c, const double* x, long long ldx, int n, long long m, double* g, int check) {
+  const int p = c->world, b = c->rank;
+  const cqr::ShardGram sg = cqr::shard_gram_plan(m, p, b);
+  const int K = shard_slots(m, p);
+  ShardWs w = shard_ws(c, m, p, n, K);
+  const size_t np2 = (size_t)w.np * w.np;
+  double* head_in = w.ht;
+  double* tail_out = w.ht + np2;
+  shard_tail(c, sg, x, ldx, n, w.np, tail_out, check);
+  ckn(ncclGroupStart(), "group");
+  if (sg.tail && !sg.span) ckn(ncclSend(tail_out, np2, ncclDouble, b + 1, c->comm, c->stream), "send tail");
+  if (sg.head) ckn(ncclRecv(head_in, np2, ncclDouble, b - 1, c->comm, c->stream), "recv head");
+  ckn(ncclGroupEnd(), "group");
+  ck(cudaMemsetAsync(w.slots, 0, sizeof(double) * K * n * n, c->stream), "slots");
+  shard_body(c, sg, x, ldx, n, w, head_in, tail_out, w.slots, check);
+  if (sg.span) ckn(ncclSend(tail_out, np2, ncclDouble, b + 1, c->comm, c->stream), "forward span");
+  ckn(ncclAllGather(w.slots, w.all, (size_t)K * n * n, ncclDouble, c->comm, c->stream), "allgather nodes");
+  shard_top(c, m, p, n, w, g);
+}
+
+// The same protocol for p virtual ranks on this device, rank after rank (the
+// exchanges become buffer hand-offs): cqr_gram_sharded_sim.
+void gram_det_sim(cqr_ctx* c, const double* x, long long ldx, int n, long long m, int p, double* g) {
+  const int K = shard_slots(m, p);
+  ShardWs w = shard_ws(c, m, p, n, K);
+  const size_t np2 = (size_t)w.np * w.np;
+  ck(cudaMemsetAsync(w.all, 0, sizeof(double) * p * K * n * n, c->stream), "slots");
+  int cur = 0;  // w.ht + cur*np2: the chain arriving from the previous rank
+  for (int b = 0; b < p; ++b) {
+    const cqr::ShardGram sg = cqr::shard_gram_plan(m, p, b);
+    const double* xb = x + sg.r0 * ldx;
+    double* in = w.ht + cur * np2;
+    double* out = w.ht + ((cur + 1) % 3) * np2;
+    shard_tail(c, sg, xb, ldx, n, w.np, out, 1);
+    shard_body(c, sg, xb, ldx, n, w, in, out, w.all + (size_t)b * K * n * n, 1);
+    cur = (cur + 1) % 3;
+  }
+  shard_top(c, m, p, n, w, g);
+}
+
+// Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
+void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g, int check = 0,
+              Job* pj = nullptr) {
+  if (pj && pj->det && c->comm && !c->local_only) {
+    wait_all(*pj);
+    gram_det(c, x, ldx, n, pj->m_global, g, check);
+    return;
+  }
+  cqr::GramPlan p = cqr::gram_plan(m, n, cqr::gram_tma_ok(x, ldx, m, n));
+  double* part = dbuf<double>(c, B_GPART, std::max<size_t>(p.workspace_doubles, 1));
+  const int32_t* tiles = gram_tiles_dev(c, p);
   if (m > 0) {
     if (pj && pipelined(*pj) && pj->waited + 1 < (int)pj->bounds.size()) {
       // leaves as their rows land (whole leaves per launch: the partials are per leaf, so identical)
@@ -734,15 +867,19 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     }
     if (c->comm) {  // every rank takes the same path
       DevStatus s0 = read_status(c);
-      int bad = s0.code != 0;
+      // flags[1]: this rank's rows are not its standard block (parexec.cpp:13-15); then
+      // every rank sums plain Gram partials instead of the rank-count-independent tree
+      int flags[2] = {s0.code != 0, j.row0 != cqr::shard_offset(j.m_global, c->world, c->rank) ||
+                                        j.row0 + j.m_local != cqr::shard_offset(j.m_global, c->world, c->rank + 1)};
       {
-        int* flag = dbuf<int>(c, B_DIAG, 1);
-        ck(cudaMemcpyAsync(flag, &bad, sizeof(int), cudaMemcpyHostToDevice, c->stream), "flag");
-        ckn(ncclAllReduce(flag, flag, 1, ncclInt, ncclMax, c->comm, c->stream), "allreduce flag");
-        ck(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "flag");
+        int* flag = dbuf<int>(c, B_DIAG, 2);
+        ck(cudaMemcpyAsync(flag, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream), "flag");
+        ckn(ncclAllReduce(flag, flag, 2, ncclInt, ncclMax, c->comm, c->stream), "allreduce flag");
+        ck(cudaMemcpyAsync(flags, flag, sizeof(flags), cudaMemcpyDeviceToHost, c->stream), "flag");
         ck(cudaStreamSynchronize(c->stream), "sync");
       }
-      if (bad) throw Fail{CQR_INVALID_ARGUMENT, -1, "A has non-finite entries"};
+      if (flags[0]) throw Fail{CQR_INVALID_ARGUMENT, -1, "A has non-finite entries"};
+      j.det = flags[1] ? 0 : 1;
     }
     switch (j.method) {
       case CQR_CHOLQR:
@@ -997,6 +1134,17 @@ int cqr_gram_dev(cqr_ctx* c, const double* x, int64_t m, int64_t n, int64_t ldx,
     reset_status(c);
     gram_dev(c, x, m, (int)n, ldx, g);
     ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int cqr_gram_sharded_sim(cqr_ctx* c, const double* x, int64_t m, int64_t n, int64_t ldx, int p, double* g) {
+  if (!c || m < n || n < 1 || ldx < n || n > 512 || p < 1 || p > m) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    reset_status(c);
+    gram_det_sim(c, x, ldx, (int)n, m, p, g);
+    DevStatus s = read_status(c);
+    if (s.code) throw Fail{s.code, s.index, status_msg(s.code)};
   });
 }
 

@@ -2,9 +2,12 @@
 parexec (parexec.hpp:11-57, simulated there with threads) on real GPUs.
 
 Rank b owns rows [ceil(b*m/p), ceil((b+1)*m/p)) of the global m x n matrix
-(parexec.cpp:13-15). The library sums the s x n sketch partials and the n x n
-Gram partials with NCCL all-reduce (its own communicator, created from a
-unique id that rank 0 broadcasts through torch.distributed), runs the small
+(parexec.cpp:13-15). The library sums the s x n sketch partials with NCCL
+all-reduce (its own communicator, created from a unique id that rank 0
+broadcasts through torch.distributed), forms the n x n Gram with the
+rank-count-independent protocol of csrc/gram_shard.cu (leaf chains continued
+across block boundaries, tree nodes all-gathered: bitwise equal to one GPU for
+any p, as the reference's parallel Gram, engine.cpp:24-39), runs the small
 factorizations redundantly on every rank (identical inputs give identical R,
 so no broadcast and no collective for the retry decision), and leaves Q
 row-sharded. torch.distributed is only the plumbing (id exchange, barriers).
@@ -23,6 +26,29 @@ def shard_rows(m: int, p: int, b: int):
     """(row0, rows) of block b (parexec.cpp:9-18)."""
     lo, hi = cq.block_offset(m, p, b), cq.block_offset(m, p, b + 1)
     return lo, hi - lo
+
+
+def gram_shard_plan(m: int, p: int, b: int) -> dict:
+    """Rank b's part of the rank-count-independent Gram (cqr_gram_shard_plan):
+    head/tail/span chains across block boundaries, complete leaves, owned leaves
+    and the tree nodes they are combined into."""
+    s = _abi.GramShard()
+    if cq._lib().cqr_gram_shard_plan(m, p, b, C.byref(s)) != 0:
+        raise ValueError("cqr_gram_shard_plan: bad arguments")
+    out = {k: getattr(s, k) for k, _ in _abi.GramShard._fields_ if not k.startswith("node_")}
+    for k in ("head", "tail", "span"):
+        out[k] = bool(out[k])
+    out["node_list"] = [(s.node_start[k], s.node_count[k]) for k in range(s.nodes)]
+    return out
+
+
+def gram_tree_program(m: int, p: int):
+    """(program, K): postfix ops over gathered slots b*K + k, -1 = left + right."""
+    K = C.c_int()
+    need = -cq._lib().cqr_gram_tree_program(m, p, None, 0, C.byref(K))
+    buf = (C.c_int * max(need, 1))()
+    ln = cq._lib().cqr_gram_tree_program(m, p, buf, need, C.byref(K))
+    return list(buf[:ln]), K.value
 
 
 def make_context(device: int, rank: int | None = None, world: int | None = None):

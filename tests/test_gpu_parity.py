@@ -129,6 +129,25 @@ def test_gram_bitwise(m, n, seed):
     assert np.array_equal(g, g.T)
 
 
+@pytest.mark.parametrize("m,n,p,ld", [(5003, 12, 3, 12), (3000, 6, 8, 6), (100_000, 128, 8, 128),
+                                      (1_000_003, 64, 7, 64), (50_000, 256, 5, 256), (20000, 33, 4, 40),
+                                      (9000, 200, 2, 200), (2048, 16, 2, 16), (300_000, 128, 3, 130)])
+def test_sharded_gram_sim_bitwise_for_any_p(m, n, p, ld):
+    # the multi-rank Gram protocol (head/tail chains across block boundaries, owned
+    # tree nodes, all-gathered top of the tree) run rank by rank on this device:
+    # bit-identical to the one-GPU Gram and to the oracle for every p, as the
+    # reference's parallel Gram is (test_parexec.cpp:47-56)
+    import torch
+
+    full = torch.as_tensor(o.gaussian_matrix(m, ld, 40 + p), device="cuda")
+    x = full[:, :n]
+    one = G.gram(x)
+    for q in sorted({1, 2, p}):
+        assert torch.equal(G.gram_sharded_sim(x, q), one), q
+    if m * n <= 2e7:
+        assert np.array_equal(one.cpu().numpy(), o.gram(x.cpu().numpy()))
+
+
 def test_gram_known_answers():
     assert np.array_equal(G.gram(np.eye(3)), np.eye(3))
     assert G.gram(np.array([[1.0], [2.0], [2.0]]))[0, 0] == 9.0
