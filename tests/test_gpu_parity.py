@@ -321,7 +321,10 @@ def test_breakdowns_match():
 
 @pytest.mark.parametrize("m,n,kappa,l,seed", [(400, 16, 1.0, 32, 17), (500, 15, 1e8, 30, 26),
                                               (20000, 50, 1e12, 100, 20), (20000, 50, 1e15, 100, 21),
-                                              (100000, 64, 1e10, 128, 1)])
+                                              (100000, 64, 1e10, 128, 1),
+                                              # n in (64, 128]: the solve fused with the Gram leaves
+                                              (200_000, 128, 1e12, 256, 2), (5000, 100, 1e8, 200, 3),
+                                              (3000, 65, 1e6, 130, 4), (160_000 + 37, 96, 1e14, 192, 5)])
 def test_rlu_uniform_bitwise(m, n, kappa, l, seed):
     a = o.synthesize(m, n, kappa, seed) if kappa > 1 else o.random_orthogonal(m, n, seed)
     ref = o.factor(_abi.RLU, a, _abi.sketch_cfg(size=l, seed=seed + 1))
