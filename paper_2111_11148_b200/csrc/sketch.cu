@@ -214,7 +214,26 @@ constexpr int kWsIlp = CQR_WS_ILP;
 #define CQR_WS_MMA 8
 #endif
 constexpr int kWsMma = CQR_WS_MMA;
-constexpr int kWsThreads = (kWsGen + kWsMma) * 32;
+// n <= 64 (NPC = 64: each drawn entry feeds only 64 columns) draws with 16 generator warps,
+// 2 pairs side by side (c3 shape: 0.923 -> 0.850 ms at m = 1e6); wider A keeps 8 x 4.
+#ifndef CQR_WS_GEN64
+#define CQR_WS_GEN64 16
+#endif
+#ifndef CQR_WS_ILP64
+#define CQR_WS_ILP64 2
+#endif
+template <int NPC>
+constexpr int ws_gen() {
+  return NPC == 64 ? CQR_WS_GEN64 : kWsGen;
+}
+template <int NPC>
+constexpr int ws_ilp() {
+  return NPC == 64 ? CQR_WS_ILP64 : kWsIlp;
+}
+template <int NPC>
+constexpr int ws_threads() {
+  return (ws_gen<NPC>() + kWsMma) * 32;
+}
 
 // NPC columns of A per CTA (128, or 256 for wider A with 32 Omega rows per CTA so
 // that each drawn Omega entry feeds twice the DMMA work), ST Omega rows per CTA.
@@ -229,13 +248,14 @@ struct WsShape {
   static constexpr int OTILE = ST * (kKS + 4);  // doubles per Omega stage (stride 36)
   static constexpr int NGW = NPC / (8 * kWsMma);  // 8-column groups per MMA warp
   static constexpr int MGW = ST / 8;            // 8-row groups per MMA warp
-  static constexpr int PAIRS = ST * kKS / 2 / (kWsGen * 32);  // Box-Muller pairs per generator thread per step
-  static constexpr int ILP = PAIRS < kWsIlp ? PAIRS : kWsIlp;  // pairs drawn side by side
+  static constexpr int GEN = ws_gen<NPC>();
+  static constexpr int PAIRS = ST * kKS / 2 / (GEN * 32);  // Box-Muller pairs per generator thread per step
+  static constexpr int ILP = PAIRS < ws_ilp<NPC>() ? PAIRS : ws_ilp<NPC>();  // pairs drawn side by side
   static constexpr size_t SMEM = (size_t)kWsStages * (ATILE + OTILE) * sizeof(double) + 1024;
 };
 
 template <int NPC, int ST>
-__global__ void __launch_bounds__(kWsThreads, 1)
+__global__ void __launch_bounds__(ws_threads<NPC>(), 1)
     sketch_ws_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global, long long row0,
                      int l, uint64_t seed, long long rows_per_chunk, double* __restrict__ partial, int lp,
                      int np_total, int check, int y0, int tma3, DevStatus* st) {
@@ -258,11 +278,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   {
     const double* src = reinterpret_cast<const double*>(&c_bm);
     double* dst = reinterpret_cast<double*>(&T);
-    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += kWsThreads) dst[e] = src[e];
+    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += ws_threads<NPC>()) dst[e] = src[e];
   }
   if (tid == 0) {
     for (int s = 0; s < kWsStages; ++s) {
-      mbar_init(&full[s], kWsGen * 32 + 1);  // every generator thread + the TMA issuer's expect_tx
+      mbar_init(&full[s], S::GEN * 32 + 1);  // every generator thread + the TMA issuer's expect_tx
       mbar_init(&empty[s], kWsMma);          // one elected lane per MMA warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -279,7 +299,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     uint64_t z[S::PAIRS];
 #pragma unroll
     for (int u = 0; u < S::PAIRS; ++u) {
-      const int e = gt + kWsGen * 32 * u;
+      const int e = gt + S::GEN * 32 * u;
       const unsigned long long c0 = (unsigned long long)(s0 + (e >> 4)) * (unsigned long long)m_global + row0 + k_begin;
       z[u] = seed + (2 * ((c0 >> 1) + (e & 15)) + 1) * kGolden;
     }
@@ -318,7 +338,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #endif
 #pragma unroll
         for (int j = 0; j < S::ILP; ++j) {
-          const int e = gt + kWsGen * 32 * (u0 + j);
+          const int e = gt + S::GEN * 32 * (u0 + j);
           const int i = e >> 4, pp = e & 15;
           if (!all_live && s0 + i >= l) ge[j] = go[j] = 0.0;  // Omega rows past l (last s-tile only)
           *reinterpret_cast<double2*>(Om + i * LDO + 2 * pp) = make_double2(ge[j], go[j]);
@@ -405,7 +425,7 @@ cudaError_t launch_ws(const SketchPlan& p, const double* a, long long lda, long 
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsShape<NPC, ST>::SMEM);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NPC));
-  k<<<grid, kWsThreads, WsShape<NPC, ST>::SMEM, s>>>(tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
+  k<<<grid, ws_threads<NPC>(), WsShape<NPC, ST>::SMEM, s>>>(tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
                                                       partial, p.lp, p.np, check, y0, tma3,
                                                       const_cast<DevStatus*>(st));
   return cudaGetLastError();
