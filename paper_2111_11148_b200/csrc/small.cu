@@ -407,13 +407,17 @@ __device__ long long g_lu_trace[1024];
   {}
 #endif
 #ifndef CQR_LU_UNROLL
-#define CQR_LU_UNROLL 4
+#define CQR_LU_UNROLL 16
 #endif
 constexpr int kLuUnroll = CQR_LU_UNROLL;
 #ifndef CQR_LU_ROWTILES
 #define CQR_LU_ROWTILES 8
 #endif
 constexpr int kLuRowTilesMax = CQR_LU_ROWTILES;
+#ifndef CQR_LU_ROT_PANEL
+#define CQR_LU_ROT_PANEL 16
+#endif
+constexpr int kLuRotPanel = CQR_LU_ROT_PANEL;  // panel width of lu_rot_kernel
 
 // l <= 512: one thread per physical row, the panel's 32 columns of that row in
 // registers. Rows never move: partial pivoting is tracked with logical
@@ -1072,9 +1076,9 @@ cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work,
   if (!legacy && l <= 512 && (size_t)l * kLuLdp * sizeof(double) + (size_t)l * sizeof(int) <= 220 * 1024) {
     // as few warps as rows need: the per-step barriers and arg-max dominate (8 vs 16 warps at
     // l = 256: 276 vs 332 us)
-    if (l <= 128) return launch_lu_rot<4, kLuPanel>(a1, l, n, u, work, st, s);
-    if (l <= 256) return launch_lu_rot<8, kLuPanel>(a1, l, n, u, work, st, s);
-    return launch_lu_rot<16, kLuPanel>(a1, l, n, u, work, st, s);
+    if (l <= 128) return launch_lu_rot<4, kLuRotPanel>(a1, l, n, u, work, st, s);
+    if (l <= 256) return launch_lu_rot<8, kLuRotPanel>(a1, l, n, u, work, st, s);
+    return launch_lu_rot<16, kLuRotPanel>(a1, l, n, u, work, st, s);
   }
   // taller sketches (c4: 768 x 512) keep the swapping kernel: 24 warps x 16-column panels measured slower
   // (6.08 vs 4.95 ms)

@@ -1,0 +1,7 @@
+# LU panel-width variants: parity (LU / rLU bitwise tests) and the c1 precondition stage
+for v in ${LIBS:-default}; do
+  if [ "$v" = default ]; then unset CQR_LIB; else export CQR_LIB=tools/gpu/libcqr_$v.so; fi
+  r=$(timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "lu_bitwise or rlu_uniform or singular or pivot" 2>&1 | tail -1)
+  s=$(PROF_REPS=6 timeout 120 python tools/prof_c1.py 2>&1 | tail -1)
+  echo "$v | $r | $s"
+done
