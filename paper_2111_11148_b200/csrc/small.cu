@@ -618,9 +618,16 @@ cudaError_t launch_lu_rot(const double* a1, int l, int n, double* u, double* wor
 // upper triangle gets s(a,b) += sum_i (-r(i,a)) r(i,b) over the panel's i in
 // ascending order on DMMA. S lives in the L2-resident global workspace, the
 // panel rows in shared memory.
-constexpr int kChPanel = 32;
+#ifndef CQR_CH_PANEL
+#define CQR_CH_PANEL 16
+#endif
+constexpr int kChPanel = CQR_CH_PANEL;
+#ifndef CQR_CH_THREADS
+#define CQR_CH_THREADS 512
+#endif
+constexpr int kChThreads = CQR_CH_THREADS;
 
-__global__ void __launch_bounds__(512) cholesky_blocked_kernel(const double* __restrict__ g, int n,
+__global__ void __launch_bounds__(kChThreads) cholesky_blocked_kernel(const double* __restrict__ g, int n,
                                                                double* __restrict__ r, double* S, int shift_mode,
                                                                double shift_value, double theory_coef,
                                                                double* shift_out, DevStatus* st) {
@@ -1062,7 +1069,7 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
     cudaError_t e =
         cudaFuncSetAttribute(cholesky_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cholesky_blocked_kernel<<<1, 512, smem, s>>>(g, n, r, work, shift_mode, shift_value, theory_coef, shift_out, st);
+    cholesky_blocked_kernel<<<1, kChThreads, smem, s>>>(g, n, r, work, shift_mode, shift_value, theory_coef, shift_out, st);
     return cudaGetLastError();
   }
   const size_t bytes = (size_t)n * n * sizeof(double);
