@@ -86,11 +86,22 @@ __global__ void __launch_bounds__(WPC * 32, 1)
     for (int s = 0; s < 4; ++s) tma_load_2d(sL + b * 2 * kTile + s * kSlab, &tm_ll, 16 * ch + 4 * s, row0, bar + b);
   };
 
-  // the input tiles of (pass P, group grp) -> sL on bar[0]
+  // the input tiles of (pass P, group grp) -> sL on bar[0]. L2 policy: the input is read once
+  // (evict first), the solved rows are read back by the later passes' left-looking part (evict
+  // last), so at wide n the recently solved rows, not the streamed input, stay in L2.
+#ifndef CQR_TRI_NO_HINT
+  const uint64_t pol_in = l2_policy_evict_first(), pol_out = l2_policy_evict_last();
+#endif
   auto issue_in = [&](int P, long long grp) {
     mbar_expect_tx(bar, W * kTile * 8);
 #pragma unroll
-    for (int t = 0; t < W; ++t) tma_load_2d(sL + t * kTile, &tm_in, 8 * W * P + 8 * t, (int)(grp * kRW), bar);
+    for (int t = 0; t < W; ++t) {
+#ifndef CQR_TRI_NO_HINT
+      tma_load_2d_hint(sL + t * kTile, &tm_in, 8 * W * P + 8 * t, (int)(grp * kRW), bar, pol_in);
+#else
+      tma_load_2d(sL + t * kTile, &tm_in, 8 * W * P + 8 * t, (int)(grp * kRW), bar);
+#endif
+    }
   };
 
   uint32_t ph0 = 0, ph1 = 0;
@@ -241,7 +252,11 @@ __global__ void __launch_bounds__(WPC * 32, 1)
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
+#ifndef CQR_TRI_NO_HINT
+          tma_store_2d_hint(&tm_st, 8 * J, row0, tile, pol_out);
+#else
           tma_store_2d(&tm_st, 8 * J, row0, tile);
+#endif
           bulk_commit();
         }
         double af[4][2];
