@@ -427,9 +427,14 @@ constexpr int kLuRotPanel = CQR_LU_ROT_PANEL;  // panel width of lu_rot_kernel
 // step loop stays rolled: no dynamic register indexing, a small I-cache
 // footprint). Per pivot step: one arg-max barrier, one barrier to publish the
 // pivot row, register fma updates; U rows go straight to the output.
-template <int NW, int PW>
+// SPLIT (l in (512, 1024], c4: 768 x 512): one launch per panel (columns [j0, j0 + PW)) that only
+// takes the pivot steps; the multipliers (Pg, l x PW), logical positions (LPg) and pivot rows (PVg)
+// go to global memory and lu_trail_kernel applies U12 and the A22 update over many SMs.
+template <int NW, int PW, bool SPLIT = false>
 __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restrict__ a1, int l, int n,
-                                                        double* __restrict__ u, double* W, DevStatus* st) {
+                                                        double* __restrict__ u, double* W, DevStatus* st,
+                                                        int j0s = 0, double* Pg = nullptr, int* LPg = nullptr,
+                                                        int* PVg = nullptr) {
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(16) double cv[2][NW][PW];  // each warp winner's panel row, double-buffered
   __shared__ double cinv[2][NW];                  // and RN(1 / its current element)
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
   double* P = smem;                                                    // multipliers: l x kLuLdp
   int* lpS = reinterpret_cast<int*>(smem + (size_t)l * kLuLdp);        // logical positions after a panel
   const bool mine = tid < l;
-  {  // W = A1, eight independent loads in flight per thread
+  if constexpr (!SPLIT) {  // W = A1, eight independent loads in flight per thread
     const long long total = (long long)l * n;
     for (long long e0 = tid; e0 < total; e0 += 8LL * nt) {
       double v[8];
@@ -451,13 +456,13 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       for (int k = 0; k < 8; ++k)
         if (e0 + k * nt < total) W[e0 + k * nt] = v[k];
     }
+    for (int i = warp; i < n; i += NW)
+      for (int c = lane; c < i; c += 32) u[(long long)i * n + c] = 0.0;
   }
-  for (int i = warp; i < n; i += NW)
-    for (int c = lane; c < i; c += 32) u[(long long)i * n + c] = 0.0;
-  int my_lp = tid, buf = 0;
+  int my_lp = SPLIT ? (j0s == 0 || !mine ? tid : LPg[tid]) : tid, buf = 0;
   __syncthreads();
   LU_MARK(0)
-  for (int j0 = 0; j0 < n; j0 += PW) {
+  for (int j0 = SPLIT ? j0s : 0; j0 < (SPLIT ? min(n, j0s + PW) : n); j0 += PW) {
     const int w = min(PW, n - j0);
     LU_MARK(1 + 4 * (j0 / PW))
     double x[PW];
@@ -509,11 +514,17 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
         if (j < 32) LU_MARK(302 + 8 * j)
         if (warp == 0) {  // U row j, panel part
           if (lane < w - jj) u[(long long)j * n + j + lane] = prow[lane];
-          if (lane == 0) pv[jj] = ps;
+          if (lane == 0) {
+            pv[jj] = ps;
+            if constexpr (SPLIT) PVg[jj] = ps;
+          }
         }
         if (act && tid != ps) {
           const double mult = div_rn(x[o], prow[0], pinv);
-          P[tid * kLuLdp + jj] = mult;
+          if constexpr (SPLIT)
+            Pg[tid * PW + jj] = mult;
+          else
+            P[tid * kLuLdp + jj] = mult;
           if (mult != 0.0) {
 #pragma unroll
             for (int c = o + 1; c < PW; ++c) x[c] = fma(-mult, prow[c - o], x[c]);
@@ -527,6 +538,10 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
       }
 #pragma unroll
       for (int c = 0; c < PW; ++c) x[c] = c + kLuUnroll < PW ? x[c + kLuUnroll] : 0.0;
+    }
+    if constexpr (SPLIT) {
+      if (mine) LPg[tid] = my_lp;
+      return;
     }
     if (mine) lpS[tid] = my_lp;
     __syncthreads();
@@ -600,6 +615,80 @@ __global__ void __launch_bounds__(NW * 32) lu_rot_kernel(const double* __restric
     __syncthreads();
     LU_MARK(3 + 4 * (j0 / PW))
   }
+}
+
+// The trailing part of panel [j0, j0 + w) for lu_rot_kernel<..., SPLIT>: one CTA per 8-column strip of
+// [j0 + w, n). U12 of the strip (one thread per column, fma chain over the panel's pivots in order,
+// zero multipliers skipped), then A22 += (-L21) U12 on DMMA for the rows still unpivoted (k = the
+// pivots in order): the same operations, in the same order, as the one-CTA kernel.
+template <int PW>
+__global__ void __launch_bounds__(256) lu_trail_kernel(double* W, int l, int n, int j0, int w, double* __restrict__ u,
+                                                       const double* __restrict__ Pg, const int* __restrict__ LPg,
+                                                       const int* __restrict__ PVg, const DevStatus* st) {
+  __shared__ double sU[PW][8];
+  if (failed(st)) return;
+  const int c1 = j0 + w, cc0 = c1 + 8 * blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 8) {
+    const int c = cc0 + tid;
+    double y[PW];
+#pragma unroll
+    for (int jj = 0; jj < PW; ++jj) y[jj] = (jj < w && c < n) ? W[(long long)PVg[jj] * n + c] : 0.0;
+#pragma unroll
+    for (int jj = 1; jj < PW; ++jj) {
+      if (jj < w) {
+        const double* pr = Pg + (long long)PVg[jj] * PW;
+#pragma unroll
+        for (int k = 0; k < jj; ++k) {
+          const double mult = pr[k];
+          if (mult != 0.0) y[jj] = fma(-mult, y[k], y[jj]);
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < PW; ++jj) {
+      if (jj < w && c < n) u[(long long)(j0 + jj) * n + c] = y[jj];
+      sU[jj][tid] = (jj < w && c < n) ? y[jj] : 0.0;
+    }
+  }
+  __syncthreads();
+  const int q = lane & 3, gr = lane >> 2, col = cc0 + 2 * q;
+  double bv[PW / 4];
+#pragma unroll
+  for (int k4 = 0; k4 < PW / 4; ++k4) bv[k4] = sU[4 * k4 + q][gr];  // B: k = q, col = gr
+  for (int rt = warp; rt * 8 < l; rt += 8) {
+    const int row = rt * 8 + gr;
+    const bool live = row < l && LPg[row] >= c1;
+    double c0v = (live && col < n) ? W[(long long)row * n + col] : 0.0;
+    double c1v = (live && col + 1 < n) ? W[(long long)row * n + col + 1] : 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < PW / 4; ++k4) {
+      const int kk = 4 * k4 + q;
+      const double av = (row < l && kk < w) ? -Pg[(long long)row * PW + kk] : 0.0;  // A: row gr, k = q
+      dmma(c0v, c1v, av, bv[k4]);
+    }
+    if (live && col < n) W[(long long)row * n + col] = c0v;
+    if (live && col + 1 < n) W[(long long)row * n + col + 1] = c1v;
+  }
+}
+
+// l in (512, 1024]: panel launches on one CTA (one thread per row) + trailing launches over many SMs.
+// work: W (l x n), then Pg (l x PW), LPg (l ints), PVg (PW ints) -- within l * (n + 33) doubles.
+template <int NW, int PW>
+cudaError_t launch_lu_split(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
+  double* W = work;
+  double* Pg = work + (size_t)l * n;
+  int* LPg = reinterpret_cast<int*>(Pg + (size_t)l * PW);
+  int* PVg = LPg + l;
+  cudaError_t e = cudaMemcpyAsync(W, a1, sizeof(double) * l * n, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(u, 0, sizeof(double) * n * n, s);
+  if (e != cudaSuccess) return e;
+  for (int j0 = 0; j0 < n; j0 += PW) {
+    lu_rot_kernel<NW, PW, true><<<1, NW * 32, 0, s>>>(a1, l, n, u, W, st, j0, Pg, LPg, PVg);
+    const int w = min(PW, n - j0), c1 = j0 + w;
+    if (c1 < n) lu_trail_kernel<PW><<<(n - c1 + 7) / 8, 256, 0, s>>>(W, l, n, j0, w, u, Pg, LPg, PVg, st);
+  }
+  return cudaGetLastError();
 }
 
 template <int NW, int PW>
@@ -1080,6 +1169,9 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
 
 cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
   static const bool legacy = std::getenv("CQR_LU_LEGACY") != nullptr;  // tuning: the swapping blocked kernel
+  static const bool split_all = std::getenv("CQR_LU_SPLIT_ALL") != nullptr;  // A/B runs: split launches for l <= 512
+  if (!legacy && split_all && l <= 256) return launch_lu_split<8, kLuRotPanel>(a1, l, n, u, work, st, s);
+  if (!legacy && split_all && l <= 512) return launch_lu_split<16, kLuRotPanel>(a1, l, n, u, work, st, s);
   if (!legacy && l <= 512 && (size_t)l * kLuLdp * sizeof(double) + (size_t)l * sizeof(int) <= 220 * 1024) {
     // as few warps as rows need: the per-step barriers and arg-max dominate (8 vs 16 warps at
     // l = 256: 276 vs 332 us)
@@ -1087,8 +1179,11 @@ cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work,
     if (l <= 256) return launch_lu_rot<8, kLuRotPanel>(a1, l, n, u, work, st, s);
     return launch_lu_rot<16, kLuRotPanel>(a1, l, n, u, work, st, s);
   }
-  // taller sketches (c4: 768 x 512) keep the swapping kernel: 24 warps x 16-column panels measured slower
-  // (6.08 vs 4.95 ms)
+  // taller sketches (c4: 768 x 512): panel launches + trailing launches over many SMs (the one-CTA
+  // swapping kernel did the 768-row trailing updates on one SM: 4.97 ms)
+  static const bool no_split = std::getenv("CQR_LU_NO_SPLIT") != nullptr;  // A/B runs
+  if (!legacy && !no_split && l <= 768) return launch_lu_split<24, kLuRotPanel>(a1, l, n, u, work, st, s);
+  if (!legacy && !no_split && l <= 1024) return launch_lu_split<32, kLuRotPanel>(a1, l, n, u, work, st, s);
   {
     const bool fits = (size_t)l * kLuLdp * sizeof(double) <= 220 * 1024;
     const size_t smem = fits ? (size_t)l * kLuLdp * sizeof(double) : 0;

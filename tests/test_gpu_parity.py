@@ -226,13 +226,16 @@ def test_trisolve_identity_and_singular():
 
 
 @pytest.mark.parametrize("l,n,seed", [(2, 2, 1), (30, 10, 2), (128, 64, 3), (256, 128, 4), (300, 150, 5),
-                                      (512, 256, 6), (768, 512, 7), (1100, 40, 8)])
+                                      (512, 256, 6), (768, 512, 7), (1100, 40, 8),
+                                      # l in (512, 1024]: panel launches + trailing launches over many SMs
+                                      (600, 100, 9), (1000, 333, 10), (700, 500, 11), (513, 17, 12)])
 def test_lu_bitwise(l, n, seed):
     a1 = o.gaussian_matrix(l, n, seed)
     assert np.array_equal(G.lu_u_factor(a1), o.lu_u_factor(a1))
 
 
-@pytest.mark.parametrize("l,n,seed", [(64, 32, 1), (300, 100, 2), (1100, 40, 3), (96, 96, 4)])
+@pytest.mark.parametrize("l,n,seed", [(64, 32, 1), (300, 100, 2), (1100, 40, 3), (96, 96, 4), (800, 200, 5),
+                                      (640, 64, 6)])
 def test_lu_pivot_ties(l, n, seed):
     # small integers: many equal |pivot| candidates, so the "first maximum in the
     # reference's swapped row order" rule decides; also exact zero pivots
