@@ -716,20 +716,26 @@ constexpr int kChPanel = CQR_CH_PANEL;
 #endif
 constexpr int kChThreads = CQR_CH_THREADS;
 
+// SPLIT (n >= 256): one launch per panel for the panel rows (S = G copied by the launcher, the shift
+// added by the first launch); chol_trail_kernel applies the trailing update over many SMs and
+// chol_out_kernel writes R.
+template <bool SPLIT = false>
 __global__ void __launch_bounds__(kChThreads) cholesky_blocked_kernel(const double* __restrict__ g, int n,
                                                                double* __restrict__ r, double* S, int shift_mode,
                                                                double shift_value, double theory_coef,
-                                                               double* shift_out, DevStatus* st) {
+                                                               double* shift_out, DevStatus* st, int j0s = 0) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double s_pd[kChPanel];  // the panel's pivots, stored after the panel
   if (failed(st)) return;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int ldp = n + 1;
   double* Pn = smem;  // kChPanel x n panel rows (stride ldp), absolute column index
-  for (int i = warp; i < n; i += nw)
-    for (int c = lane; c < n; c += 32) S[(long long)i * n + c] = g[(long long)i * n + c];
-  __syncthreads();
-  if (shift_mode != 0 && tid == 0) {
+  if constexpr (!SPLIT) {
+    for (int i = warp; i < n; i += nw)
+      for (int c = lane; c < n; c += 32) S[(long long)i * n + c] = g[(long long)i * n + c];
+    __syncthreads();
+  }
+  if (shift_mode != 0 && tid == 0 && (!SPLIT || j0s == 0)) {
     double sh = shift_value;
     if (shift_mode == 2) {
       double tr = 0.0;
@@ -740,7 +746,7 @@ __global__ void __launch_bounds__(kChThreads) cholesky_blocked_kernel(const doub
     if (shift_out) *shift_out = sh;
   }
   __syncthreads();
-  for (int j0 = 0; j0 < n; j0 += kChPanel) {
+  for (int j0 = SPLIT ? j0s : 0; j0 < (SPLIT ? min(n, j0s + kChPanel) : n); j0 += kChPanel) {
     const int w = min(kChPanel, n - j0);
     for (int rr = warp; rr < w; rr += nw)
       for (int c = j0 + rr + lane; c < n; c += 32) Pn[rr * ldp + c] = S[(long long)(j0 + rr) * n + c];
@@ -775,6 +781,7 @@ __global__ void __launch_bounds__(kChThreads) cholesky_blocked_kernel(const doub
     // panel rows of R back to S
     for (int rr = warp; rr < w; rr += nw)
       for (int c = j0 + rr + lane; c < n; c += 32) S[(long long)(j0 + rr) * n + c] = Pn[rr * ldp + c];
+    if constexpr (SPLIT) return;
     // trailing upper triangle: S22 += (-R12^T) R12, 8x8 tiles, k = panel rows ascending
     const int c1 = j0 + w;
     if (c1 < n) {
@@ -1151,14 +1158,75 @@ cudaError_t launch_small(K kernel, size_t bytes, cudaStream_t s, Args... args) {
 
 size_t small_work_doubles(int rows, int n) { return (size_t)rows * n; }
 
+// Trailing update of cholesky_blocked_kernel<true>'s panel [j0, j0 + w): one warp per upper 8x8 tile of
+// [c1, n)^2, S(a,b) += sum over the panel rows i ascending of (-R(i,a)) R(i,b) on DMMA (the blocked
+// kernel's tile loop, with the panel rows read from S).
+__global__ void __launch_bounds__(256) chol_trail_kernel(double* S, int n, int j0, int w, const DevStatus* st) {
+  if (failed(st)) return;
+  const int lane = threadIdx.x & 31;
+  const int c1 = j0 + w;
+  const int T = (n - c1 + 7) / 8;
+  int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T * (T + 1) / 2) return;
+  int ti = 0;  // upper tile t in row-major order: row ti has T - ti tiles
+  while (t >= T - ti) {
+    t -= T - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const int q = lane & 3, gr = lane >> 2;
+  const int a0 = c1 + 8 * ti, b0 = c1 + 8 * tj;
+  const int row = a0 + gr, col = b0 + 2 * q;
+  double c0v = 0.0, c1v = 0.0;
+  if (row < n && col < n) c0v = S[(long long)row * n + col];
+  if (row < n && col + 1 < n) c1v = S[(long long)row * n + col + 1];
+#pragma unroll
+  for (int k4 = 0; k4 < kChPanel / 4; ++k4) {
+    const int k = 4 * k4 + q;
+    const double av = (k < w && row < n) ? -S[(long long)(j0 + k) * n + row] : 0.0;
+    const double bv = (k < w && b0 + gr < n) ? S[(long long)(j0 + k) * n + b0 + gr] : 0.0;
+    dmma(c0v, c1v, av, bv);
+  }
+  if (row < n && col < n) S[(long long)row * n + col] = c0v;
+  if (row < n && col + 1 < n) S[(long long)row * n + col + 1] = c1v;
+}
+
+__global__ void chol_out_kernel(const double* __restrict__ S, int n, double* __restrict__ r, const DevStatus* st) {
+  if (failed(st)) return;
+  const int i = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) r[(long long)i * n + c] = c >= i ? S[(long long)i * n + c] : 0.0;
+}
+
 cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int shift_mode, double shift_value,
                             double theory_coef, double* shift_out, DevStatus* st, cudaStream_t s) {
+  static const int split_min = [] {  // A/B runs: CQR_CHOL_SPLIT_MIN=n0 splits from n0 columns on
+    const char* v = std::getenv("CQR_CHOL_SPLIT_MIN");
+    return v ? std::atoi(v) : 256;
+  }();
+  if (n >= split_min && n > 64) {
+    const size_t smem = (size_t)kChPanel * (n + 1) * sizeof(double);
+    cudaError_t e =
+        cudaFuncSetAttribute(cholesky_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(work, g, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    for (int j0 = 0; j0 < n; j0 += kChPanel) {
+      cholesky_blocked_kernel<true><<<1, kChThreads, smem, s>>>(g, n, r, work, shift_mode, shift_value, theory_coef,
+                                                                shift_out, st, j0);
+      const int w = min(kChPanel, n - j0), c1 = j0 + w;
+      if (c1 < n) {
+        const int T = (n - c1 + 7) / 8;
+        chol_trail_kernel<<<(T * (T + 1) / 2 + 7) / 8, 256, 0, s>>>(work, n, j0, w, st);
+      }
+    }
+    chol_out_kernel<<<dim3((n + 127) / 128, n), 128, 0, s>>>(work, n, r, st);
+    return cudaGetLastError();
+  }
   if (n > 64) {
     const size_t smem = (size_t)kChPanel * (n + 1) * sizeof(double);
     cudaError_t e =
-        cudaFuncSetAttribute(cholesky_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(cholesky_blocked_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cholesky_blocked_kernel<<<1, kChThreads, smem, s>>>(g, n, r, work, shift_mode, shift_value, theory_coef, shift_out, st);
+    cholesky_blocked_kernel<false><<<1, kChThreads, smem, s>>>(g, n, r, work, shift_mode, shift_value, theory_coef, shift_out, st);
     return cudaGetLastError();
   }
   const size_t bytes = (size_t)n * n * sizeof(double);

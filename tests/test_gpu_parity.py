@@ -153,7 +153,7 @@ def test_gram_known_answers():
     assert G.gram(np.array([[1.0], [2.0], [2.0]]))[0, 0] == 9.0
 
 
-@pytest.mark.parametrize("n,seed", [(1, 1), (2, 2), (30, 3), (64, 4), (128, 5), (129, 6), (256, 7)])
+@pytest.mark.parametrize("n,seed", [(1, 1), (2, 2), (30, 3), (64, 4), (128, 5), (129, 6), (256, 7), (300, 8), (512, 9)])
 def test_cholesky_bitwise(n, seed):
     a = o.gaussian_matrix(3 * n + 5, n, seed)
     g = o.gram(a)
