@@ -216,10 +216,21 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 constexpr int kGtMma = 12;
 constexpr int kGtThreads = (kGtMma + 1) * 32;
 
+// Stage layout (NP <= 256): NP/8 boxes of ROWS x 8 columns (64-byte rows, no swizzle). A fragment load reads
+// 8 consecutive columns of 4 consecutive rows (k = 4 rows per DMMA step); with 64-byte rows, rows
+// q and q + 1 sit in opposite bank halves, so the 256 bytes take the minimum two wavefronts (the
+// earlier 16-column SWIZZLE_128B boxes kept all four rows in one half: four wavefronts, LSU 83%).
+// NP = 512 keeps 16-column SWIZZLE_128B boxes: 64 narrow boxes per 16-row stage from one producer lane
+// cost more than the conflicts they remove (9.31 vs 11.44 ms at m = 1e6).
+template <int NP>
+constexpr int gram_box_cols() {
+  return NP <= 256 ? 8 : 16;
+}
 template <int NP, int ROWS>
 struct GtShape {
-  static constexpr int CHUNK = ROWS * NP;  // doubles per stage (NP/16 boxes of ROWS x 16)
-  static constexpr int BOX = ROWS * 16;
+  static constexpr int BW = gram_box_cols<NP>();
+  static constexpr int CHUNK = ROWS * NP;  // doubles per stage (NP/BW boxes of ROWS x BW)
+  static constexpr int BOX = ROWS * BW;
   static constexpr int STAGES = CHUNK * 8 * 4 <= 200 * 1024 ? 4 : 3;
   static constexpr size_t SMEM = (size_t)STAGES * CHUNK * sizeof(double) + 1024;
 };
@@ -264,7 +275,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
           mbar_expect_tx(&full[s], S::CHUNK * 8);
           const int row = lf * kLeafRows + c * ROWS;
 #pragma unroll
-          for (int b = 0; b < NP / 16; ++b) tma_load_2d(sm + s * S::CHUNK + b * S::BOX, &tmx, 16 * b, row, &full[s]);
+          for (int b = 0; b < NP / S::BW; ++b)
+            tma_load_2d(sm + s * S::CHUNK + b * S::BOX, &tmx, S::BW * b, row, &full[s]);
         }
       }
     }
@@ -281,9 +293,14 @@ __global__ void __launch_bounds__(kGtThreads, 1)
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
   bool bad = false;
-  // column group h (8 columns) of row r inside a stage: box h/2, 128B-swizzled 16-byte chunks
+  // column group h (8 columns) of row r inside a stage: box h (64-byte rows), or box h/2 with
+  // 128B-swizzled 16-byte chunks (16-column boxes)
   auto at = [&](const double* base, int r, int h) {
-    return base[(h >> 1) * S::BOX + r * 16 + 2 * ((4 * (h & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
+    if constexpr (S::BW == 8) {
+      return base[h * S::BOX + r * 8 + gr];
+    } else {
+      return base[(h >> 1) * S::BOX + r * 16 + 2 * ((4 * (h & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
+    }
   };
   int it = 0;
   for (int w = blockIdx.x;; w += gridDim.x) {
@@ -461,7 +478,7 @@ cudaError_t launch_leaves_p(const GramPlan& p, const double* x, long long ldx, c
 bool gram_tma_ok(const double* x, long long ldx, long long m, int n) {
   static const bool off = std::getenv("CQR_GRAM_NO_TMA") != nullptr;  // tuning: the cp.async kernels
   CUtensorMap probe;
-  return !off && n > 64 && m > 0 && m < (1LL << 31) - 1024 && make_tmap_2d(&probe, x, n, m, ldx, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
+  return !off && n > 64 && m > 0 && m < (1LL << 31) - 1024 && make_tmap_2d(&probe, x, n, m, ldx, 8, 16, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 GramPlan gram_plan(long long m, int n, bool tma_ok) {
@@ -520,7 +537,10 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
                                int leaf1, int num_sms) {
   if (p.tma) {
     CUtensorMap tm;
-    if (!make_tmap_2d(&tm, x, p.n, p.m, ldx, 16, p.ch, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    const bool narrow = p.np <= 256;  // gram_box_cols
+    if (!make_tmap_2d(&tm, x, p.n, p.m, ldx, narrow ? 8 : 16, p.ch,
+                      narrow ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
     if (p.np == 128) return launch_leaves_tma<128, 3, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 256) return launch_leaves_tma<256, 4, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);

@@ -244,7 +244,11 @@ __device__ long long g_trace[16 * kTraceSteps * 2];
 
 template <int NPC, int ST>
 struct WsShape {
-  static constexpr int ATILE = kKS * NPC;       // doubles per A stage (NPC/16 boxes of 32 x 16)
+  // A tile boxes: 8 columns (64-byte rows: a fragment's four rows fall in alternating bank halves,
+  // two wavefronts) for NPC = 64 (0.851 -> 0.832 ms at m = 1e6); wider tiles keep 16-column
+  // SWIZZLE_128B boxes (narrow boxes: 2.515 -> 2.52 ms at n = 128, 8.97 -> 9.14 at n = 256)
+  static constexpr int BW = NPC <= 64 ? 8 : 16;
+  static constexpr int ATILE = kKS * NPC;       // doubles per A stage (NPC/BW boxes of 32 x BW)
   static constexpr int OTILE = ST * (kKS + 4);  // doubles per Omega stage (stride 36)
   static constexpr int NGW = NPC / (8 * kWsMma);  // 8-column groups per MMA warp
   static constexpr int MGW = ST / 8;            // 8-row groups per MMA warp
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(ws_threads<NPC>(), 1)
   __shared__ __align__(8) uint64_t full[kWsStages], empty[kWsStages];
   if (failed(st)) return;
   double* sm = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-  double* sA = sm;                            // [stage][box][32 rows][16 cols, 128B-swizzled]
+  double* sA = sm;                            // [stage][box][32 rows][BW cols]
   double* sO = sm + kWsStages * S::ATILE;     // [stage][ST][36]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s0 = blockIdx.x * ST;
@@ -312,12 +316,12 @@ __global__ void __launch_bounds__(ws_threads<NPC>(), 1)
       const long long kb = k_begin + (long long)stp * kKS;
       if (gt == 0) {
         mbar_expect_tx(&full[s], S::ATILE * 8);
-        if (tma3) {  // all NPC/16 column boxes in one 3-D load
-          tma_load_3d(sA + s * S::ATILE, &tma_a, 0, (int)kb, col0 / 16, &full[s]);
+        if (tma3) {  // all NPC/BW column boxes in one 3-D load
+          tma_load_3d(sA + s * S::ATILE, &tma_a, 0, (int)kb, col0 / S::BW, &full[s]);
         } else {
 #pragma unroll
-          for (int b = 0; b < NPC / 16; ++b)
-            tma_load_2d(sA + s * S::ATILE + b * (kKS * 16), &tma_a, col0 + 16 * b, (int)kb, &full[s]);
+          for (int b = 0; b < NPC / S::BW; ++b)
+            tma_load_2d(sA + s * S::ATILE + b * (kKS * S::BW), &tma_a, col0 + S::BW * b, (int)kb, &full[s]);
         }
       }
       double* Om = sO + s * S::OTILE;
@@ -382,8 +386,11 @@ __global__ void __launch_bounds__(ws_threads<NPC>(), 1)
       for (int g = 0; g < S::MGW; ++g) af[g] = Om[g * 8 * LDO + 4 * k4];
 #pragma unroll
       for (int h = 0; h < S::NGW; ++h) {
-        const int cg = warp * S::NGW + h;  // 8-column group: box cg/2, half cg&1
-        bf[h] = As[(cg >> 1) * (kKS * 16) + r * 16 + 2 * ((4 * (cg & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
+        const int cg = warp * S::NGW + h;  // 8-column group: box cg (BW = 8) or box cg/2, half cg&1
+        if constexpr (S::BW == 8)
+          bf[h] = As[cg * (kKS * 8) + r * 8 + gr];
+        else
+          bf[h] = As[(cg >> 1) * (kKS * 16) + r * 16 + 2 * ((4 * (cg & 1) + (gr >> 1)) ^ (r & 7)) + (gr & 1)];
         bad |= nonfinite(bf[h]);
       }
 #pragma unroll
@@ -416,10 +423,11 @@ cudaError_t launch_ws(const SketchPlan& p, const double* a, long long lda, long 
                       int y1) {
   CUtensorMap tm;
   static const bool no3d = std::getenv("CQR_SKETCH_TMA2D") != nullptr;  // tuning: per-box 2-D loads
-  const int tma3 = !no3d && p.n % 16 == 0 && p.np % NPC == 0 &&
-                   make_tmap_colblocks(&tm, a, p.n, p.m_local, lda, kKS, NPC / 16, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!tma3 && !make_tmap_2d(&tm, a, p.n, p.m_local, lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
+  constexpr int BW = WsShape<NPC, ST>::BW;
+  constexpr CUtensorMapSwizzle SW = BW == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
+  const int tma3 = !no3d && p.n % BW == 0 && p.np % NPC == 0 &&
+                   make_tmap_colblocks(&tm, a, p.n, p.m_local, lda, kKS, NPC / BW, SW, BW);
+  if (!tma3 && !make_tmap_2d(&tm, a, p.n, p.m_local, lda, BW, kKS, SW)) return cudaErrorInvalidValue;
   auto k = sketch_ws_kernel<NPC, ST>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsShape<NPC, ST>::SMEM);
@@ -555,7 +563,7 @@ bool sketch_ws_ok(const double* a, long long lda, long long m_global, long long 
   static const bool off = std::getenv("CQR_SKETCH_LEGACY") != nullptr;  // tuning: force the interleaved kernel
   if (off || n <= 32 || n > 512 || (m_global & 1) || (row0 & 1) || m_global > (1LL << 31) - 64) return false;
   CUtensorMap probe;
-  return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, 16, kKS, CU_TENSOR_MAP_SWIZZLE_128B);
+  return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, 8, kKS, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 SketchPlan sketch_plan(long long m_local, int n, int l, int num_sms, bool ws_ok, int splits) {

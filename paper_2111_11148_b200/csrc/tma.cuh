@@ -104,10 +104,10 @@ __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy
 // entry point is unavailable or the layout is not TMA-addressable.
 bool make_tmap_2d(CUtensorMap* map, const double* base, long long cols, long long rows, long long ld, int box_cols,
                   int box_rows, CUtensorMapSwizzle swizzle);
-// Host: the same matrix seen as (16 columns) x rows x (cols/16 column blocks), so that one 3-D box
-// {16, box_rows, box_blocks} lands as box_blocks consecutive 2-D {16, box_rows} boxes (one TMA
-// instruction instead of box_blocks). Requires cols % 16 == 0 (no column tail to zero-fill).
+// Host: the same matrix seen as (bw columns) x rows x (cols/bw column blocks), so that one 3-D box
+// {bw, box_rows, box_blocks} lands as box_blocks consecutive 2-D {bw, box_rows} boxes (one TMA
+// instruction instead of box_blocks). Requires cols % bw == 0 (no column tail to zero-fill).
 bool make_tmap_colblocks(CUtensorMap* map, const double* base, long long cols, long long rows, long long ld,
-                         int box_rows, int box_blocks, CUtensorMapSwizzle swizzle);
+                         int box_rows, int box_blocks, CUtensorMapSwizzle swizzle, int bw = 16);
 
 }  // namespace cqr

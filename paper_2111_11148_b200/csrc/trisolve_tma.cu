@@ -339,13 +339,13 @@ bool make_tmap_2d(CUtensorMap* map, const double* base, long long cols, long lon
 }
 
 bool make_tmap_colblocks(CUtensorMap* map, const double* base, long long cols, long long rows, long long ld,
-                         int box_rows, int box_blocks, CUtensorMapSwizzle swizzle) {
+                         int box_rows, int box_blocks, CUtensorMapSwizzle swizzle, int bw) {
   auto fn = encode_fn();
-  if (!fn || ((uintptr_t)base & 15) || ((ld * 8) & 15) || cols < 16 || (cols & 15) || rows < 1 || ld < cols)
+  if (!fn || ((uintptr_t)base & 15) || ((ld * 8) & 15) || cols < bw || (cols % bw) || rows < 1 || ld < cols)
     return false;
-  const cuuint64_t dims[3] = {16, (cuuint64_t)rows, (cuuint64_t)(cols / 16)};
-  const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, 16 * 8};
-  const cuuint32_t box[3] = {16, (cuuint32_t)box_rows, (cuuint32_t)box_blocks};
+  const cuuint64_t dims[3] = {(cuuint64_t)bw, (cuuint64_t)rows, (cuuint64_t)(cols / bw)};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)bw * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)box_rows, (cuuint32_t)box_blocks};
   const cuuint32_t es[3] = {1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
