@@ -255,6 +255,13 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_sample(a, l, CPU_SAMPLE_ROWS, method, mname)
     stage_avg = {cq_name: float(v / args.steps) for cq_name, v in zip(_abi.STAGE_NAMES, stage_tot)}
+    # per stage: algorithmic flops of this rank's part / CUDA-event stage time, vs the DMMA peak
+    qr = mname.startswith("rqr")
+    st_flops = {"sketch": 2.0 * l * m_local * n, "precondition": (2.0 if qr else 1.0) * (l * n * n - n ** 3 / 3.0),
+                "gram": float(m_local) * n * (n + 1), "cholesky": n ** 3 / 3.0, "trisolve": 2.0 * m_local * n * n,
+                "recover": n ** 3 / 3.0}
+    stage_roof = {k: {"tflops": f / (stage_avg[k] * 1e-3) / 1e12, "frac": f / (stage_avg[k] * 1e-3) / 1e12 /
+                      pk["fp64_tflops"]} for k, f in st_flops.items() if stage_avg.get(k, 0.0) > 0.0}
     line = {"metric": "rQR/rLU-CholeskyQR fp64 TFLOP/s (ms/factorization in ms_per_step)", "value": value,
             "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -265,7 +272,7 @@ def run_ours(args):
                        "l2": f"inputs larger than L2 ({8 * m_local * n / 1e9:.2f} GB per GPU vs 126 MB L2), no flush",
                        "parallelism": f"row-block dp{world}"},
             "stage_ms": stage_avg, "clocks": clk.summary(), "gpu_launches": launches,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu, "e2e": e2e,
             "check": {"orth": orth, "res": res, "sketch_rows": rep.sketch_rows}}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -679,7 +679,7 @@ Outcome run_precond(Job& j) {
     }
     // ---- Precondition: R~ = QR/LU of A1 (kernels.hpp:175-257)
     double* rt = dbuf<double>(c, B_RT, (size_t)n * n);
-    double* work = dbuf<double>(c, B_WORK, std::max<size_t>((size_t)l * (n + 33), (size_t)n * n));
+    double* work = dbuf<double>(c, B_WORK, std::max<size_t>(cqr::qr_work_doubles((int)l, n), (size_t)n * n));
     double* pack1 = dbuf<double>(c, B_PACK1, cqr::trisolve_pack_doubles(n));
     {
       StageScope t(c, CQR_STAGE_PRECONDITION);
@@ -1249,7 +1249,7 @@ static int small_factor(cqr_ctx* c, const double* a1, int64_t l, int64_t n, doub
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     double* da = dbuf<double>(c, B_A1, (size_t)l * n);
     double* dr = dbuf<double>(c, B_RT, (size_t)n * n);
-    double* work = dbuf<double>(c, B_WORK, (size_t)l * (n + 33));
+    double* work = dbuf<double>(c, B_WORK, cqr::qr_work_doubles((int)l, (int)n));
     ck(cudaMemcpyAsync(da, a1, sizeof(double) * l * n, cudaMemcpyHostToDevice, c->stream), "A1 H2D");
     reset_status(c);
     if (lu)

@@ -94,6 +94,7 @@ cudaError_t launch_box_muller_bits(const uint64_t* bits, long long pairs, double
 // kernels.hpp:76-90 (+ G += shift*I, engine.cpp:85; theory shift from trace(G)).
 // shift_mode 0 none, 1 fixed (value), 2 theory (coef * trace(G)); shift_out optional.
 size_t small_work_doubles(int rows, int n);
+size_t qr_work_doubles(int l, int n);  // workspace of launch_qr_r / launch_lu_u
 cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int shift_mode, double shift_value,
                             double theory_coef, double* shift_out, DevStatus* st, cudaStream_t s);
 // kernels.hpp:211-257 (U only; status SingularTriangular(j) on a zero pivot).

@@ -902,8 +902,14 @@ __global__ void __launch_bounds__(kT) qr_kernel(const double* __restrict__ a1, i
 constexpr int kQrB = 32;
 constexpr int kQrT = 512;
 
+// SPLIT (c2: 512 x 256): one launch per panel (the panel's reflectors, its R rows and T), V and T to
+// global memory (Vg: kQrB columns of ld l, Tg: kQrB x kQrB); qr_trail_kernel applies A2 -= V (T^T
+// (V^T A2)) with one CTA per 8-column strip and qr_out_kernel writes the sign-normalised R. Same
+// operations in the same order per element as the one-CTA kernel.
+template <bool SPLIT = false>
 __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restrict__ a1, int l, int n,
-                                                         double* __restrict__ r, double* W, DevStatus* st) {
+                                                         double* __restrict__ r, double* W, DevStatus* st,
+                                                         int j0s = 0, double* Vg = nullptr, double* Tg = nullptr) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double scratch[33];
   __shared__ double taus[kQrB];
@@ -916,13 +922,15 @@ __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restri
   double* Pn = smem;                 // kQrB columns of (l - j0) rows
   double* Ys = smem + kQrB * ldr;    // kQrB x n (row stride n + 4): V^T A2, then T^T V^T A2
   const int ldy = n + 4;
-  for (long long e = tid; e < (long long)l * n; e += nt) {
-    const int i = (int)(e / n), c = (int)(e % n);
-    W[(long long)c * l + i] = a1[e];
+  if (!SPLIT || j0s == 0) {
+    for (long long e = tid; e < (long long)l * n; e += nt) {
+      const int i = (int)(e / n), c = (int)(e % n);
+      W[(long long)c * l + i] = a1[e];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const double tol = 2.2250738585072014e-308 * 2.2250738585072014e-308;  // (smallest normal)^2
-  for (int j0 = 0; j0 < n; j0 += kQrB) {
+  for (int j0 = SPLIT ? j0s : 0; j0 < (SPLIT ? min(n, j0s + kQrB) : n); j0 += kQrB) {
     const int b = min(kQrB, n - j0), rp = l - j0;  // panel width, panel rows
     for (int e = tid; e < b * rp; e += nt) {
       const int c = e / rp, i = e - (e / rp) * rp;
@@ -1024,6 +1032,14 @@ __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restri
         }
       }
       __syncthreads();
+      if constexpr (SPLIT) {  // V (rows [0, rp) of the panel, unit diagonal) and T for qr_trail_kernel
+        for (int e = tid; e < kQrB * rp; e += nt) {
+          const int c = e / rp, i = e - (e / rp) * rp;
+          Vg[(long long)c * l + i] = Pn[c * ldr + i];
+        }
+        for (int e = tid; e < kQrB * kQrB; e += nt) Tg[e] = T[e / kQrB][e % kQrB];
+        return;
+      }
       // ---- Y = V^T A2 (kQrB x n2, k over the panel rows) on DMMA
       const int q = lane & 3, gr = lane >> 2;
       const int n2 = n - c1, tcn = (n2 + 7) / 8;
@@ -1092,6 +1108,7 @@ __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restri
     }
     __syncthreads();
   }
+  if constexpr (SPLIT) return;
   for (int e = tid; e < n * n; e += nt) {
     const int i = e / n, c = e % n;
     r[e] = c >= i ? W[(long long)c * l + i] : 0.0;
@@ -1157,6 +1174,8 @@ cudaError_t launch_small(K kernel, size_t bytes, cudaStream_t s, Args... args) {
 }  // namespace
 
 size_t small_work_doubles(int rows, int n) { return (size_t)rows * n; }
+// workspace of launch_qr_r / launch_lu_u: W (l x n) + panel buffers (the split QR: V, kQrB x l, and T)
+size_t qr_work_doubles(int l, int n) { return (size_t)l * (n + 33) + (size_t)kQrB * kQrB; }
 
 // Trailing update of cholesky_blocked_kernel<true>'s panel [j0, j0 + w): one warp per upper 8x8 tile of
 // [c1, n)^2, S(a,b) += sum over the panel rows i ascending of (-R(i,a)) R(i,b) on DMMA (the blocked
@@ -1274,15 +1293,97 @@ cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work,
   return cudaGetLastError();
 }
 
+// The trailing update of qr_blocked_kernel<true>'s panel [j0, j0 + kQrB): one CTA (8 warps) per
+// 8-column strip of [j0 + b, n); the blocked kernel's Y / T^T Y / A2 -= V Z steps for that strip.
+__global__ void __launch_bounds__(256) qr_trail_kernel(double* W, int l, int n, int j0, int b,
+                                                       const double* __restrict__ Vg, const double* __restrict__ Tg,
+                                                       const DevStatus* st) {
+  __shared__ double Ys[kQrB][9];
+  __shared__ double Ts[kQrB][kQrB + 1];
+  if (failed(st)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, gr = lane >> 2;
+  const int rp = l - j0, c1 = j0 + b, cbase = c1 + 8 * blockIdx.x;
+  for (int e = tid; e < kQrB * kQrB; e += 256) Ts[e / kQrB][e % kQrB] = Tg[e];
+  if (warp < kQrB / 8) {  // Y tile kt = warp: rows k of V^T, the strip's 8 columns
+    const int kt = warp, cb = cbase + gr;
+    double y0 = 0.0, y1 = 0.0;
+    for (int r0 = 0; r0 < rp; r0 += 32) {
+      double av[8], bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int rr = r0 + 4 * u + q;
+        av[u] = rr < rp ? Vg[(long long)(kt * 8 + gr) * l + rr] : 0.0;
+        bv[u] = (rr < rp && cb < n) ? W[(long long)cb * l + j0 + rr] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dmma(y0, y1, av[u], bv[u]);
+    }
+    Ys[kt * 8 + gr][2 * q] = y0;
+    Ys[kt * 8 + gr][2 * q + 1] = y1;
+  }
+  __syncthreads();
+  if (tid < 8) {  // Y <- T^T Y, column tid, k descending
+    for (int k = kQrB - 1; k >= 0; --k) {
+      double z = 0.0;
+      for (int i = 0; i <= k; ++i) z = fma(Ts[i][k], Ys[i][tid], z);
+      Ys[k][tid] = z;
+    }
+  }
+  __syncthreads();
+  double bv[kQrB / 4];
+#pragma unroll
+  for (int k4 = 0; k4 < kQrB / 4; ++k4) bv[k4] = cbase + gr < n ? Ys[4 * k4 + q][gr] : 0.0;  // B = Z: row k, col c
+  const int col = cbase + 2 * q;
+  for (int rt = warp; rt * 8 < rp; rt += 8) {
+    const int rowl = rt * 8 + gr;
+    double c0v = (rowl < rp && col < n) ? W[(long long)col * l + j0 + rowl] : 0.0;
+    double c1v = (rowl < rp && col + 1 < n) ? W[(long long)(col + 1) * l + j0 + rowl] : 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < kQrB / 4; ++k4) {
+      const int kk = 4 * k4 + q;
+      const double av = rowl < rp ? -Vg[(long long)kk * l + rowl] : 0.0;  // A = -V: row r, col k
+      dmma(c0v, c1v, av, bv[k4]);
+    }
+    if (rowl < rp && col < n) W[(long long)col * l + j0 + rowl] = c0v;
+    if (rowl < rp && col + 1 < n) W[(long long)(col + 1) * l + j0 + rowl] = c1v;
+  }
+}
+
+__global__ void qr_out_kernel(const double* __restrict__ W, int l, int n, double* __restrict__ r,
+                              const DevStatus* st) {  // R = upper part of W, rows sign-normalised (kernels.hpp:165-168)
+  if (failed(st)) return;
+  const int i = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const double sg = W[(long long)i * l + i] < 0.0 ? -1.0 : 1.0;
+  r[(long long)i * n + c] = c >= i ? sg * W[(long long)c * l + i] : 0.0;
+}
+
 cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work, DevStatus* st, cudaStream_t s) {
   if (n > 512) return cudaErrorInvalidValue;
   const size_t bytes = (size_t)l * n * sizeof(double);
   const int use_smem = bytes <= kSmemCap;
   const size_t bsmem = ((size_t)kQrB * (l + 4) + (size_t)kQrB * (n + 4)) * sizeof(double);
-  if (!use_smem && bsmem <= 200 * 1024) {  // blocked: the panel and V^T A2 in shared memory
-    cudaError_t e = cudaFuncSetAttribute(qr_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+  static const bool no_split = std::getenv("CQR_QR_NO_SPLIT") != nullptr;  // A/B runs: the one-CTA kernel
+  if (!use_smem && bsmem <= 200 * 1024 && !no_split) {  // per-panel launches, trailing update over many SMs
+    cudaError_t e =
+        cudaFuncSetAttribute(qr_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
     if (e != cudaSuccess) return e;
-    qr_blocked_kernel<<<1, kQrT, bsmem, s>>>(a1, l, n, r, work, st);
+    double* Vg = work + (size_t)l * n;  // kQrB x l, then Tg (kQrB x kQrB): qr_work_doubles
+    double* Tg = Vg + (size_t)kQrB * l;
+    for (int j0 = 0; j0 < n; j0 += kQrB) {
+      qr_blocked_kernel<true><<<1, kQrT, bsmem, s>>>(a1, l, n, r, work, st, j0, Vg, Tg);
+      const int b = min(kQrB, n - j0), c1 = j0 + b;
+      if (c1 < n) qr_trail_kernel<<<(n - c1 + 7) / 8, 256, 0, s>>>(work, l, n, j0, b, Vg, Tg, st);
+    }
+    qr_out_kernel<<<dim3((n + 127) / 128, n), 128, 0, s>>>(work, l, n, r, st);
+    return cudaGetLastError();
+  }
+  if (!use_smem && bsmem <= 200 * 1024) {  // blocked: the panel and V^T A2 in shared memory
+    cudaError_t e =
+        cudaFuncSetAttribute(qr_blocked_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+    if (e != cudaSuccess) return e;
+    qr_blocked_kernel<false><<<1, kQrT, bsmem, s>>>(a1, l, n, r, work, st);
     return cudaGetLastError();
   }
   return launch_small(qr_kernel, bytes, s, a1, l, n, r, work, use_smem, st);
