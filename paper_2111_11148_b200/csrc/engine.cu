@@ -388,22 +388,37 @@ void gram_det(cqr_ctx* c, const double* x, long long ldx, int n, long long m, do
   shard_top(c, m, p, n, w, g);
 }
 
-// The same protocol for p virtual ranks on this device, rank after rank (the
-// exchanges become buffer hand-offs): cqr_gram_sharded_sim.
+// The same protocol for p virtual ranks on this device, rank after rank: cqr_gram_sharded_sim.
+// The hand-offs between ranks are device copies, or -- with an attached one-rank communicator --
+// the NCCL calls of gram_det itself (ncclSend/ncclRecv to self in a group, ncclAllGather of the
+// node slots), so the exchange code runs on a one-GPU box.
 void gram_det_sim(cqr_ctx* c, const double* x, long long ldx, int n, long long m, int p, double* g) {
   const int K = shard_slots(m, p);
   ShardWs w = shard_ws(c, m, p, n, K);
   const size_t np2 = (size_t)w.np * w.np;
+  const bool nccl = c->comm && !c->local_only && c->world == 1;
   ck(cudaMemsetAsync(w.all, 0, sizeof(double) * p * K * n * n, c->stream), "slots");
-  int cur = 0;  // w.ht + cur*np2: the chain arriving from the previous rank
+  double* in = w.ht;         // the chain arriving from the previous rank
+  double* out = w.ht + np2;  // this rank's tail (or forwarded span)
   for (int b = 0; b < p; ++b) {
     const cqr::ShardGram sg = cqr::shard_gram_plan(m, p, b);
     const double* xb = x + sg.r0 * ldx;
-    double* in = w.ht + cur * np2;
-    double* out = w.ht + ((cur + 1) % 3) * np2;
+    double* slots = nccl ? w.slots : w.all + (size_t)b * K * n * n;
+    if (nccl) ck(cudaMemsetAsync(w.slots, 0, sizeof(double) * K * n * n, c->stream), "slots");
     shard_tail(c, sg, xb, ldx, n, w.np, out, 1);
-    shard_body(c, sg, xb, ldx, n, w, in, out, w.all + (size_t)b * K * n * n, 1);
-    cur = (cur + 1) % 3;
+    shard_body(c, sg, xb, ldx, n, w, in, out, slots, 1);
+    if (nccl) {
+      ckn(ncclAllGather(w.slots, w.all + (size_t)b * K * n * n, (size_t)K * n * n, ncclDouble, c->comm, c->stream),
+          "allgather nodes");
+      if (sg.tail) {
+        ckn(ncclGroupStart(), "group");
+        ckn(ncclSend(out, np2, ncclDouble, 0, c->comm, c->stream), "send tail");
+        ckn(ncclRecv(in, np2, ncclDouble, 0, c->comm, c->stream), "recv head");
+        ckn(ncclGroupEnd(), "group");
+      }
+    } else if (sg.tail) {
+      ck(cudaMemcpyAsync(in, out, sizeof(double) * np2, cudaMemcpyDeviceToDevice, c->stream), "hand-off");
+    }
   }
   shard_top(c, m, p, n, w, g);
 }

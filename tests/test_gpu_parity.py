@@ -144,6 +144,10 @@ def test_sharded_gram_sim_bitwise_for_any_p(m, n, p, ld):
     one = G.gram(x)
     for q in sorted({1, 2, p}):
         assert torch.equal(G.gram_sharded_sim(x, q), one), q
+    # the hand-offs through NCCL itself (send/recv to self, all-gather) on a one-rank communicator
+    coll = G.Context(0)
+    coll.attach_comm(0, 1, G.make_comm_id())
+    assert torch.equal(G.gram_sharded_sim(x, p, ctx=coll), one)
     if m * n <= 2e7:
         assert np.array_equal(one.cpu().numpy(), o.gram(x.cpu().numpy()))
 
