@@ -59,7 +59,7 @@ struct cqr_ctx {
   size_t ev_used = 0;
   std::vector<StageEv> stage_evs;
   long long launches = 0;
-  int tiles_key = -1;  // gram tile table currently on the device
+  int tiles_key[2] = {-1, -1};  // gram tile tables currently on the device
   int local_only = 0;  // temporarily treat an attached communicator as absent (replicated small work)
   cudaStream_t cstream = nullptr;  // copy stream of the host-buffer pipeline
   std::vector<cudaEvent_t> pipe_ev;
@@ -274,15 +274,16 @@ void allreduce(cqr_ctx* c, double* p, size_t count) {
   ckn(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->comm, c->stream), "ncclAllReduce");
 }
 
-const int32_t* gram_tiles_dev(cqr_ctx* c, const cqr::GramPlan& p) {
-  int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 4096);
+// slot 0: the main plan's table; slot 1: the last-wave table of the split launch (gram_dev)
+const int32_t* gram_tiles_dev(cqr_ctx* c, const cqr::GramPlan& p, int slot = 0) {
+  int32_t* tiles = dbuf<int32_t>(c, B_GTILES, 8192) + 4096 * slot;
   const int key = p.np * 1000000 + p.wpc * 10000 + p.parts * 100 + p.maxt + (p.tma ? 5000 : 0);
-  if (c->tiles_key != key) {  // the table depends on (np, parts, maxt) only: upload once
+  if (c->tiles_key[slot] != key) {  // the table depends on (np, parts, maxt) only: upload once
     std::vector<int32_t> ht(p.tiles_bytes / sizeof(int32_t));
     cqr::gram_tiles(p, ht.data());
     ck(cudaStreamSynchronize(c->stream), "sync");
     ck(cudaMemcpy(tiles, ht.data(), p.tiles_bytes, cudaMemcpyHostToDevice), "tiles H2D");
-    c->tiles_key = key;
+    c->tiles_key[slot] = key;
   }
   return tiles;
 }
@@ -448,8 +449,24 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
       }
     } else {
       if (pj) wait_all(*pj);
-      LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
-                                        c->stream, 0, -1, c->num_sms));
+      // n in (64, 128], one CTA per leaf: the leaves past the last whole wave of CTAs run as a second launch
+      // with each leaf's 36 macro tiles split over 3 CTAs (same tiles, same k order: identical partials), so
+      // the last wave takes 1/3 leaf-times per round instead of a full leaf with most SMs idle
+      const int waves = p.leaves / c->num_sms, split = waves * c->num_sms, rem = p.leaves - split;
+      if (p.tma && p.np == 128 && p.parts == 1 && waves >= 1 && rem > 0 && 3 * rem <= 2 * (c->num_sms / 3) * 3) {
+        cqr::GramPlan p3 = p;
+        p3.parts = 3;
+        p3.maxt = 1;
+        p3.tiles_bytes = (size_t)p3.parts * p3.wpc * p3.maxt * sizeof(int32_t);
+        const int32_t* tiles3 = gram_tiles_dev(c, p3, 1);
+        LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
+                                          c->stream, 0, split, c->num_sms));
+        LAUNCH(c, cqr::launch_gram_leaves(p3, x, ldx, tiles3, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
+                                          c->stream, split, p.leaves, c->num_sms));
+      } else {
+        LAUNCH(c, cqr::launch_gram_leaves(p, x, ldx, tiles, part, vec_ok(x, ldx, n) ? 1 : 0, check, c->status,
+                                          c->stream, 0, -1, c->num_sms));
+      }
     }
     LAUNCH(c, cqr::launch_gram_combine(p, part, g, (!c->comm || c->local_only) ? 1 : 0, c->status, c->stream));
     ++c->launches;

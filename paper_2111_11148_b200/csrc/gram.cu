@@ -541,6 +541,8 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
     if (!make_tmap_2d(&tm, x, p.n, p.m, ldx, narrow ? 8 : 16, p.ch,
                       narrow ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
+    if (p.np == 128 && p.maxt == 1)  // the split last wave (engine gram_dev)
+      return launch_leaves_tma<128, 1, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 128) return launch_leaves_tma<128, 3, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 256) return launch_leaves_tma<256, 4, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);

@@ -121,7 +121,9 @@ def test_box_muller_edge_bits():
 # ---------------- kernels -------------------------------------------------------------
 @pytest.mark.parametrize("m,n,seed", [(3, 3, 0), (50, 10, 7), (2500, 6, 11), (3000, 12, 2), (5000, 64, 3),
                                       (4113, 128, 4), (2048, 1, 5), (20000, 33, 6), (9000, 200, 7),
-                                      (3000, 300, 8), (33 * 1024 + 5, 16, 9), (70000, 64, 10), (16 * 1024, 24, 11)])
+                                      (3000, 300, 8), (33 * 1024 + 5, 16, 9), (70000, 64, 10), (16 * 1024, 24, 11),
+                                      # n in (64, 128] past one wave of leaves: the last wave split over 3 CTAs
+                                      (200_000, 128, 12), (1_000_003, 72, 13)])
 def test_gram_bitwise(m, n, seed):
     a = o.gaussian_matrix(m, n, seed)
     g = G.gram(a)
