@@ -107,12 +107,20 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   uint32_t ph0 = 0, ph1 = 0;
   const long long groups = (m + kRW - 1) / kRW;
   const long long gstride = (long long)gridDim.x * WPC;
-  long long grp = (long long)blockIdx.x * WPC + warp;
+  // Whole rounds give group k * gstride + blockIdx.x * WPC + warp; the groups of the last, partial round
+  // are dealt CTA-major (warp w of CTA b takes rounds * gstride + w * gridDim.x + b), so every SM keeps a
+  // share of them instead of the first CTAs taking all (c1: 31250 groups, 1776 warps).
+  const long long rounds = groups / gstride;
+  auto next_grp = [&](long long g) -> long long {
+    const long long k = g < rounds * gstride ? g / gstride : rounds;
+    if (k + 1 < rounds) return g + gstride;
+    if (k + 1 == rounds) return rounds * gstride + (long long)warp * gridDim.x + blockIdx.x;
+    return groups;
+  };
+  long long grp = rounds > 0 ? (long long)blockIdx.x * WPC + warp : (long long)warp * gridDim.x + blockIdx.x;
   if (lane == 0 && grp < groups) issue_in(0, grp);
-  for (; grp < groups; grp += gstride) {
+  for (; grp < groups; grp = next_grp(grp)) {
     const int row0 = (int)(grp * kRW);
-    // warps of this CTA with a group in this round (the others have left the loop)
-    const int nact_thr = (int)min((long long)WPC, groups - (grp - warp)) * 32;
 #pragma unroll 1
     for (int P = 0; P < NPASS; ++P) {
       const int c0 = 8 * W * P;
@@ -173,10 +181,10 @@ __global__ void __launch_bounds__(WPC * 32, 1)
       // prefetch the next pass's input (sL is free again)
       {
         const bool last = P + 1 == NPASS;
-        if (!last || grp + gstride < groups) {
+        if (!last || next_grp(grp) < groups) {
           fence_async_shared();
           __syncwarp();
-          if (lane == 0) issue_in(last ? 0 : P + 1, last ? grp + gstride : grp);
+          if (lane == 0) issue_in(last ? 0 : P + 1, last ? next_grp(grp) : grp);
         }
       }
       // 3. right-looking inside the pass
@@ -195,9 +203,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
         for (int g = 0; g < 4; ++g)
           *reinterpret_cast<double2*>(tile + swz64(8 * g + gr, q)) = make_double2(acc[g][0][0], acc[g][0][1]);
         __syncwarp();
-#ifdef CQR_TRI_SYNC
-        asm volatile("bar.sync 1, %0;" ::"r"(nact_thr) : "memory");
-#endif
         {
           const double* D = sD + J * kDiagStride;
           double y[8];
@@ -246,9 +251,6 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           for (int u = 0; u < 4; ++u)
             *reinterpret_cast<double2*>(tile + swz64(lane, u)) = make_double2(y[2 * u], y[2 * u + 1]);
         }
-#ifdef CQR_TRI_SYNC
-        asm volatile("bar.sync 1, %0;" ::"r"(nact_thr) : "memory");
-#endif
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
