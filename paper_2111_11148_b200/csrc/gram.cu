@@ -385,14 +385,22 @@ __device__ __forceinline__ void push_merge(double* stk, int& top, double v, unsi
   stk[top++] = v;
 }
 
+// Level A over the upper triangle laid out linearly (thread e -> (i, j >= i), every lane busy; a
+// row-per-block grid left half of each block idle): 16 leaf loads in flight per element.
 __global__ void gram_combine_a_kernel(const double* __restrict__ partial, int leaves, int np, int n,
                                       double* __restrict__ gsum, const DevStatus* st) {
   if (failed(st)) return;
-  const int i = blockIdx.y;
-  const int xb = (n + 127) / 128;  // column blocks per row; grid.x = groups * xb (grid.z would cap at 65535)
-  const int grp = blockIdx.x / xb;
-  const int j = i + (blockIdx.x - grp * xb) * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+  const int tri = n * (n + 1) / 2;
+  const int per = (tri + blockDim.x - 1) / blockDim.x;  // blocks per group
+  const int grp = blockIdx.x / per;
+  const int e = (blockIdx.x - grp * per) * blockDim.x + threadIdx.x;
+  if (e >= tri) return;
+  // row i: elements [i n - i (i - 1) / 2, ...) of the packed upper triangle
+  const double tn = 2.0 * n + 1.0;
+  int i = (int)((tn - sqrt(tn * tn - 8.0 * e)) * 0.5);
+  while (i > 0 && i * n - i * (i - 1) / 2 > e) --i;
+  while ((i + 1) * n - (i + 1) * i / 2 <= e) ++i;
+  const int j = i + (e - (i * n - i * (i - 1) / 2));
   const long long stride = (long long)np * np;
   const int l0 = grp * kGroup, l1 = min(leaves, l0 + kGroup);
   const double* p = partial + (long long)i * np + j;
@@ -579,8 +587,9 @@ cudaError_t launch_gram_combine(const GramPlan& p, double* partial, double* g, i
                                 const DevStatus* st, cudaStream_t s) {
   const int groups = (p.leaves + kGroup - 1) / kGroup;
   double* gsum = partial + p.partial_doubles;  // workspace after the leaf partials (gram_plan reserves it)
-  dim3 ga((unsigned)(((p.n + 127) / 128) * groups), (unsigned)p.n);
-  gram_combine_a_kernel<<<ga, 128, 0, s>>>(partial, p.leaves, p.np, p.n, gsum, st);
+  const int tri = p.n * (p.n + 1) / 2;
+  gram_combine_a_kernel<<<(unsigned)(((tri + 255) / 256) * groups), 256, 0, s>>>(partial, p.leaves, p.np, p.n, gsum,
+                                                                                   st);
   dim3 gb((unsigned)((p.n + 127) / 128), (unsigned)p.n);
   gram_combine_b_kernel<<<gb, 128, 0, s>>>(gsum, p.leaves, p.np, p.n, g, mirror, st);
   return cudaGetLastError();
