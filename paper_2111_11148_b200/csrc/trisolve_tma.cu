@@ -359,10 +359,13 @@ bool trisolve_tma_eligible(const TrisolveArgs& a, int np) {
          (a.ldi & 1) == 0 && (a.ldo & 1) == 0 && encode_fn() != nullptr;
 }
 
+#ifndef CQR_TRI64_WPC
+#define CQR_TRI64_WPC 12
+#endif
 cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s) {
   switch (np) {
     case 32: return launch_t<32, 16, true>(a, s);
-    case 64: return launch_t<64, 12, true>(a, s);
+    case 64: return launch_t<64, CQR_TRI64_WPC, true>(a, s);
     case 128: return launch_t<128, 12, true>(a, s);
     case 256: return launch_t<256, 12, false>(a, s);
     case 512: return launch_t<512, 12, false>(a, s);
