@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(256) lu_trail_kernel(double* W, int l, int n, 
   if (failed(st)) return;
   const int c1 = j0 + w, cc0 = c1 + 8 * blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 8) {
+  if (tid < 8) {  // every row chunk of the strip recomputes the strip's U12; chunk 0 writes it
     const int c = cc0 + tid;
     double y[PW];
 #pragma unroll
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) lu_trail_kernel(double* W, int l, int n, 
     }
 #pragma unroll
     for (int jj = 0; jj < PW; ++jj) {
-      if (jj < w && c < n) u[(long long)(j0 + jj) * n + c] = y[jj];
+      if (jj < w && c < n && blockIdx.y == 0) u[(long long)(j0 + jj) * n + c] = y[jj];
       sU[jj][tid] = (jj < w && c < n) ? y[jj] : 0.0;
     }
   }
@@ -656,19 +656,32 @@ __global__ void __launch_bounds__(256) lu_trail_kernel(double* W, int l, int n, 
   double bv[PW / 4];
 #pragma unroll
   for (int k4 = 0; k4 < PW / 4; ++k4) bv[k4] = sU[4 * k4 + q][gr];  // B: k = q, col = gr
-  for (int rt = warp; rt * 8 < l; rt += 8) {
-    const int row = rt * 8 + gr;
-    const bool live = row < l && LPg[row] >= c1;
-    double c0v = (live && col < n) ? W[(long long)row * n + col] : 0.0;
-    double c1v = (live && col + 1 < n) ? W[(long long)row * n + col + 1] : 0.0;
+  // this CTA's row chunk: tiles [blockIdx.y * 32, +32), at most 4 per warp, all loads issued before the DMMAs
+  constexpr int TPW = 4;
+  double c0v[TPW], c1v[TPW], av[TPW][PW / 4];
+  bool live[TPW];
+  int row[TPW];
+#pragma unroll
+  for (int h = 0; h < TPW; ++h) {
+    const int rt = blockIdx.y * 32 + warp + 8 * h;
+    row[h] = rt * 8 + gr;
+    live[h] = row[h] < l && LPg[row[h]] >= c1;
+    c0v[h] = (live[h] && col < n) ? W[(long long)row[h] * n + col] : 0.0;
+    c1v[h] = (live[h] && col + 1 < n) ? W[(long long)row[h] * n + col + 1] : 0.0;
 #pragma unroll
     for (int k4 = 0; k4 < PW / 4; ++k4) {
       const int kk = 4 * k4 + q;
-      const double av = (row < l && kk < w) ? -Pg[(long long)row * PW + kk] : 0.0;  // A: row gr, k = q
-      dmma(c0v, c1v, av, bv[k4]);
+      av[h][k4] = (row[h] < l && kk < w) ? -Pg[(long long)row[h] * PW + kk] : 0.0;  // A: row gr, k = q
     }
-    if (live && col < n) W[(long long)row * n + col] = c0v;
-    if (live && col + 1 < n) W[(long long)row * n + col + 1] = c1v;
+  }
+#pragma unroll
+  for (int k4 = 0; k4 < PW / 4; ++k4)
+#pragma unroll
+    for (int h = 0; h < TPW; ++h) dmma(c0v[h], c1v[h], av[h][k4], bv[k4]);
+#pragma unroll
+  for (int h = 0; h < TPW; ++h) {
+    if (live[h] && col < n) W[(long long)row[h] * n + col] = c0v[h];
+    if (live[h] && col + 1 < n) W[(long long)row[h] * n + col + 1] = c1v[h];
   }
 }
 
@@ -686,7 +699,8 @@ cudaError_t launch_lu_split(const double* a1, int l, int n, double* u, double* w
   for (int j0 = 0; j0 < n; j0 += PW) {
     lu_rot_kernel<NW, PW, true><<<1, NW * 32, 0, s>>>(a1, l, n, u, W, st, j0, Pg, LPg, PVg);
     const int w = min(PW, n - j0), c1 = j0 + w;
-    if (c1 < n) lu_trail_kernel<PW><<<(n - c1 + 7) / 8, 256, 0, s>>>(W, l, n, j0, w, u, Pg, LPg, PVg, st);
+    if (c1 < n)  // one CTA per 8-column strip and 32 row tiles (256 rows)
+      lu_trail_kernel<PW><<<dim3((n - c1 + 7) / 8, (l + 255) / 256), 256, 0, s>>>(W, l, n, j0, w, u, Pg, LPg, PVg, st);
   }
   return cudaGetLastError();
 }
