@@ -216,6 +216,12 @@ constexpr int kWsIlp = CQR_WS_ILP;
 constexpr int kWsMma = CQR_WS_MMA;
 // n <= 64 (NPC = 64: each drawn entry feeds only 64 columns) draws with 16 generator warps,
 // 2 pairs side by side (c3 shape: 0.923 -> 0.850 ms at m = 1e6); wider A keeps 8 x 4.
+#ifndef CQR_WS_GEN256
+#define CQR_WS_GEN256 kWsGen
+#endif
+#ifndef CQR_WS_MMA256
+#define CQR_WS_MMA256 kWsMma
+#endif
 #ifndef CQR_WS_GEN64
 #define CQR_WS_GEN64 16
 #endif
@@ -224,15 +230,19 @@ constexpr int kWsMma = CQR_WS_MMA;
 #endif
 template <int NPC>
 constexpr int ws_gen() {
-  return NPC == 64 ? CQR_WS_GEN64 : kWsGen;
+  return NPC == 64 ? CQR_WS_GEN64 : NPC == 256 ? CQR_WS_GEN256 : kWsGen;
 }
 template <int NPC>
 constexpr int ws_ilp() {
   return NPC == 64 ? CQR_WS_ILP64 : kWsIlp;
 }
 template <int NPC>
+constexpr int ws_mma() {
+  return NPC == 256 ? CQR_WS_MMA256 : kWsMma;
+}
+template <int NPC>
 constexpr int ws_threads() {
-  return (ws_gen<NPC>() + kWsMma) * 32;
+  return (ws_gen<NPC>() + ws_mma<NPC>()) * 32;
 }
 
 // NPC columns of A per CTA (128, or 256 for wider A with 32 Omega rows per CTA so
@@ -250,7 +260,8 @@ struct WsShape {
   static constexpr int BW = NPC <= 64 ? 8 : 16;
   static constexpr int ATILE = kKS * NPC;       // doubles per A stage (NPC/BW boxes of 32 x BW)
   static constexpr int OTILE = ST * (kKS + 4);  // doubles per Omega stage (stride 36)
-  static constexpr int NGW = NPC / (8 * kWsMma);  // 8-column groups per MMA warp
+  static constexpr int MMA = ws_mma<NPC>();
+  static constexpr int NGW = NPC / (8 * MMA);  // 8-column groups per MMA warp
   static constexpr int MGW = ST / 8;            // 8-row groups per MMA warp
   static constexpr int GEN = ws_gen<NPC>();
   static constexpr int PAIRS = ST * kKS / 2 / (GEN * 32);  // Box-Muller pairs per generator thread per step
@@ -287,15 +298,15 @@ __global__ void __launch_bounds__(ws_threads<NPC>(), 1)
   if (tid == 0) {
     for (int s = 0; s < kWsStages; ++s) {
       mbar_init(&full[s], S::GEN * 32 + 1);  // every generator thread + the TMA issuer's expect_tx
-      mbar_init(&empty[s], kWsMma);          // one elected lane per MMA warp
+      mbar_init(&empty[s], S::MMA);          // one elected lane per MMA warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_shared();
   }
   __syncthreads();
-  if (warp >= kWsMma) {
+  if (warp >= S::MMA) {
     // ---- generator warps: Omega tiles + the A tile's TMA
-    const int gt = tid - kWsMma * 32;
+    const int gt = tid - S::MMA * 32;
     // Counter state of each of this thread's pairs: pair p = (c >> 1) + pp with c = (s0 + i) m_global
     // + row0 + k (even: m_global, row0 and the chunk starts are even), so from one step to the next
     // p grows by kKS/2 and the pair's first counter word seed + (2p + 1) G by kKS G.
