@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   constexpr int HEAD = head_doubles<NP, BSMEM>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (failed(st)) return;
-  double* smem = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  // 512-byte alignment: the staging tiles' SWIZZLE_64B pattern repeats every 512 bytes (tiles sit at 2 KB steps)
+  double* smem = reinterpret_cast<double*>(smem_raw + ((512u - (smem_u32(smem_raw) & 511u)) & 511u));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, gr = lane >> 2;
   double* sD = smem;
@@ -313,7 +314,7 @@ cudaError_t launch_t(const TrisolveArgs& a, cudaStream_t s) {
       !make_tmap_2d(&tll, a.out, a.n, a.m, a.ldo, 4, kRW, CU_TENSOR_MAP_SWIZZLE_NONE) ||
       !make_tmap_2d(&tst, a.out, a.n, a.m, a.ldo, 8, kRW, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorNotSupported;
-  const size_t smem = (size_t)(head_doubles<NP, BSMEM>() + WPC * kWarpDoubles) * 8 + WPC * 16 + 1024;
+  const size_t smem = (size_t)(head_doubles<NP, BSMEM>() + WPC * kWarpDoubles) * 8 + WPC * 16 + 512;
   auto k = trisolve_tma_kernel<NP, WPC, BSMEM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -359,6 +360,12 @@ bool trisolve_tma_eligible(const TrisolveArgs& a, int np) {
          (a.ldi & 1) == 0 && (a.ldo & 1) == 0 && encode_fn() != nullptr;
 }
 
+#ifndef CQR_TRI256_WPC
+#define CQR_TRI256_WPC 16  // 16 warps fit at 512-byte alignment (2.857 -> 2.820 ms); n = 512: 13 warps 15.4 vs 12 warps 10.0
+#endif
+#ifndef CQR_TRI512_WPC
+#define CQR_TRI512_WPC 12
+#endif
 #ifndef CQR_TRI64_WPC
 #define CQR_TRI64_WPC 12
 #endif
@@ -367,8 +374,8 @@ cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s) {
     case 32: return launch_t<32, 16, true>(a, s);
     case 64: return launch_t<64, CQR_TRI64_WPC, true>(a, s);
     case 128: return launch_t<128, 12, true>(a, s);
-    case 256: return launch_t<256, 12, false>(a, s);
-    case 512: return launch_t<512, 12, false>(a, s);
+    case 256: return launch_t<256, CQR_TRI256_WPC, false>(a, s);
+    case 512: return launch_t<512, CQR_TRI512_WPC, false>(a, s);
   }
   return cudaErrorInvalidValue;
 }
