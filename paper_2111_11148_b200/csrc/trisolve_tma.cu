@@ -360,6 +360,12 @@ bool trisolve_tma_eligible(const TrisolveArgs& a, int np) {
          (a.ldi & 1) == 0 && (a.ldo & 1) == 0 && encode_fn() != nullptr;
 }
 
+#ifndef CQR_TRI128_WPC
+#define CQR_TRI128_WPC 12
+#endif
+#ifndef CQR_TRI128_BSMEM
+#define CQR_TRI128_BSMEM true
+#endif
 #ifndef CQR_TRI256_WPC
 #define CQR_TRI256_WPC 16  // 16 warps fit at 512-byte alignment (2.857 -> 2.820 ms); n = 512: 13 warps 15.4 vs 12 warps 10.0
 #endif
@@ -373,7 +379,7 @@ cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s) {
   switch (np) {
     case 32: return launch_t<32, 16, true>(a, s);
     case 64: return launch_t<64, CQR_TRI64_WPC, true>(a, s);
-    case 128: return launch_t<128, 12, true>(a, s);
+    case 128: return launch_t<128, CQR_TRI128_WPC, CQR_TRI128_BSMEM>(a, s);
     case 256: return launch_t<256, CQR_TRI256_WPC, false>(a, s);
     case 512: return launch_t<512, CQR_TRI512_WPC, false>(a, s);
   }
