@@ -15,13 +15,14 @@ for _ in range(2):
 buf = np.zeros(1024, dtype=np.int64)
 assert cq._lib().cqr_debug_lu_trace(C.c_void_p(buf.ctypes.data)) == 0
 t0 = buf[0]
-for p in range((n + 31) // 32):
+PW = int(os.environ.get("PROF_PW", 16))
+for p in range((n + PW - 1) // PW):
     b = buf[1 + 4 * p: 5 + 4 * p] - t0
     print(f"panel {p}: start {b[0]:8d}  steps done {b[1]:8d} (+{b[1]-b[0]})  U12 done {b[3]:8d} (+{b[3]-b[1]})  "
           f"DMMA done {b[2 + 4 - 4 + 0] if False else buf[3 + 4 * p] - t0:8d}")
 st = np.diff(buf[100:100 + n])
-print("cycles per pivot step (panel 0):", st[:31].tolist())
-print("mean per step, per panel:", [int(st[32 * p: 32 * p + 31].mean()) for p in range(n // 32)])
+print("cycles per pivot step (panel 0):", st[:PW - 1].tolist())
+print("mean per step, per panel:", [int(st[PW * p: PW * p + PW - 1].mean()) for p in range(n // PW)])
 sub = buf[300:300 + 8 * 32].reshape(32, 8)
 for j in range(1, 6):
     r = sub[j]
