@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 // cp.async issue work per chunk. Same tiles, same k order as gram_leaf_p_kernel:
 // bit-identical partials.
 constexpr int kGtMma = 12;
+#ifndef CQR_GRAM_CH128
+#define CQR_GRAM_CH128 64  // rows per ring stage at n in (64, 128] (16/32/64: 0.677/0.636/0.628 ms at c1)
+#endif
 constexpr int kGtThreads = (kGtMma + 1) * 32;
 
 // Stage layout (NP <= 256): NP/8 boxes of ROWS x 8 columns (64-byte rows, no swizzle). A fragment load reads
@@ -505,7 +508,7 @@ GramPlan gram_plan(long long m, int n, bool tma_ok) {
     p.wpc = kGtMma;
     p.parts = p.np == 128 ? 1 : p.np == 256 ? 3 : 11;  // 36 / 136 / 528 macros: 3, 4, 4 per warp (13 warps: 128 regs)
     p.maxt = (macros + p.wpc * p.parts - 1) / (p.wpc * p.parts);
-    p.ch = p.np == 512 ? 16 : 32;
+    p.ch = p.np == 512 ? 16 : p.np == 128 ? CQR_GRAM_CH128 : 32;
   } else if (p.np == 128 && !legacy) {  // persistent: the 36 macro tiles divide evenly over 12 warps (measured: n = 64 is faster per leaf)
     p.persistent = 1;
     p.wpc = p.np == 64 ? 10 : 12;
@@ -550,8 +553,9 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
                       narrow ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
     if (p.np == 128 && p.maxt == 1)  // the split last wave (engine gram_dev)
-      return launch_leaves_tma<128, 1, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
-    if (p.np == 128) return launch_leaves_tma<128, 3, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+      return launch_leaves_tma<128, 1, CQR_GRAM_CH128>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 128)
+      return launch_leaves_tma<128, 3, CQR_GRAM_CH128>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 256) return launch_leaves_tma<256, 4, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     return cudaErrorInvalidValue;
