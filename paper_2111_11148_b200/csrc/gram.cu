@@ -225,13 +225,9 @@ constexpr int kGtThreads = (kGtMma + 1) * 32;
 // earlier 16-column SWIZZLE_128B boxes kept all four rows in one half: four wavefronts, LSU 83%).
 // NP = 512 keeps 16-column SWIZZLE_128B boxes: 64 narrow boxes per 16-row stage from one producer lane
 // cost more than the conflicts they remove (9.31 vs 11.44 ms at m = 1e6).
-template <int NP>
-constexpr int gram_box_cols() {
-  return NP <= 256 ? 8 : 16;
-}
-template <int NP, int ROWS>
+template <int NP, int ROWS, int BW_ = (NP <= 256 ? 8 : 16)>
 struct GtShape {
-  static constexpr int BW = gram_box_cols<NP>();
+  static constexpr int BW = BW_;
   static constexpr int CHUNK = ROWS * NP;  // doubles per stage (NP/BW boxes of ROWS x BW)
   static constexpr int BOX = ROWS * BW;
   static constexpr int STAGES = CHUNK * 8 * 4 <= 200 * 1024 ? 4 : 3;
@@ -240,12 +236,12 @@ struct GtShape {
 
 // Work item w = blockIdx.x + k * gridDim.x (gridDim.x a multiple of parts): part
 // w % parts (fixed per CTA: its warps' macro-tile lists), leaf leaf0 + w / parts.
-template <int NP, int MAXT, int ROWS, bool CHECK>
+template <int NP, int MAXT, int ROWS, bool CHECK, int BW = (NP <= 256 ? 8 : 16)>
 __global__ void __launch_bounds__(kGtThreads, 1)
-    gram_leaf_tma_kernel(const __grid_constant__ CUtensorMap tmx, long long m, int parts,
+    gram_leaf_tma_kernel(const __grid_constant__ CUtensorMap tmx, int tma3, long long m, int parts,
                          const int32_t* __restrict__ tiles, double* __restrict__ partial, int leaf0, int leaf1,
                          DevStatus* st) {
-  using S = GtShape<NP, ROWS>;
+  using S = GtShape<NP, ROWS, BW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[S::STAGES], empty[S::STAGES];
   if (failed(st)) return;
@@ -277,9 +273,13 @@ __global__ void __launch_bounds__(kGtThreads, 1)
           mbar_wait(&empty[s], ((it / S::STAGES) & 1) ^ 1);
           mbar_expect_tx(&full[s], S::CHUNK * 8);
           const int row = lf * kLeafRows + c * ROWS;
+          if (tma3) {  // all NP/BW column boxes of the stage in one 3-D load
+            tma_load_3d(sm + s * S::CHUNK, &tmx, 0, row, 0, &full[s]);
+          } else {
 #pragma unroll
-          for (int b = 0; b < NP / S::BW; ++b)
-            tma_load_2d(sm + s * S::CHUNK + b * S::BOX, &tmx, S::BW * b, row, &full[s]);
+            for (int b = 0; b < NP / S::BW; ++b)
+              tma_load_2d(sm + s * S::CHUNK + b * S::BOX, &tmx, S::BW * b, row, &full[s]);
+          }
         }
       }
     }
@@ -354,21 +354,39 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   }
 }
 
+// x is encoded here: 8-column boxes (conflict-free fragment loads), one 3-D load per stage when n % 8 == 0
+// (NP = 512 needs it: 64 separate narrow boxes per stage are TMA-issue bound), else 2-D boxes
+// (16-column SWIZZLE_128B ones at NP = 512).
 template <int NP, int MAXT, int ROWS>
-cudaError_t launch_leaves_tma(const GramPlan& p, const CUtensorMap& tm, const int32_t* tiles, double* partial,
-                              int check, const DevStatus* st, cudaStream_t s, int leaf0, int leaf1, int num_sms) {
+cudaError_t launch_leaves_tma(const GramPlan& p, const double* x, long long ldx, const int32_t* tiles,
+                              double* partial, int check, const DevStatus* st, cudaStream_t s, int leaf0, int leaf1,
+                              int num_sms) {
   if (leaf1 < 0) leaf1 = p.leaves;
   if (leaf1 <= leaf0) return cudaSuccess;
-  using S = GtShape<NP, ROWS>;
-  auto k = check ? gram_leaf_tma_kernel<NP, MAXT, ROWS, true> : gram_leaf_tma_kernel<NP, MAXT, ROWS, false>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-  if (e != cudaSuccess) return e;
+  CUtensorMap tm;
+  static const bool no3d = std::getenv("CQR_GRAM_TMA2D") != nullptr;  // A/B runs
+  const bool tma3 = !no3d && p.n % 8 == 0 &&
+                    make_tmap_colblocks(&tm, x, p.n, p.m, ldx, ROWS, NP / 8, CU_TENSOR_MAP_SWIZZLE_NONE, 8);
   const long long items = (long long)(leaf1 - leaf0) * p.parts;
   const int slots = std::max(1, num_sms / p.parts) * p.parts;
   const int grid = (int)std::min<long long>(items, slots);
-  k<<<(unsigned)grid, kGtThreads, S::SMEM, s>>>(tm, p.m, p.parts, tiles, partial, leaf0, leaf1,
-                                               const_cast<DevStatus*>(st));
-  return cudaGetLastError();
+  auto run = [&](auto kfn, size_t smem) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<(unsigned)grid, kGtThreads, smem, s>>>(tm, tma3 ? 1 : 0, p.m, p.parts, tiles, partial, leaf0, leaf1,
+                                                const_cast<DevStatus*>(st));
+    return cudaGetLastError();
+  };
+  if (tma3 || NP <= 256) {
+    if (!tma3 && !make_tmap_2d(&tm, x, p.n, p.m, ldx, 8, ROWS, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    using S = GtShape<NP, ROWS, 8>;
+    return check ? run(gram_leaf_tma_kernel<NP, MAXT, ROWS, true, 8>, S::SMEM)
+                 : run(gram_leaf_tma_kernel<NP, MAXT, ROWS, false, 8>, S::SMEM);
+  }
+  if (!make_tmap_2d(&tm, x, p.n, p.m, ldx, 16, ROWS, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  using S = GtShape<NP, ROWS, 16>;
+  return check ? run(gram_leaf_tma_kernel<NP, MAXT, ROWS, true, 16>, S::SMEM)
+               : run(gram_leaf_tma_kernel<NP, MAXT, ROWS, false, 16>, S::SMEM);
 }
 
 // The pairwise tree of kernels.hpp:42-57 in streaming form: after pushing leaf
@@ -547,17 +565,12 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
                                double* partial, int vec16, int check, const DevStatus* st, cudaStream_t s, int leaf0,
                                int leaf1, int num_sms) {
   if (p.tma) {
-    CUtensorMap tm;
-    const bool narrow = p.np <= 256;  // gram_box_cols
-    if (!make_tmap_2d(&tm, x, p.n, p.m, ldx, narrow ? 8 : 16, p.ch,
-                      narrow ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B))
-      return cudaErrorInvalidValue;
     if (p.np == 128 && p.maxt == 1)  // the split last wave (engine gram_dev)
-      return launch_leaves_tma<128, 1, CQR_GRAM_CH128>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+      return launch_leaves_tma<128, 1, CQR_GRAM_CH128>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 128)
-      return launch_leaves_tma<128, 3, CQR_GRAM_CH128>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
-    if (p.np == 256) return launch_leaves_tma<256, 4, 32>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
-    if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, tm, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+      return launch_leaves_tma<128, 3, CQR_GRAM_CH128>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 256) return launch_leaves_tma<256, 4, 32>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     return cudaErrorInvalidValue;
   }
   if (p.persistent) {
