@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 // cp.async issue work per chunk. Same tiles, same k order as gram_leaf_p_kernel:
 // bit-identical partials.
 constexpr int kGtMma = 12;
+#ifndef CQR_GRAM_CH256
+#define CQR_GRAM_CH256 32  // rows per ring stage at n in (128, 256] (16 rows: 2.32 vs 2.30 ms)
+#endif
 #ifndef CQR_GRAM_CH128
 #define CQR_GRAM_CH128 64  // rows per ring stage at n in (64, 128] (16/32/64: 0.677/0.636/0.628 ms at c1)
 #endif
@@ -526,7 +529,7 @@ GramPlan gram_plan(long long m, int n, bool tma_ok) {
     p.wpc = kGtMma;
     p.parts = p.np == 128 ? 1 : p.np == 256 ? 3 : 11;  // 36 / 136 / 528 macros: 3, 4, 4 per warp (13 warps: 128 regs)
     p.maxt = (macros + p.wpc * p.parts - 1) / (p.wpc * p.parts);
-    p.ch = p.np == 512 ? 16 : p.np == 128 ? CQR_GRAM_CH128 : 32;
+    p.ch = p.np == 512 ? 16 : p.np == 128 ? CQR_GRAM_CH128 : CQR_GRAM_CH256;
   } else if (p.np == 128 && !legacy) {  // persistent: the 36 macro tiles divide evenly over 12 warps (measured: n = 64 is faster per leaf)
     p.persistent = 1;
     p.wpc = p.np == 64 ? 10 : 12;
@@ -569,7 +572,7 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
       return launch_leaves_tma<128, 1, CQR_GRAM_CH128>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 128)
       return launch_leaves_tma<128, 3, CQR_GRAM_CH128>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
-    if (p.np == 256) return launch_leaves_tma<256, 4, 32>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 256) return launch_leaves_tma<256, 4, CQR_GRAM_CH256>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     return cudaErrorInvalidValue;
   }
