@@ -1,23 +1,39 @@
 """bench.py — rQR/rLU-CholeskyQR fp64 on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], "c1"): rLU-CholeskyQR, m = 1,000,000 rows
-per GPU, n = 128, Gaussian sketch s = 2n = 256, A = U diag(sigma) V^T with
-sigma log-spaced 1 .. 1e-14 (cond 1e14). Synthetic, seeded; U from a QR of a
-torch Gaussian on the device, V from a numpy QR (input generation is outside
-the timed region). N > 1: weak scaling, one 1e6-row block per rank
-(parexec.cpp:9-18), partials summed with NCCL.
+Workload (BASELINE.json configs[1], "c1", the default): rLU-CholeskyQR with a
+Gaussian sketch, m = 1,000,000 rows per GPU, n = 128, s = 2n = 256,
+A = U diag(sigma) V^T with sigma log-spaced 1 .. 1e-14 (cond 1e14). Synthetic
+and seeded: A is generated on the device by the library's matgen
+(cqr_synthesize_dev, matgen.cpp:21-46 restated: counter-RNG Gaussians from
+derive(1, 0/1), orthonormalised); the sketch seed is derive(1, 0x5E7C)
+(experiments.cpp:94). Input generation is outside the timed region.
 
-One step = one full factorization (sketch, LU, two trisolves, Gram, Cholesky,
-recover) through the C-ABI on the HBM-resident A. value = algorithmic TFLOP/s
-of the whole job; ms_per_step = ms per factorization.
+  --workload c2   rQR-Gaussian, m = 4e6 FIXED, n = 256, s = 512, cond 1e12: strong
+                  scaling, rank b owns rows [ceil(b m/p), ceil((b+1) m/p)) (parexec.cpp:13-15)
+  --workload c3   rQR-Gaussian, 4,194,304 rows PER GPU, n = 64, s = 128, cond 1e15: weak scaling
+  --workload c4   rLU-Gaussian, m = 1e6, n = 512, s = 768, two-segment sigma (strong)
+  c1              1e6 rows per GPU (weak) -- BASELINE.json runs it on 1 B200
 
---impl reference: the CPU oracle port of the reference (oracle/, the
-reference itself cannot be built here: no Eigen) on the host cores, rank 0
-only, on a bounded row sample of the same workload.
+One step = one full factorization (sketch, LU/QR, two trisolves, Gram,
+Cholesky, recover) through the C-ABI on the HBM-resident A. value = algorithmic
+TFLOP/s of the whole job (all ranks); ms_per_step = ms per factorization (max
+over ranks, CUDA events on the library's stream). e2e = the same factorization
+through the host-buffer C-ABI (cqr_factor / cqr_factor_sharded): H2D of A and
+D2H of Q and R inside the timed region.
+
+--gpus N without WORLD_SIZE in the environment re-launches this script under
+torch.distributed.run (one process per GPU, 127.0.0.1, NCCL_DEBUG=INFO so the
+log shows the ranks); with WORLD_SIZE set it must equal N.
+
+--impl reference: the CPU oracle port of the reference (oracle/; the reference
+itself cannot be built here or on the GPU box: no Eigen) on the host cores,
+rank 0 only, on a bounded row sample of the same workload per step.
 """
 import argparse
 import json
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -27,54 +43,61 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-M_PER_GPU = 1_000_000
 N = 128
 RATE = 2.0
 KAPPA = 1e14
 SEED = 1
-CPU_SAMPLE_ROWS = 100_000
-WORKLOAD = "c1: rLU-CholeskyQR fp64, m=1e6 rows/GPU, n=128, Gaussian sketch s=256, cond 1e14"
-# BASELINE.json configs (per-GPU shapes; c1 is the benchmark line, the others via --workload):
-# name -> (method name, m per GPU, n, sketch rows l, kappa or "two-segment", description)
+REF_SAMPLE_ROWS = 100_000  # --impl reference: rows of the per-step CPU sample
+METRIC = "rQR/rLU-CholeskyQR fp64 TFLOP/s (ms/factorization in ms_per_step)"
+# BASELINE.json configs: name -> (method, rows, per_gpu (weak) or fixed global (strong), n, l, kappa, description)
 WORKLOADS = {
-    "c1": ("rlu", M_PER_GPU, N, 256, KAPPA, WORKLOAD),
-    "c2": ("rqr-gaussian", 4_000_000, 256, 512, 1e12,
-           "c2: rQR-CholeskyQR (Gaussian) fp64, m=4e6 rows/GPU, n=256, s=512, cond 1e12"),
-    "c3": ("rqr-gaussian", 4_194_304, 64, 128, 1e15,
+    "c1": ("rlu", 1_000_000, True, N, 256, KAPPA,
+           "c1: rLU-CholeskyQR (Gaussian) fp64, m=1e6 rows/GPU, n=128, s=256, cond 1e14"),
+    "c2": ("rqr-gaussian", 4_000_000, False, 256, 512, 1e12,
+           "c2: rQR-CholeskyQR (Gaussian) fp64, m=4e6 (fixed, row blocks ceil(b*m/p)), n=256, s=512, cond 1e12"),
+    "c3": ("rqr-gaussian", 4_194_304, True, 64, 128, 1e15,
            "c3: rQR-CholeskyQR (Gaussian) fp64, m=4194304 rows/GPU, n=64, s=128, cond 1e15"),
-    "c4": ("rlu", 1_000_000, 512, 768, "two-segment",
-           "c4: rLU-CholeskyQR (Gaussian) fp64, m=1e6 rows/GPU, n=512, s=768, sigma 10^(-8i/255) then 1e-8"),
+    "c4": ("rlu", 1_000_000, False, 512, 768, "two-segment",
+           "c4: rLU-CholeskyQR (Gaussian) fp64, m=1e6, n=512, s=768, sigma 10^(-8i/255) then 1e-8"),
 }
+FP64_PEAK = {"value": 37.1, "src": "builder-measured: DMMA m8n8k4 FP64 peak of this B200 pool "
+             "(tools/probe/fp64_probe.cu, profiles/r01_fp64_probe.txt); MEASURED_PEAKS.json has no FP64 entry"}
 
 
 def workload_sigma(n, kappa):
     import numpy as np
 
-    if kappa == "two-segment":  # BASELINE.json c4
+    if kappa == "two-segment":  # BASELINE.json configs[4]
         s = np.full(n, 1e-8)
         s[:256] = 10.0 ** (-8.0 * np.arange(256) / 255.0)
         return s
-    from paper_2111_11148_b200 import cholqr as cq
+    sig = np.ones(n)
+    if n > 1:  # matgen.cpp:27-31
+        sig[1:] = np.exp(-np.log(kappa) * np.arange(1, n) / (n - 1))
+    return sig
 
-    return cq.geometric_sigma(n, kappa)
 
-
-def flops_rlu(m, n, l):
-    """Algorithmic flops of one rLU-CholeskyQR factorization."""
+def flops_factorization(method, m, n, l):
+    """Algorithmic flops of one rQR/rLU-CholeskyQR factorization: sketch
+    2lmn, two tall solves 2mn^2, Gram mn(n+1), plus the small factorizations."""
     tall = 2.0 * l * m * n + 2.0 * m * n * n + m * n * (n + 1)
-    small = (l * n * n - n ** 3 / 3.0) + n ** 3 / 3.0 + n ** 3 / 3.0  # LU, Cholesky, recover
-    return tall + small
+    pre = (2.0 if method.startswith("rqr") else 1.0) * (l * n * n - n ** 3 / 3.0)  # QR 2n^2(l-n/3), LU n^2(l-n/3)
+    return tall + pre + n ** 3 / 3.0 + n ** 3 / 3.0  # + Cholesky + recover
 
 
-def peaks():
-    p = {"hbm_gbs": None, "fp64_tflops": 37.1, "fp64_src": "measured DMMA m8n8k4 peak, tools/probe/fp64_probe.cu "
-         "(profiles/r01_fp64_probe.txt); MEASURED_PEAKS.json has no FP64 entry"}
+def flops_cholqr_family(method, m, n):
+    passes = {"cholqr": 1, "cholqr2": 2, "scholqr3": 3}[method]
+    return passes * (m * n * (n + 1) + m * n * n + n ** 3 / 3.0) + (passes - 1) * n ** 3 / 3.0
+
+
+def cpu_model():
     try:
-        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        p["hbm_gbs"] = mp.get("hbm_gbs")
-    except Exception:
-        p["hbm_gbs"] = 6650.0
-    return p
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -124,22 +147,33 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_input(m_local, n, rank, world, device, kappa=None, ctx=None, sigma=None):
-    """Rows [rank*m_local, (rank+1)*m_local) of A = U diag(sigma) V^T, generated on
-    the device by the library (matgen.cpp:21-46 restated: counter-RNG Gaussians,
-    seeds derive(SEED, 0/1), orthonormalised across all ranks)."""
-    from paper_2111_11148_b200 import cholqr as cq
+def shard(m_global, world, rank):
+    """(row0, rows) of rank's block, ceil(b*m/p) offsets (parexec.cpp:13-15)."""
+    lo = -(-rank * m_global // world)
+    hi = -(-(rank + 1) * m_global // world)
+    return lo, hi - lo
 
-    if ctx is None:
-        from paper_2111_11148_b200 import dist
 
-        ctx = dist.make_context(device.index if hasattr(device, "index") else int(device), rank, world)
-    k = KAPPA if kappa is None else kappa
-    return cq.synthesize_dev(m_local, n, k, SEED, sigma=sigma, device=ctx.device, m_global=m_local * world,
-                             row0=rank * m_local, ctx=ctx)
+def workload_shape(name, world, rank):
+    mname, rows, weak, n, l, kap, desc = WORKLOADS[name]
+    m_global = rows * world if weak else rows
+    row0, m_local = shard(m_global, world, rank)
+    return mname, m_global, row0, m_local, n, l, kap, desc, weak
+
+
+def traffic_for(workload):
+    """dram read+write bytes per launch of the workload's dominant kernel, from the
+    committed ncu capture (profiles/traffic.json, written by tools/traffic_summary.py)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return d[workload]
+    except Exception:
+        return None
 
 
 def run_ours(args):
+    import ctypes as C
+
     import numpy as np
     import torch
     import torch.distributed as td
@@ -156,15 +190,15 @@ def run_ours(args):
     if world > 1:
         td.init_process_group("nccl", device_id=dev)
     ctx = dist.make_context(local, rank, world)
-    mname, m_local, n, l_req, kap, wdesc = WORKLOADS[args.workload]
+    mname, m_global, row0, m_local, n, l_req, kap, wdesc, weak = workload_shape(args.workload, world, rank)
     method = {v: k for k, v in _abi.METHOD_NAMES.items()}[mname]
-    m_global = m_local * world
-    row0 = rank * m_local
-    a = make_input(m_local, n, rank, world, dev, ctx=ctx, sigma=workload_sigma(n, kap))
+    a = cq.synthesize_dev(m_local, n, seed=SEED, sigma=workload_sigma(n, kap), m_global=m_global, row0=row0,
+                          ctx=ctx)
     q = torch.empty_like(a)
-    cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, size=l_req, rate=RATE, seed=_seed_value())
+    cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, size=l_req, rate=RATE, seed=cq.derive(SEED, 0x5E7C))
     l = cfg.resolved_size(m_global, n)
     opts = _abi.options()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
 
     def step():
         return dist.factor_sharded(ctx, method, a, m_global, row0, cfg, opts, q_out=q)
@@ -176,7 +210,6 @@ def run_ours(args):
     orth = cq.orthogonality_error_dev(q, ctx)  # sharded: Gram of Q summed over the ranks
     res = cq.residual_error_dev(a, q, r, ctx)
 
-    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sketch_ms, stage_tot = [], np.zeros(_abi.STAGE_COUNT)
     if world > 1:
@@ -198,9 +231,8 @@ def run_ours(args):
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         td.all_reduce(t, op=td.ReduceOp.MAX)
-    ms = float(t.item())
-    ms_step = ms / args.steps
-    total_flops = flops_rlu(m_global, n, l)
+    ms_step = float(t.item()) / args.steps
+    total_flops = flops_factorization(mname, m_global, n, l)
     value = total_flops / (ms_step * 1e-3) / 1e12
 
     # e2e through the public host-buffer API (H2D of A, factorization, D2H of Q and R):
@@ -213,7 +245,6 @@ def run_ours(args):
     cfg_c = cfg._c()
 
     def e2e_step():
-        import ctypes as C
         if world == 1:
             st = cq._lib().cqr_factor(ctx.h, method, C.c_void_p(an.ctypes.data), m_local, n, n, C.byref(cfg_c),
                                       C.byref(opts), C.c_void_p(qn.ctypes.data), n, cq._ptr(rh), n, C.byref(rep2))
@@ -239,40 +270,49 @@ def run_ours(args):
     e2e = {"value": total_flops / te / 1e12, "unit": "TFLOP/s", "ms_per_step": te * 1e3,
            "h2d_bytes_per_step": int(8 * m_global * n), "d2h_bytes_per_step": int(8 * m_global * n + 8 * n * n * world),
            "api": "cqr_factor (host pinned buffers)" if world == 1 else
-                  "cqr_factor_sharded per rank (host pinned buffers), max over ranks"}
+                  "cqr_factor_sharded per rank (host pinned buffers), max over ranks",
+           "timer": "host wall clock around blocking calls, max over ranks"}
 
-    pk = peaks()
     sk_ms = statistics.mean(sketch_ms)
     sk_flops = 2.0 * l * m_local * n
     achieved = sk_flops / (sk_ms * 1e-3) / 1e12
-    roof = {"kernel": "sketch_ws_kernel (8 Box-Muller warps + 8 DMMA warps) + sketch_reduce (Sketch stage)",
-            "bound": "tensor",
-            "achieved": achieved, "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"],
-            "peak_src": pk["fp64_src"], "algorithmic": f"2*l*m*n flops per launch (l={l}, m={m_local}, n={n}); "
-            "Omega generation (l*m Gaussian draws) is extra work not counted",
-            "traffic": _traffic() if args.workload == "c1" else None}
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample(a, l, CPU_SAMPLE_ROWS, method, mname)
-    stage_avg = {cq_name: float(v / args.steps) for cq_name, v in zip(_abi.STAGE_NAMES, stage_tot)}
+    roof = {"kernel": "sketch (warp-specialised DMMA kernel + fixed-order reduce; Sketch stage events)",
+            "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK["value"], "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK["value"], "peak_src": FP64_PEAK["src"],
+            "algorithmic": f"2*l*m*n flops per launch (l={l}, m={m_local}, n={n}); the l*m Gaussian draws of "
+                           "Omega are extra FP64-pipe work, not counted",
+            "traffic": traffic_for(args.workload)}
+    stage_avg = {nm: float(v / args.steps) for nm, v in zip(_abi.STAGE_NAMES, stage_tot)}
     # per stage: algorithmic flops of this rank's part / CUDA-event stage time, vs the DMMA peak
     qr = mname.startswith("rqr")
     st_flops = {"sketch": 2.0 * l * m_local * n, "precondition": (2.0 if qr else 1.0) * (l * n * n - n ** 3 / 3.0),
                 "gram": float(m_local) * n * (n + 1), "cholesky": n ** 3 / 3.0, "trisolve": 2.0 * m_local * n * n,
                 "recover": n ** 3 / 3.0}
     stage_roof = {k: {"tflops": f / (stage_avg[k] * 1e-3) / 1e12, "frac": f / (stage_avg[k] * 1e-3) / 1e12 /
-                      pk["fp64_tflops"]} for k, f in st_flops.items() if stage_avg.get(k, 0.0) > 0.0}
-    line = {"metric": "rQR/rLU-CholeskyQR fp64 TFLOP/s (ms/factorization in ms_per_step)", "value": value,
-            "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      FP64_PEAK["value"]} for k, f in st_flops.items() if stage_avg.get(k, 0.0) > 0.0}
+
+    comparison = None
+    if args.workload == "c1" and not args.no_compare:
+        comparison = compare_methods(ctx, a, m_global, row0, n, args, stream, dev, world)
+
+    cpu = None
+    if not args.no_cpu:
+        # the oracle on the whole c1 A of rank 0 (the same bytes), after the timed regions
+        cpu = cpu_baseline(a, m_local, n, l, method, mname) if (rank == 0 and args.workload == "c1") else None
+    if world > 1:
+        td.barrier()
+    line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: A = U diag(sigma) V^T generated on the device (matgen.cpp restated), "
                     + ("sigma log-spaced 1..1/kappa" if kap != "two-segment" else "c4 two-segment spectrum"),
-            "config": {"workload": wdesc, "method": mname, "sketch": "gaussian", "m_per_gpu": m_local,
-                       "m_global": m_global, "n": n, "l": l, "kappa": kap,
+            "config": {"workload": wdesc, "method": mname, "sketch": "gaussian", "m_global": m_global,
+                       "m_per_gpu": m_local if weak else None, "n": n, "l": l, "kappa": kap,
                        "l2": f"inputs larger than L2 ({8 * m_local * n / 1e9:.2f} GB per GPU vs 126 MB L2), no flush",
-                       "parallelism": f"row-block dp{world}"},
+                       "parallelism": f"row-block dp{world}" + ("" if weak else " (strong: fixed m, ceil(b*m/p) blocks)")},
             "stage_ms": stage_avg, "clocks": clk.summary(), "gpu_launches": launches,
             "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "comparison": comparison,
             "check": {"orth": orth, "res": res, "sketch_rows": rep.sketch_rows}}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -280,47 +320,82 @@ def run_ours(args):
         td.destroy_process_group()
 
 
-def _traffic():
-    p = os.path.join(ROOT, "profiles", "sketch_traffic.json")
-    try:
-        return json.load(open(p))["bytes_per_launch"]
-    except Exception:
-        return None
+def compare_methods(ctx, a, m_global, row0, n, args, stream, dev, world):
+    """BASELINE.json configs[1]: CholeskyQR2 and shifted CholeskyQR3 (fixed shift 1e-15,
+    experiments.hpp:52) on the same A. CholeskyQR2 breaks down at cond 1e14 (its time is
+    the time to the breakdown verdict)."""
+    import torch
+    import torch.distributed as td
+
+    from paper_2111_11148_b200 import _abi
+    from paper_2111_11148_b200 import cholqr as cq
+    from paper_2111_11148_b200 import dist
+
+    out = {}
+    fixed = _abi.options(shift_kind=_abi.SHIFT_FIXED, shift_value=1e-15)
+    q = torch.empty_like(a)
+    for name, meth in (("cholqr2", _abi.CHOLQR2), ("scholqr3", _abi.SCHOLQR3)):
+        status, pivot = "ok", None
+
+        def one():
+            nonlocal status, pivot
+            try:
+                dist.factor_sharded(ctx, meth, a, m_global, row0, None, fixed, q_out=q)
+            except cq.CholeskyBreakdown as e:
+                status, pivot = "breakdown", e.pivot_index
+
+        one()
+        k = max(3, min(args.steps, 10))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            td.barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(k):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([e0.elapsed_time(e1) / k], device=dev, dtype=torch.float64)
+        if world > 1:
+            td.all_reduce(t, op=td.ReduceOp.MAX)
+        ms = float(t.item())
+        d = {"status": status, "ms_per_factorization": ms, "shift": "fixed 1e-15"}
+        if status == "ok":
+            d["tflops"] = flops_cholqr_family(name, m_global, n) / (ms * 1e-3) / 1e12
+            _, r, _ = dist.factor_sharded(ctx, meth, a, m_global, row0, None, fixed, q_out=q)
+            d["orth"] = cq.orthogonality_error_dev(q, ctx)
+            d["res"] = cq.residual_error_dev(a, q, r, ctx)
+        else:
+            d["pivot_index"] = pivot
+        out[name] = d
+    return out
 
 
-def cpu_baseline_sample(a_dev, l, rows, method=None, mname="rlu"):
-    """Oracle (CPU port of the reference) on the first `rows` rows of the same A."""
+def cpu_baseline(a_dev, m, n, l, method, mname):
+    """The oracle (CPU port of the reference) on the SAME A bytes as the GPU arm, the
+    whole c1 shape: serial Gaussian sketch as sketch.cpp:94-116, Gram and trisolves on
+    all host cores as parexec's workers."""
     import numpy as np
 
     from oracle import oracle as o
     from paper_2111_11148_b200 import _abi
 
-    a = np.ascontiguousarray(a_dev[:rows].cpu().numpy())
+    a = np.ascontiguousarray(a_dev.cpu().numpy())
     cores = os.cpu_count() or 1
-    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, size=l, rate=RATE, seed=_seed_value())
+    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, size=l, rate=RATE, seed=o.derive(SEED, 0x5E7C))
+    o.set_test_threads(1)
     t0 = time.perf_counter()
-    o.factor(_abi.RLU if method is None else method, a, cfg, _abi.options(), workers=cores)
+    f = o.factor(method, a, cfg, _abi.options(), workers=cores)
     dt = time.perf_counter() - t0
-    fl = flops_rlu(rows, a.shape[1], l)
-    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-            "sample": f"one {mname} factorization of the first {rows} rows (n={a.shape[1]}, l={l}); "
-                      f"{dt:.2f} s; sketch serial as in sketch.cpp:94-116, Gram/trisolve on {cores} workers"}
-
-
-def _seed_value():
-    # derive(SEED, 0x5E7C) (experiments.cpp:94), computed with the product's own host RNG
-    m64 = (1 << 64) - 1
-
-    def mix(z):
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m64
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m64
-        return z ^ (z >> 31)
-
-    return mix(SEED ^ mix((0x5E7C + 0x51ED270B8A5EC473) & m64))
+    stage_s = {nm: f.report.stage_ms[i] / 1e3 for i, nm in enumerate(_abi.STAGE_NAMES) if f.report.stage_ms[i] > 0}
+    return {"value": flops_factorization(mname, m, n, l) / dt / 1e12, "unit": "TFLOP/s", "cores": cores,
+            "kind": "port", "cpu": cpu_model(), "seconds": dt, "stage_s": stage_s,
+            "sample": f"one {mname} factorization of the full c1 A (the GPU arm's bytes, {m} x {n}, l={l}); "
+                      f"sketch serial as sketch.cpp:94-116, Gram/trisolves on {cores} workers"}
 
 
 def run_reference(args):
-    """--impl reference: the oracle port on all host cores, rank 0 only."""
+    """--impl reference: the oracle port on the host cores, rank 0 only."""
     import numpy as np
 
     rank = int(os.environ.get("RANK", "0"))
@@ -329,51 +404,86 @@ def run_reference(args):
     from oracle import oracle as o
     from paper_2111_11148_b200 import _abi
 
-    mname, _, n, l, kap, wdesc = WORKLOADS[args.workload]
+    mname, _, _, n, l, kap, wdesc = WORKLOADS[args.workload]
     method = {v: k for k, v in _abi.METHOD_NAMES.items()}[mname]
-    rows = CPU_SAMPLE_ROWS
-    rs = np.random.default_rng(SEED)
-    u, _ = np.linalg.qr(rs.standard_normal((rows, n)))
-    v, _ = np.linalg.qr(rs.standard_normal((n, n)))
-    sigma = workload_sigma(n, kap)
-    a = np.ascontiguousarray(u @ (sigma[:, None] * v.T))
+    rows = REF_SAMPLE_ROWS
+    # the sample is the first `rows` rows of the reference's own generator applied to the workload's
+    # spectrum (matgen.cpp:21-46 restated in the oracle), not our device generator
+    a = o.synthesize(rows, n, 1.0, SEED, sigma=workload_sigma(n, kap))
     cores = os.cpu_count() or 1
-    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, size=l, rate=RATE, seed=_seed_value())
+    cfg = _abi.sketch_cfg(strategy=_abi.GAUSSIAN, size=l, rate=RATE, seed=o.derive(SEED, 0x5E7C))
+    o.set_test_threads(1)
     for _ in range(args.warmup):
         o.factor(method, a, cfg, _abi.options(), workers=cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         o.factor(method, a, cfg, _abi.options(), workers=cores)
     dt = (time.perf_counter() - t0) / args.steps
-    value = flops_rlu(rows, n, l) / dt / 1e12
-    line = {"impl": "reference", "metric": "rQR/rLU-CholeskyQR fp64 TFLOP/s (ms/factorization in ms_per_step)",
+    value = flops_factorization(mname, rows, n, l) / dt / 1e12
+    line = {"impl": "reference", "metric": METRIC,
             "value": value, "unit": "TFLOP/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wdesc, "method": mname, "sketch": "gaussian", "n": n, "l": l,
                        "kappa": kap, "sample_rows": rows},
-            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                             "sample": f"{mname} of a {rows} x {n} sample per step (the reference is "
-                                       "not buildable here: no Eigen); serial Gaussian sketch as the reference"},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port", "cpu": cpu_model(),
+                             "sample": f"{mname} of a {rows} x {n} sample per step (the reference is not buildable "
+                                       "here or on the GPU box: no Eigen); serial Gaussian sketch as the reference, "
+                                       f"Gram/trisolves on {cores} workers"},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def main():
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_cmd(argv, gpus):
+    """torch.distributed.run command that runs this script once per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-compare", action="store_true", help="skip the CholeskyQR2 / sCholeskyQR3 arms (c1)")
+    ap.add_argument("--dry-run", action="store_true", help="print the multi-GPU launch command and exit")
     ap.add_argument("--workload", default="c1", choices=sorted(WORKLOADS),
                     help="BASELINE.json config (c1, the benchmark line, by default)")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        cmd = launch_cmd(argv, args.gpus)
+        if args.dry_run:
+            print(json.dumps({"launch": cmd}))
+            return 0
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        return subprocess.call(cmd, env=env)
+    if world is not None and int(world) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        print(json.dumps({"launch": None, "world": args.gpus}))
+        return 0
     if args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

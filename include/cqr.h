@@ -87,7 +87,8 @@ typedef struct {
   int32_t r_less;      /* skip R */
   int32_t shift_kind;  /* cqr_shift_kind; default CQR_SHIFT_THEORY */
   double shift_value;  /* used when shift_kind == CQR_SHIFT_FIXED */
-  int32_t workers;     /* accepted for API parity; device work is not split by it */
+  int32_t workers;     /* p of parexec::run_parallel: must be in [0, m] (0 = 1); sets the comm-model
+                          counters of a one-process call; device work is not split by it */
 } cqr_options;
 
 /* cholqr::StageInfo, cholqr.hpp:25-34 (optionals carried as has_* flags). */

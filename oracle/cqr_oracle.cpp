@@ -9,6 +9,7 @@
 #include "cqr_oracle.h"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -154,6 +155,14 @@ Mat sample_rows_uniform(const Mat& a, Index l, bool without, Stream& s, std::vec
 // sketch.cpp:94-116. Omega(i, j) = gaussian_at(seed, i*m + j), generated in
 // 2048-column chunks; fixed order: for each chunk, t(i,c) = fma-chain over the
 // chunk's rows in ascending order starting from 0, then a1(i,c) += t(i,c).
+// Test-harness knob (orc_set_test_threads): the reference's sketch is serial
+// (sketch.cpp:94-116) and so is this one by default (bench.py's CPU arm keeps it
+// so); the parity tests may split the sketch rows i, and the diagnostics' Gram
+// leaves and residual panels, over threads. Each a1(i, :) is computed by one thread
+// with exactly the serial arithmetic (chunks ascending, rows ascending inside a
+// chunk), so the result is bitwise the same for any thread count.
+std::atomic<int> g_test_threads{1};
+
 Mat sketch_gaussian(const Mat& a, Index l, uint64_t seed, Index m_global = -1, Index row0 = 0) {
   // m_global/row0: a row block of a larger matrix (counters use global rows,
   // the decomposition the multi-GPU path relies on)
@@ -161,25 +170,27 @@ Mat sketch_gaussian(const Mat& a, Index l, uint64_t seed, Index m_global = -1, I
   const Index mg = m_global < 0 ? m : m_global;
   Mat a1(l, n);
   constexpr Index kChunk = 2048;
-  std::vector<double> omega(static_cast<size_t>(l * std::min(m, kChunk)));
-  std::vector<double> t(static_cast<size_t>(n));
-  for (Index j0 = 0; j0 < m; j0 += kChunk) {
-    const Index len = std::min(m - j0, kChunk);
-    for (Index i = 0; i < l; ++i)
-      for (Index jj = 0; jj < len; ++jj)
-        omega[static_cast<size_t>(i * len + jj)] = gaussian_at(seed, static_cast<uint64_t>(i * mg + row0 + j0 + jj));
-    for (Index i = 0; i < l; ++i) {
-      std::fill(t.begin(), t.end(), 0.0);
-      const double* om = omega.data() + i * len;
-      for (Index jj = 0; jj < len; ++jj) {
-        const double w = om[jj];
-        const double* ar = a.row(j0 + jj);
-        for (Index c = 0; c < n; ++c) t[c] = std::fma(w, ar[c], t[c]);
-      }
+  const int workers = static_cast<int>(std::max<Index>(1, std::min<Index>(g_test_threads.load(), l)));
+  run_on_workers(workers, [&](int w) {
+    std::vector<double> omega(static_cast<size_t>(std::min(m, kChunk)));
+    std::vector<double> t(static_cast<size_t>(n));
+    const Index i0 = l * w / workers, i1 = l * (w + 1) / workers;
+    for (Index i = i0; i < i1; ++i) {
       double* out = a1.row(i);
-      for (Index c = 0; c < n; ++c) out[c] += t[c];
+      for (Index j0 = 0; j0 < m; j0 += kChunk) {
+        const Index len = std::min(m - j0, kChunk);
+        for (Index jj = 0; jj < len; ++jj)
+          omega[static_cast<size_t>(jj)] = gaussian_at(seed, static_cast<uint64_t>(i * mg + row0 + j0 + jj));
+        std::fill(t.begin(), t.end(), 0.0);
+        for (Index jj = 0; jj < len; ++jj) {
+          const double wv = omega[static_cast<size_t>(jj)];
+          const double* ar = a.row(j0 + jj);
+          for (Index c = 0; c < n; ++c) t[c] = std::fma(wv, ar[c], t[c]);
+        }
+        for (Index c = 0; c < n; ++c) out[c] += t[c];
+      }
     }
-  }
+  });
   return a1;
 }
 
@@ -611,14 +622,24 @@ struct Engine {  // engine.cpp:45-74: owns a copy of A mutated in place A->X->Q
   }
 };
 
-// engine.cpp:78-92. `shift_from_trace`: theory shift resolved from trace(G) of
-// this pass (exact-arithmetic equal to ||A||_F^2 of cholqr.cpp:21-26; saves the
-// extra pass over A; the B200 engine does the same).
+// engine.cpp:78-92 with the shift of cholqr.cpp:21-26 already resolved by the
+// caller (engine.cpp:270 resolves the theory shift from a.squaredNorm() before
+// the first pass).
 struct ShiftSpec {
   bool enabled = false;
-  bool theory = false;
   double value = 0;
 };
+
+// Eigen's a.squaredNorm() (engine.cpp:270): the sum of the squared entries.
+// Eigen does not pin the order; this restatement sums row-major, sequentially.
+// (The B200 engine takes trace(G1) of the first Gram instead -- the same number
+// in exact arithmetic, without the extra pass over A -- so the sCholQR3-theory
+// parity test is a tolerance test.)
+double squared_norm(const Mat& a) {
+  double s = 0.0;
+  for (const double v : a.v) s += v * v;
+  return s;
+}
 
 double theory_shift(Index m, Index n, double fro2) {  // cholqr.cpp:21-26
   const double mn = static_cast<double>(m) * static_cast<double>(n);
@@ -635,11 +656,6 @@ Mat cholesky_pass(Engine& eng, Fact& f, ShiftSpec shift = {}) {
     Scoped t(eng.clock, CQR_STAGE_CHOLESKY);
     if (shift.enabled) {
       applied = shift.value;
-      if (shift.theory) {
-        double tr = 0.0;
-        for (Index j = 0; j < g.rows; ++j) tr += g(j, j);
-        applied = theory_shift(eng.work.rows, eng.work.cols, tr);
-      }
       for (Index j = 0; j < g.rows; ++j) g(j, j) += applied;
     }
     r = cholesky_upper(g);
@@ -804,8 +820,7 @@ Fact run_method(int method, const Mat& a, int p, const cqr_sketch_cfg& sk, const
     case CQR_SCHOLQR3: {  // engine.cpp:268-284
       ShiftSpec sh;
       sh.enabled = true;
-      sh.theory = o.shift_kind == CQR_SHIFT_THEORY;
-      sh.value = o.shift_value;
+      sh.value = o.shift_kind == CQR_SHIFT_THEORY ? theory_shift(a.rows, a.cols, squared_norm(a)) : o.shift_value;
       Engine eng(a, p, clock);
       Fact f;
       const Mat r1 = cholesky_pass(eng, f, sh);
@@ -993,6 +1008,8 @@ int orc_sample_rows_uniform(const double* a, int64_t m, int64_t n, int64_t lda, 
   });
 }
 
+void orc_set_test_threads(int w) { g_test_threads.store(w < 1 ? 1 : w); }
+
 int orc_sketch_gaussian(const double* a, int64_t m, int64_t n, int64_t lda, int64_t l, uint64_t seed,
                         double* a1) {
   return guarded([&] { store(sketch_gaussian(from_strided(a, m, n, lda), l, seed), a1); });
@@ -1120,7 +1137,7 @@ int orc_precond_factor(const double* a, int64_t m, int64_t n, int64_t lda, cqr_p
 }
 
 double orc_orthogonality_error(const double* q, int64_t m, int64_t n) {  // diagnostics.cpp:10-14
-  Mat g = gram(q, m, n, n, 1);
+  Mat g = gram(q, m, n, n, g_test_threads.load());  // leaves over threads: bitwise the same G
   double s = 0.0;
   for (Index i = 0; i < n; ++i)
     for (Index j = 0; j < n; ++j) {
@@ -1136,20 +1153,27 @@ double orc_residual_error(const double* a, const double* q, const double* r, int
   for (int64_t e = 0; e < m * n; ++e) na = std::fma(a[e], a[e], na);
   na = std::sqrt(na);
   if (na == 0.0) return std::numeric_limits<double>::quiet_NaN();
-  double acc = 0.0;
   constexpr int64_t kPanel = 4096;
-  for (int64_t p0 = 0; p0 < m; p0 += kPanel) {
-    const int64_t len = std::min(m - p0, kPanel);
-    double s = 0.0;
-    for (int64_t i = p0; i < p0 + len; ++i)
-      for (int64_t j = 0; j < n; ++j) {
-        double qr = 0.0;
-        for (int64_t k = 0; k < n; ++k) qr = std::fma(q[i * n + k], r[k * n + j], qr);
-        const double d = a[i * n + j] - qr;
-        s = std::fma(d, d, s);
-      }
-    acc += s;
-  }
+  const int64_t panels = (m + kPanel - 1) / kPanel;
+  std::vector<double> ps(static_cast<size_t>(panels));
+  // panel sums in parallel (test-harness threads), accumulated in panel order: the same bits
+  const int workers = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g_test_threads.load(), panels)));
+  run_on_workers(workers, [&](int w) {
+    for (int64_t pi = panels * w / workers; pi < panels * (w + 1) / workers; ++pi) {
+      const int64_t p0 = pi * kPanel, len = std::min(m - p0, kPanel);
+      double s = 0.0;
+      for (int64_t i = p0; i < p0 + len; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+          double qr = 0.0;
+          for (int64_t k = 0; k < n; ++k) qr = std::fma(q[i * n + k], r[k * n + j], qr);
+          const double d = a[i * n + j] - qr;
+          s = std::fma(d, d, s);
+        }
+      ps[static_cast<size_t>(pi)] = s;
+    }
+  });
+  double acc = 0.0;
+  for (const double s : ps) acc += s;
   return std::sqrt(acc) / na;
 }
 

@@ -47,6 +47,9 @@ void orc_stream_indices(uint64_t seed, uint64_t start, int64_t bound, int64_t co
 int64_t orc_resolved_size(const cqr_sketch_cfg* cfg, int64_t m, int64_t n);
 int orc_sample_rows_uniform(const double* a, int64_t m, int64_t n, int64_t lda, int64_t l,
                             uint64_t seed, int without_replacement, double* a1, int64_t* idx);
+/* test-harness knob: split the Gaussian sketch's rows and the diagnostics over w threads
+   (bitwise the same results) */
+void orc_set_test_threads(int w);
 int orc_sketch_gaussian(const double* a, int64_t m, int64_t n, int64_t lda, int64_t l,
                         uint64_t seed, double* a1);
 /* the same for rows [row0, row0+m_local) of an m_global-row matrix (global counters) */

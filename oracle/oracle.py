@@ -42,6 +42,7 @@ def lib():
             "orc_stream_indices": (None, [u64, u64, i64, i64, pi64]),
             "orc_resolved_size": (i64, [P(_abi.SketchCfg), i64, i64]),
             "orc_sample_rows_uniform": (i32, [pd, i64, i64, i64, i64, u64, i32, pd, pi64]),
+            "orc_set_test_threads": (None, [i32]),
             "orc_sketch_gaussian": (i32, [pd, i64, i64, i64, i64, u64, pd]),
             "orc_sketch_gaussian_shard": (i32, [pd, i64, i64, i64, i64, i64, u64, pd]),
             "orc_gram": (i32, [pd, i64, i64, i64, i32, pd]),
@@ -99,6 +100,13 @@ def _f64(a):
 def _check(st, index=-1):
     if st != 0:
         raise OracleError(st, index)
+
+
+def set_test_threads(w):
+    """Test-harness knob: split the Gaussian sketch's rows and the diagnostics over
+    w threads (bitwise the same results; the reference's sketch, and the bench's
+    CPU arm, are serial)."""
+    lib().orc_set_test_threads(int(w))
 
 
 # rng (rng.hpp)

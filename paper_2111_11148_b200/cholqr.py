@@ -161,8 +161,8 @@ class ParallelRun:
 
 # ---- library / context ------------------------------------------------------------------
 _LIB = None
-_CTX = {}
 _LOCK = threading.Lock()
+_TLS = threading.local()  # per-thread default contexts (cqr.h: a context is not shared across threads)
 
 
 def _lib():
@@ -276,15 +276,20 @@ def make_comm_id():
 
 
 def context(device=None):
-    """Per-device default context (the reference is reentrant per thread)."""
+    """Default context of (this thread, device). The reference is pure and
+    reentrant on distinct inputs, while a cqr_ctx owns one stream,
+    status word and workspace and must not be shared across host threads
+    (cqr.h), so every thread gets its own -- as the C++ shim's thread_local
+    Context does."""
     if device is None:
         device = _current_device()
-    with _LOCK:
-        ctx = _CTX.get(device)
-        if ctx is None:
-            ctx = Context(device)
-            _CTX[device] = ctx
-        return ctx
+    cache = getattr(_TLS, "ctx", None)
+    if cache is None:
+        cache = _TLS.ctx = {}
+    ctx = cache.get(device)
+    if ctx is None:
+        ctx = cache[device] = Context(device)
+    return ctx
 
 
 def _current_device():
@@ -339,6 +344,18 @@ def _stages(rep):
     return out
 
 
+def _check_cuda_matrix(a, what="A"):
+    """A CUDA tensor the library may read as a row-major float64 matrix with
+    leading dimension stride(0); waits for the producer's pending work (the
+    library runs on its own non-blocking stream, which is not ordered after
+    torch's streams)."""
+    import torch
+
+    if a.dtype != torch.float64 or a.dim() != 2 or a.stride(1) != 1 or a.stride(0) < a.shape[1]:
+        raise ValueError(f"{what}: expected a CUDA float64 row-major matrix (stride(1) == 1, stride(0) >= cols)")
+    torch.cuda.current_stream(a.device).synchronize()
+
+
 def _factor(method, a, cfg: SketchConfig | None, opts_c, ctx=None, precond=None):
     cfg_c = (cfg or SketchConfig())._c()
     rep = _abi.Report()
@@ -346,15 +363,13 @@ def _factor(method, a, cfg: SketchConfig | None, opts_c, ctx=None, precond=None)
     if _is_torch_cuda(a):
         import torch
 
-        if a.dtype != torch.float64 or a.dim() != 2 or a.stride(1) != 1:
-            raise ValueError("expected a CUDA float64 row-major (stride(1) == 1) matrix")
+        _check_cuda_matrix(a)
         if precond is not None:
             raise ValueError("a custom preconditioner needs host buffers")
         ctx = ctx or context(a.device.index)
         m, n = a.shape
         q = torch.empty((m, n), dtype=torch.float64, device=a.device)
         r = np.zeros((n, n))
-        torch.cuda.current_stream(a.device).synchronize()
         st = _lib().cqr_factor_dev(ctx.h, method, C.c_void_p(a.data_ptr()), m, m, 0, n, a.stride(0),
                                    C.byref(cfg_c), C.byref(opts_c), C.c_void_p(q.data_ptr()), n, _ptr(r), n,
                                    C.byref(rep))
@@ -495,10 +510,10 @@ def gram(x, ctx=None):
     if _is_torch_cuda(x):
         import torch
 
+        _check_cuda_matrix(x, "gram")
         ctx = ctx or context(x.device.index)
         m, n = x.shape
         g = torch.empty((n, n), dtype=torch.float64, device=x.device)
-        torch.cuda.current_stream(x.device).synchronize()
         ctx._check(_lib().cqr_gram_dev(ctx.h, C.c_void_p(x.data_ptr()), m, n, x.stride(0), C.c_void_p(g.data_ptr())))
         return g
     x = _host(x)
@@ -516,10 +531,10 @@ def gram_sharded_sim(x, p, ctx=None):
     compute it (cqr_gram_sharded_sim: the multi-rank protocol on one device)."""
     import torch
 
+    _check_cuda_matrix(x, "gram_sharded_sim")
     ctx = ctx or context(x.device.index)
     m, n = x.shape
     g = torch.empty((n, n), dtype=torch.float64, device=x.device)
-    torch.cuda.current_stream(x.device).synchronize()
     ctx._check(_lib().cqr_gram_sharded_sim(ctx.h, C.c_void_p(x.data_ptr()), m, n, x.stride(0), p,
                                             C.c_void_p(g.data_ptr())))
     return g
@@ -544,10 +559,13 @@ def right_trisolve_in_place(x, r, ctx=None):
     if _is_torch_cuda(x):
         import torch
 
+        _check_cuda_matrix(x, "right_trisolve_in_place")
         ctx = ctx or context(x.device.index)
         m, n = x.shape
         rd = r if _is_torch_cuda(r) else torch.as_tensor(np.ascontiguousarray(r, dtype=np.float64), device=x.device)
-        rd = rd.contiguous()
+        rd = rd.to(torch.float64).contiguous()
+        if tuple(rd.shape) != (n, n):
+            raise ValueError("right_trisolve: dimension mismatch")
         idx = C.c_int64(-1)
         torch.cuda.current_stream(x.device).synchronize()
         st = _lib().cqr_trisolve_inplace_dev(ctx.h, C.c_void_p(x.data_ptr()), m, n, x.stride(0),
@@ -697,10 +715,10 @@ def orthogonality_error_dev(q, ctx=None):
     """diagnostics::orthogonality_error (diagnostics.cpp:10-14) on a CUDA tensor."""
     import torch
 
+    _check_cuda_matrix(q, "Q")
     ctx = ctx or context(q.device.index)
     out = C.c_double()
     m, n = q.shape
-    torch.cuda.current_stream(q.device).synchronize()
     ctx._check(_lib().cqr_orthogonality_error_dev(ctx.h, C.c_void_p(q.data_ptr()), m, n, q.stride(0), C.byref(out)))
     return out.value
 
@@ -709,11 +727,16 @@ def residual_error_dev(a, q, r, ctx=None):
     """diagnostics::residual_error (diagnostics.cpp:16-28) on CUDA tensors (r host)."""
     import torch
 
+    _check_cuda_matrix(a, "A")
+    _check_cuda_matrix(q, "Q")
+    if q.shape != a.shape:
+        raise ValueError("residual_error: A and Q shapes differ")
     ctx = ctx or context(a.device.index)
     out = C.c_double()
     m, n = a.shape
     rh = np.ascontiguousarray(r, dtype=np.float64)
-    torch.cuda.current_stream(a.device).synchronize()
+    if rh.shape != (n, n):
+        raise ValueError("residual_error: R must be n x n")
     ctx._check(_lib().cqr_residual_error_dev(ctx.h, C.c_void_p(a.data_ptr()), a.stride(0), C.c_void_p(q.data_ptr()),
                                              q.stride(0), _ptr(rh), m, n, C.byref(out)))
     return out.value

@@ -113,6 +113,12 @@ void ckn(ncclResult_t r, const char* what) {
     ++(c)->launches;             \
   } while (0)
 
+// Copies that the host waits for, ordered on the library's stream. (A plain cudaMemcpy runs on the
+// legacy stream, which the non-blocking library stream is not ordered against, and a pageable H2D
+// cudaMemcpy may return before its DMA lands -- a kernel queued next on the library stream could
+// read the old bytes.)
+void copy_sync(cqr_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, const char* what);
+
 void require(bool cond, const char* msg) {
   if (!cond) throw Fail{CQR_INVALID_ARGUMENT, -1, msg};
 }
@@ -281,8 +287,10 @@ const int32_t* gram_tiles_dev(cqr_ctx* c, const cqr::GramPlan& p, int slot = 0) 
   if (c->tiles_key[slot] != key) {  // the table depends on (np, parts, maxt) only: upload once
     std::vector<int32_t> ht(p.tiles_bytes / sizeof(int32_t));
     cqr::gram_tiles(p, ht.data());
-    ck(cudaStreamSynchronize(c->stream), "sync");
-    ck(cudaMemcpy(tiles, ht.data(), p.tiles_bytes, cudaMemcpyHostToDevice), "tiles H2D");
+    // ordered on the library's stream (kernels already queued may still read the old table: the
+    // copy waits for them, and the kernels queued after it see the new one)
+    ck(cudaMemcpyAsync(tiles, ht.data(), p.tiles_bytes, cudaMemcpyHostToDevice, c->stream), "tiles H2D");
+    ck(cudaStreamSynchronize(c->stream), "sync");  // ht is a stack buffer
     c->tiles_key[slot] = key;
   }
   return tiles;
@@ -511,6 +519,11 @@ const char* status_msg(int code) {
   }
 }
 
+void copy_sync(cqr_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, const char* what) {
+  ck(cudaMemcpyAsync(dst, src, bytes, kind, c->stream), what);
+  ck(cudaStreamSynchronize(c->stream), what);
+}
+
 void reset_status(cqr_ctx* c) { ck(cudaMemsetAsync(c->status, 0, sizeof(DevStatus), c->stream), "status reset"); }
 
 DevStatus read_status(cqr_ctx* c) {
@@ -630,7 +643,7 @@ Outcome run_cholqr_family(Job& j) {
   DevStatus s = read_status(c);
   if (s.code != 0) throw Fail{s.code, s.index, status_msg(s.code)};
   if (j.method == CQR_SCHOLQR3 && j.opts.shift_kind != CQR_SHIFT_FIXED) {
-    ck(cudaMemcpy(c->scal_h, dbuf<double>(c, B_SCAL, 4), sizeof(double), cudaMemcpyDeviceToHost), "shift D2H");
+    copy_sync(c, c->scal_h, dbuf<double>(c, B_SCAL, 4), sizeof(double), cudaMemcpyDeviceToHost, "shift D2H");
     for (auto& st : o.rep.stages)
       if (st.has_shift) {
         st.shift = c->scal_h[0];
@@ -754,7 +767,7 @@ Outcome run_precond(Job& j) {
       DevStatus s = read_status(c);
       if (s.code == 0) {
         std::vector<double> hr((size_t)n * n), w((size_t)n * n);
-        ck(cudaMemcpy(hr.data(), rh, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "rh D2H");
+        copy_sync(c, hr.data(), rh, sizeof(double) * n * n, cudaMemcpyDeviceToHost, "rh D2H");
         for (int i = 0; i < n; ++i)
           for (int k = 0; k < n; ++k) w[(size_t)k * n + i] = hr[(size_t)i * n + k];
         std::vector<double> sv;
@@ -796,7 +809,7 @@ Outcome run_precond(Job& j) {
 }
 
 void fill_report(cqr_ctx* c, cqr_report* rep, const Outcome* o, int status, long long index, bool r_less,
-                 int method, long long n, long long l) {
+                 int method, long long n, long long l, int workers) {
   // stage times from the recorded events (accumulated across attempts)
   double ms[CQR_STAGE_COUNT] = {0};
   for (auto& e : c->stage_evs) {
@@ -825,7 +838,10 @@ void fill_report(cqr_ctx* c, cqr_report* rep, const Outcome* o, int status, long
   }
   int rmin, rmax;
   double vmin, vmax;
-  cqr_comm_model(method, c->world, n, l, &rmin, &rmax, &vmin, &vmax);
+  // parexec.cpp:64-75: the model of the p that ran -- the ranks of an attached communicator, else
+  // the simulated worker count of the options (run_parallel on one process)
+  const int p = c->comm ? c->world : std::max(1, workers);
+  cqr_comm_model(method, p, n, l, &rmin, &rmax, &vmin, &vmax);
   rep->comm_rounds = rmax;
   rep->comm_volume = vmax;
 }
@@ -885,6 +901,8 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     require(j.lda >= j.n && j.ldq >= j.n, "leading dimension must be >= n");
     require(j.m_local >= 0 && j.row0 >= 0 && j.row0 + j.m_local <= j.m_global, "bad shard");
     require(j.n <= 512, "n > 512 is not supported by the device kernels");
+    // engine.cpp:224: p in [1, m] (0 = a zero-initialised options struct: one worker)
+    require(j.opts.workers >= 0 && j.opts.workers <= j.m_global, "worker count must be in [1, m]");
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     // non-finite input is rejected up front (engine.cpp:222). One process: the
     // check only sets the status word (read with the attempt's single sync);
@@ -945,7 +963,7 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     cudaStreamSynchronize(c->stream);
     cudaGetLastError();
   }
-  fill_report(c, report, st == CQR_OK ? &o : nullptr, st, index, r_less, j.method, j.n, l);
+  fill_report(c, report, st == CQR_OK ? &o : nullptr, st, index, r_less, j.method, j.n, l, j.opts.workers);
   return st;
 }
 
@@ -1213,7 +1231,7 @@ int cqr_cholesky_upper(cqr_ctx* c, const double* g, int64_t n, double* r, int64_
       idx = s.index;
       throw Fail{s.code, s.index, "cholesky breakdown"};
     }
-    ck(cudaMemcpy(r, dr, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "R D2H");
+    copy_sync(c, r, dr, sizeof(double) * n * n, cudaMemcpyDeviceToHost, "R D2H");
   });
   if (pivot) *pivot = idx;
   return st;
@@ -1293,7 +1311,7 @@ static int small_factor(cqr_ctx* c, const double* a1, int64_t l, int64_t n, doub
       idx = s.index;
       throw Fail{s.code, s.index, "singular triangular factor"};
     }
-    ck(cudaMemcpy(out, dr, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "R D2H");
+    copy_sync(c, out, dr, sizeof(double) * n * n, cudaMemcpyDeviceToHost, "R D2H");
   });
   if (index) *index = idx;
   return st;
@@ -1506,11 +1524,11 @@ int cqr_synthesize_dev(cqr_ctx* c, int64_t m_local, int64_t m_global, int64_t ro
     }
     c->local_only = 0;
     std::vector<double> hv((size_t)n * n), svt((size_t)n * n);
-    ck(cudaMemcpy(hv.data(), v, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "V D2H");
+    copy_sync(c, hv.data(), v, sizeof(double) * n * n, cudaMemcpyDeviceToHost, "V D2H");
     for (int64_t i = 0; i < n; ++i)
       for (int64_t jj = 0; jj < n; ++jj) svt[(size_t)(i * n + jj)] = sigma[i] * hv[(size_t)(jj * n + i)];
     double* b = v + (size_t)n * n;
-    ck(cudaMemcpy(b, svt.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice), "SVt H2D");
+    copy_sync(c, b, svt.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, "SVt H2D");
     if (m_local > 0) LAUNCH(c, cqr::launch_gemm_tall(u, n, b, a, lda, m_local, (int)n, c->num_sms, c->stream));
     ck(cudaStreamSynchronize(c->stream), "sync");
     c->stage_evs.clear();

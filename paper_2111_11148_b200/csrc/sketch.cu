@@ -506,7 +506,10 @@ __global__ void rng_gauss_kernel(uint64_t seed, uint64_t k0, long long count, do
   }
 }
 
-cudaError_t ensure_tables() {
+// The Box-Muller tables are uploaded once per device, ordered on the launching
+// stream (a non-blocking stream is not ordered after the legacy stream) and
+// completed before any kernel is allowed to read them.
+cudaError_t ensure_tables(cudaStream_t s) {
   static std::mutex mu;
   static unsigned long long done = 0;  // bit per device
   int dev = 0;
@@ -516,7 +519,8 @@ cudaError_t ensure_tables() {
   if (dev < 64 && (done >> dev) & 1ull) return cudaSuccess;
   BmTables t;
   bm_tables_host(&t);
-  e = cudaMemcpyToSymbol(c_bm, &t, sizeof(t));
+  e = cudaMemcpyToSymbolAsync(c_bm, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && dev < 64) done |= 1ull << dev;
   return e;
 }
@@ -527,7 +531,7 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
                             cudaStream_t s, int y0, int y1) {
   if (y1 < 0) y1 = p.kchunks;
   if (y1 <= y0) return cudaSuccess;
-  cudaError_t e0 = ensure_tables();
+  cudaError_t e0 = ensure_tables(s);
   if (e0 != cudaSuccess) return e0;
   const size_t smem = (size_t)(2 * kST * (kKS + 4) + 2 * kKS * (NP + 4)) * sizeof(double);
   const bool aligned = (m_global % 2 == 0) && (row0 % 2 == 0) && (p.rows_per_chunk % 2 == 0);
@@ -615,7 +619,7 @@ cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long lo
   if (p.ws) {
     if (y1 < 0) y1 = p.kchunks;
     if (y1 <= y0) return cudaSuccess;
-    cudaError_t e0 = ensure_tables();
+    cudaError_t e0 = ensure_tables(s);
     if (e0 != cudaSuccess) return e0;
     if (p.npc == 64) return launch_ws<64, 128>(p, a, lda, m_global, row0, seed, partial, check, st, s, y0, y1);
     if (p.npc == 128) return launch_ws<128, kST>(p, a, lda, m_global, row0, seed, partial, check, st, s, y0, y1);
@@ -675,14 +679,14 @@ __global__ void box_muller_bits_kernel(const uint64_t* __restrict__ bits, long l
 }
 
 cudaError_t launch_box_muller_bits(const uint64_t* bits, long long pairs, double* out, cudaStream_t s) {
-  cudaError_t e = ensure_tables();
+  cudaError_t e = ensure_tables(s);
   if (e != cudaSuccess) return e;
   box_muller_bits_kernel<<<148, 256, 0, s>>>(bits, pairs, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rng_gaussian(uint64_t seed, uint64_t k0, long long count, double* out, cudaStream_t s) {
-  cudaError_t e = ensure_tables();
+  cudaError_t e = ensure_tables(s);
   if (e != cudaSuccess) return e;
   rng_gauss_kernel<<<256, 256, 0, s>>>(seed, k0, count, out);
   return cudaGetLastError();

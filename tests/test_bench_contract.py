@@ -45,3 +45,34 @@ def test_our_arm_line():
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
     assert set(d["stage_roofline"]) >= {"sketch", "gram", "trisolve"}
     assert d["check"]["orth"] < 1e-10
+
+
+def test_multi_gpu_launcher_dry_run():
+    """--gpus N without WORLD_SIZE re-launches under torch.distributed.run, one rank per GPU."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "8", "--workload", "c2",
+                          "--dry-run"], cwd=ROOT, capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode == 0, out.stderr
+    cmd = json.loads(out.stdout.strip().splitlines()[-1])["launch"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=8" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    i = cmd.index(os.path.join(ROOT, "bench.py"))
+    assert cmd[i + 1:i + 5] == ["--gpus", "8", "--workload", "c2"]
+    # under the launcher WORLD_SIZE must agree with --gpus
+    bad = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "8"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=120, env=dict(env, WORLD_SIZE="2"))
+    assert bad.returncode == 2
+
+
+def test_strong_and_weak_shards():
+    """c2 is strong-scaled (fixed m = 4e6, ceil(b*m/p) blocks, parexec.cpp:13-15); c1/c3 weak."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    for p in (1, 2, 4, 8):
+        rows = [bench.workload_shape("c2", p, b) for b in range(p)]
+        assert sum(r[3] for r in rows) == 4_000_000 and all(r[1] == 4_000_000 for r in rows)
+        assert [r[2] for r in rows] == [-(-b * 4_000_000 // p) for b in range(p)]
+        w = [bench.workload_shape("c3", p, b) for b in range(p)]
+        assert all(r[3] == 4_194_304 for r in w) and w[0][1] == 4_194_304 * p
+    assert bench.shard(10, 3, 0) == (0, 4) and bench.shard(10, 3, 1) == (4, 3) and bench.shard(10, 3, 2) == (7, 3)

@@ -308,14 +308,22 @@ def test_cholqr_family_bitwise(method, m, n, kappa, seed):
     assert [s.stage for s in f.report.stages] == [_abi.STAGE_NAMES[s.stage] for s in ref.stages]
 
 
-def test_scholqr3_theory_shift_bitwise():
-    a = o.synthesize(10000, 50, 1e5, 9)
+@pytest.mark.parametrize("m,n,kappa,seed", [(10000, 50, 1e5, 9), (100_000, 100, 1e12, 4)])
+def test_scholqr3_theory_shift_tolerance(m, n, kappa, seed):
+    # The oracle resolves the theory shift from a.squaredNorm() (engine.cpp:270, cholqr.cpp:21-26);
+    # the device from trace(G1) of its first Gram -- equal in exact arithmetic, so the shift agrees
+    # to a few ulp and (Q, R) to rounding: a tolerance test.
+    a = o.synthesize(m, n, kappa, seed)
     th = _abi.options()
     ref = o.factor(_abi.SCHOLQR3, a, opts=th)
     f, _, _ = G._factor(_abi.SCHOLQR3, a, None, th)
-    assert np.array_equal(f.q, ref.q) and np.array_equal(f.r, ref.r)
-    sh = [s.shift for s in f.report.stages if s.shift is not None]
-    assert sh and sh[0] == [s.shift for s in ref.stages if s.has_shift][0]
+    sh_g = [s.shift for s in f.report.stages if s.shift is not None][0]
+    sh_o = [s.shift for s in ref.stages if s.has_shift][0]
+    assert abs(sh_g - sh_o) <= 1e-13 * sh_o
+    assert relf(f.r, ref.r) <= 1e-12
+    assert np.linalg.norm(f.q - ref.q) / math.sqrt(n) <= q_tol(kappa)
+    assert o.orthogonality_error(f.q) <= max(2 * o.orthogonality_error(ref.q), 1e-11)
+    assert o.residual_error(a, f.q, f.r) <= max(2 * o.residual_error(a, ref.q, ref.r), 1e-12)
 
 
 def test_breakdowns_match():
