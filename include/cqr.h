@@ -151,6 +151,26 @@ int cqr_comm_make_id(void* id);
  * all-reduce, agreement on non-finite input), also for world == 1 (a one-rank
  * NCCL communicator). */
 int cqr_attach_comm(cqr_ctx* ctx, int rank, int world, const void* id);
+
+/* A caller-owned transport for the same exchange steps, on HOST buffers (the
+ * library stages device data through pinned memory around each call; every call
+ * blocks until the exchange is complete). This is how the multi-rank path runs
+ * with fewer GPUs than ranks -- several processes on one GPU whose kernels never
+ * wait on one another, the exchanges going through e.g. torch.distributed/gloo --
+ * and how a host that already owns an MPI communicator plugs it in. Callbacks
+ * return 0 on success. dtype: CQR_COMM_F64_SUM (double, sum) or CQR_COMM_I32_MAX
+ * (int32, max). sendrecv: send `count` doubles to rank dst (dst < 0: none) and
+ * receive `count` doubles from rank src (src < 0: none), concurrently. allgather:
+ * every rank contributes `count` doubles; recv holds world * count in rank order.
+ * world == 1 with a NULL table detaches. */
+enum { CQR_COMM_F64_SUM = 0, CQR_COMM_I32_MAX = 1 };
+typedef struct {
+  void* user;
+  int (*allreduce)(void* user, void* buf, int64_t count, int dtype);
+  int (*sendrecv)(void* user, const double* send, int dst, double* recv, int src, int64_t count);
+  int (*allgather)(void* user, const double* send, double* recv, int64_t count);
+} cqr_host_comm;
+int cqr_attach_host_comm(cqr_ctx* ctx, int rank, int world, const cqr_host_comm* comm);
 int cqr_stream_handle(cqr_ctx* ctx, void** stream); /* cudaStream_t the context launches on */
 
 /* ---- whole factorizations (cholqr.hpp:82-109, parexec.hpp:89-90) ----------- */

@@ -88,6 +88,19 @@ class GramShard(C.Structure):
     ]
 
 
+# cqr_host_comm (cqr.h): a caller-owned transport for the rank exchanges, on host buffers
+COMM_F64_SUM, COMM_I32_MAX = 0, 1
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int)
+SENDRECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double), C.c_int,
+                          C.c_int64)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+
+
+class HostComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce", ALLREDUCE_FN), ("sendrecv", SENDRECV_FN),
+                ("allgather", ALLGATHER_FN)]
+
+
 PRECOND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_int64,
                          C.POINTER(C.c_double), C.POINTER(C.c_int64))
 

@@ -183,6 +183,7 @@ def _lib():
             "cqr_comm_id_size": (i32, []),
             "cqr_comm_make_id": (i32, [vp]),
             "cqr_attach_comm": (i32, [vp, i32, i32, vp]),
+            "cqr_attach_host_comm": (i32, [vp, i32, i32, P(_abi.HostComm)]),
             "cqr_stream_handle": (i32, [vp, P(vp)]),
             "cqr_launch_count": (i64, [vp]),
             "cqr_factor": (i32, [vp, i32, vp, i64, i64, i64, P(_abi.SketchCfg), P(_abi.Options), vp, i64, vp,

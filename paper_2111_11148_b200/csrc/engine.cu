@@ -54,6 +54,10 @@ struct cqr_ctx {
   DevStatus* status_h = nullptr;  // pinned host
   double* scal_h = nullptr;       // pinned host scalars
   ncclComm_t comm = nullptr;
+  cqr_host_comm hcomm{};     // caller-owned host transport (cqr_attach_host_comm)
+  bool has_hcomm = false;
+  void* stage_h = nullptr;   // pinned staging for the host transport
+  size_t stage_bytes = 0;
   int rank = 0, world = 1;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -105,6 +109,82 @@ void ck(cudaError_t e, const char* what) {
 
 void ckn(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw Fail{CQR_NCCL_ERROR, -1, std::string(what) + ": " + ncclGetErrorString(r)};
+}
+
+// ---- the rank exchanges: NCCL on the library's stream, or the caller's host transport ----
+bool attached(const cqr_ctx* c) { return c->comm != nullptr || c->has_hcomm; }
+bool multi(const cqr_ctx* c) { return attached(c) && !c->local_only; }
+
+void* host_stage(cqr_ctx* c, size_t bytes) {
+  if (c->stage_bytes < bytes) {
+    if (c->stage_h) cudaFreeHost(c->stage_h);
+    c->stage_h = nullptr;
+    c->stage_bytes = 0;
+    ck(cudaMallocHost(&c->stage_h, bytes), "cudaMallocHost (comm staging)");
+    c->stage_bytes = bytes;
+  }
+  return c->stage_h;
+}
+
+void hcheck(int rc, const char* what) {
+  if (rc != 0) throw Fail{CQR_NCCL_ERROR, -1, std::string("host transport: ") + what + " failed"};
+}
+
+// in-place all-reduce of a device buffer: doubles summed, or int32 max
+void coll_allreduce(cqr_ctx* c, void* p, size_t count, int dtype) {
+  if (!multi(c)) return;
+  const size_t esz = dtype == CQR_COMM_F64_SUM ? sizeof(double) : sizeof(int32_t);
+  if (c->comm) {
+    ckn(ncclAllReduce(p, p, count, dtype == CQR_COMM_F64_SUM ? ncclDouble : ncclInt32,
+                      dtype == CQR_COMM_F64_SUM ? ncclSum : ncclMax, c->comm, c->stream),
+        "ncclAllReduce");
+    return;
+  }
+  void* h = host_stage(c, count * esz);
+  ck(cudaMemcpyAsync(h, p, count * esz, cudaMemcpyDeviceToHost, c->stream), "comm D2H");
+  ck(cudaStreamSynchronize(c->stream), "comm sync");
+  hcheck(c->hcomm.allreduce(c->hcomm.user, h, (int64_t)count, dtype), "allreduce");
+  ck(cudaMemcpyAsync(p, h, count * esz, cudaMemcpyHostToDevice, c->stream), "comm H2D");
+  ck(cudaStreamSynchronize(c->stream), "comm sync");
+}
+
+// send `count` doubles to dst and receive `count` from src, concurrently (either side may be absent: -1)
+void coll_sendrecv(cqr_ctx* c, const double* send, int dst, double* recv, int src, size_t count) {
+  if (dst < 0 && src < 0) return;
+  if (c->comm) {
+    ckn(ncclGroupStart(), "group");
+    if (dst >= 0) ckn(ncclSend(send, count, ncclDouble, dst, c->comm, c->stream), "ncclSend");
+    if (src >= 0) ckn(ncclRecv(recv, count, ncclDouble, src, c->comm, c->stream), "ncclRecv");
+    ckn(ncclGroupEnd(), "group");
+    return;
+  }
+  double* h = static_cast<double*>(host_stage(c, 2 * count * sizeof(double)));
+  if (dst >= 0) {
+    ck(cudaMemcpyAsync(h, send, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "comm D2H");
+    ck(cudaStreamSynchronize(c->stream), "comm sync");
+  }
+  hcheck(c->hcomm.sendrecv(c->hcomm.user, dst >= 0 ? h : nullptr, dst, src >= 0 ? h + count : nullptr, src,
+                           (int64_t)count),
+         "sendrecv");
+  if (src >= 0) {
+    ck(cudaMemcpyAsync(recv, h + count, count * sizeof(double), cudaMemcpyHostToDevice, c->stream), "comm H2D");
+    ck(cudaStreamSynchronize(c->stream), "comm sync");
+  }
+}
+
+// every rank's `count` doubles, in rank order
+void coll_allgather(cqr_ctx* c, const double* send, double* recv, size_t count) {
+  if (c->comm) {
+    ckn(ncclAllGather(send, recv, count, ncclDouble, c->comm, c->stream), "ncclAllGather");
+    return;
+  }
+  double* h = static_cast<double*>(host_stage(c, (size_t)(c->world + 1) * count * sizeof(double)));
+  ck(cudaMemcpyAsync(h, send, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "comm D2H");
+  ck(cudaStreamSynchronize(c->stream), "comm sync");
+  hcheck(c->hcomm.allgather(c->hcomm.user, h, h + count, (int64_t)count), "allgather");
+  ck(cudaMemcpyAsync(recv, h + count, (size_t)c->world * count * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+     "comm H2D");
+  ck(cudaStreamSynchronize(c->stream), "comm sync");
 }
 
 #define LAUNCH(c, expr)          \
@@ -275,10 +355,7 @@ void wait_rows(Job& j, long long rows_end) {
 }
 void wait_all(Job& j) { wait_rows(j, std::numeric_limits<long long>::max()); }
 
-void allreduce(cqr_ctx* c, double* p, size_t count) {
-  if (!c->comm || c->local_only) return;
-  ckn(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->comm, c->stream), "ncclAllReduce");
-}
+void allreduce(cqr_ctx* c, double* p, size_t count) { coll_allreduce(c, p, count, CQR_COMM_F64_SUM); }
 
 // slot 0: the main plan's table; slot 1: the last-wave table of the split launch (gram_dev)
 const int32_t* gram_tiles_dev(cqr_ctx* c, const cqr::GramPlan& p, int slot = 0) {
@@ -386,14 +463,12 @@ void gram_det(cqr_ctx* c, const double* x, long long ldx, int n, long long m, do
   double* head_in = w.ht;
   double* tail_out = w.ht + np2;
   shard_tail(c, sg, x, ldx, n, w.np, tail_out, check);
-  ckn(ncclGroupStart(), "group");
-  if (sg.tail && !sg.span) ckn(ncclSend(tail_out, np2, ncclDouble, b + 1, c->comm, c->stream), "send tail");
-  if (sg.head) ckn(ncclRecv(head_in, np2, ncclDouble, b - 1, c->comm, c->stream), "recv head");
-  ckn(ncclGroupEnd(), "group");
+  // tails to the next rank, heads from the previous (one group)
+  coll_sendrecv(c, tail_out, (sg.tail && !sg.span) ? b + 1 : -1, head_in, sg.head ? b - 1 : -1, np2);
   ck(cudaMemsetAsync(w.slots, 0, sizeof(double) * K * n * n, c->stream), "slots");
   shard_body(c, sg, x, ldx, n, w, head_in, tail_out, w.slots, check);
-  if (sg.span) ckn(ncclSend(tail_out, np2, ncclDouble, b + 1, c->comm, c->stream), "forward span");
-  ckn(ncclAllGather(w.slots, w.all, (size_t)K * n * n, ncclDouble, c->comm, c->stream), "allgather nodes");
+  if (sg.span) coll_sendrecv(c, tail_out, b + 1, nullptr, -1, np2);  // forward the continued chain
+  coll_allgather(c, w.slots, w.all, (size_t)K * n * n);
   shard_top(c, m, p, n, w, g);
 }
 
@@ -435,7 +510,7 @@ void gram_det_sim(cqr_ctx* c, const double* x, long long ldx, int n, long long m
 // Gram of a device tall matrix (this rank's rows) -> g (n x n, mirrored), summed over ranks.
 void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, double* g, int check = 0,
               Job* pj = nullptr) {
-  if (pj && pj->det && c->comm && !c->local_only) {
+  if (pj && pj->det && multi(c)) {
     wait_all(*pj);
     gram_det(c, x, ldx, n, pj->m_global, g, check);
     return;
@@ -476,12 +551,12 @@ void gram_dev(cqr_ctx* c, const double* x, long long m, int n, long long ldx, do
                                           c->stream, 0, -1, c->num_sms));
       }
     }
-    LAUNCH(c, cqr::launch_gram_combine(p, part, g, (!c->comm || c->local_only) ? 1 : 0, c->status, c->stream));
+    LAUNCH(c, cqr::launch_gram_combine(p, part, g, multi(c) ? 0 : 1, c->status, c->stream));
     ++c->launches;
   } else {
     ck(cudaMemsetAsync(g, 0, sizeof(double) * n * n, c->stream), "memset");
   }
-  if (c->comm && !c->local_only) {
+  if (multi(c)) {
     allreduce(c, g, (size_t)n * n);
     LAUNCH(c, cqr::launch_mirror_upper(g, n, c->status, c->stream));
   }
@@ -840,7 +915,7 @@ void fill_report(cqr_ctx* c, cqr_report* rep, const Outcome* o, int status, long
   double vmin, vmax;
   // parexec.cpp:64-75: the model of the p that ran -- the ranks of an attached communicator, else
   // the simulated worker count of the options (run_parallel on one process)
-  const int p = c->comm ? c->world : std::max(1, workers);
+  const int p = attached(c) ? c->world : std::max(1, workers);
   cqr_comm_model(method, p, n, l, &rmin, &rmax, &vmin, &vmax);
   rep->comm_rounds = rmax;
   rep->comm_volume = vmax;
@@ -910,12 +985,12 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     reset_status(c);
     const bool gaussian = j.method == CQR_RQR_GAUSSIAN || j.cfg.strategy == CQR_GAUSSIAN;
     const bool family = j.method == CQR_CHOLQR || j.method == CQR_CHOLQR2 || j.method == CQR_SCHOLQR3;
-    j.check_first = (!c->comm && !j.precond && (family || gaussian)) ? 1 : 0;
+    j.check_first = (!attached(c) && !j.precond && (family || gaussian)) ? 1 : 0;
     if (!j.check_first) {
       wait_all(j);
       check_finite(c, j.a, j.m_local, j.n, j.lda);
     }
-    if (c->comm) {  // every rank takes the same path
+    if (attached(c)) {  // every rank takes the same path
       DevStatus s0 = read_status(c);
       // flags[1]: this rank's rows are not its standard block (parexec.cpp:13-15); then
       // every rank sums plain Gram partials instead of the rank-count-independent tree
@@ -924,7 +999,7 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
       {
         int* flag = dbuf<int>(c, B_DIAG, 2);
         ck(cudaMemcpyAsync(flag, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream), "flag");
-        ckn(ncclAllReduce(flag, flag, 2, ncclInt, ncclMax, c->comm, c->stream), "allreduce flag");
+        coll_allreduce(c, flag, 2, CQR_COMM_I32_MAX);
         ck(cudaMemcpyAsync(flags, flag, sizeof(flags), cudaMemcpyDeviceToHost, c->stream), "flag");
         ck(cudaStreamSynchronize(c->stream), "sync");
       }
@@ -1019,6 +1094,7 @@ int cqr_destroy(cqr_ctx* c) {
   if (c->status) cudaFree(c->status);
   if (c->status_h) cudaFreeHost(c->status_h);
   if (c->scal_h) cudaFreeHost(c->scal_h);
+  if (c->stage_h) cudaFreeHost(c->stage_h);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->cstream) cudaStreamDestroy(c->cstream);
   for (auto e : c->pipe_ev) cudaEventDestroy(e);
@@ -1045,6 +1121,7 @@ int cqr_attach_comm(cqr_ctx* c, int rank, int world, const void* id) {
       ncclCommDestroy(c->comm);
       c->comm = nullptr;
     }
+    c->has_hcomm = false;
     c->rank = rank;
     c->world = world;
     // an attached communicator switches the collective paths on, also for world == 1
@@ -1052,6 +1129,23 @@ int cqr_attach_comm(cqr_ctx* c, int rank, int world, const void* id) {
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof(u));
     ckn(ncclCommInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
+  });
+}
+
+int cqr_attach_host_comm(cqr_ctx* c, int rank, int world, const cqr_host_comm* hc) {
+  if (!c || world < 1 || rank < 0 || rank >= world) return CQR_INVALID_ARGUMENT;
+  if (hc && (!hc->allreduce || !hc->sendrecv || !hc->allgather)) return CQR_INVALID_ARGUMENT;
+  if (!hc && world != 1) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (c->comm) {
+      ncclCommDestroy(c->comm);
+      c->comm = nullptr;
+    }
+    c->has_hcomm = hc != nullptr;
+    c->hcomm = hc ? *hc : cqr_host_comm{};
+    c->rank = hc ? rank : 0;
+    c->world = hc ? world : 1;
   });
 }
 
@@ -1095,8 +1189,8 @@ static int factor_host(cqr_ctx* c, int method, const double* a, int64_t m, int64
   if (!c) return CQR_INVALID_ARGUMENT;
   const bool sharded = m != m_global || row0 != 0;
   if (m < 1 || n < 1 || lda < n || ldq < n || (r && ldr < n) || row0 < 0 || row0 + m > m_global ||
-      (sharded && !c->comm) || (!sharded && c->world > 1)) {
-    c->err = sharded && !c->comm     ? "sharded call without an attached communicator"
+      (sharded && !attached(c)) || (!sharded && c->world > 1)) {
+    c->err = sharded && !attached(c) ? "sharded call without an attached communicator"
              : !sharded && c->world > 1 ? "a multi-rank context takes its shard through cqr_factor_sharded"
                                         : "bad shape";
     if (report) {

@@ -66,6 +66,93 @@ def make_context(device: int, rank: int | None = None, world: int | None = None)
     return ctx
 
 
+class HostTransport:
+    """cqr_host_comm over torch.distributed (any backend that takes CPU tensors: gloo).
+
+    The library stages each exchange through pinned host memory and calls back;
+    every callback blocks until its exchange is complete, so no GPU kernel ever
+    waits on another rank. This runs the multi-rank path of the engine with
+    several processes on one GPU (tests/test_gpu_multirank.py) -- the exchange
+    steps, their order and the data they move are the NCCL path's."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.errors = []
+        self.table = _abi.HostComm(None, _abi.ALLREDUCE_FN(self._allreduce), _abi.SENDRECV_FN(self._sendrecv),
+                                   _abi.ALLGATHER_FN(self._allgather))
+
+    @staticmethod
+    def _view(ptr, count, ctype):
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(int(count),))
+
+    def allreduce(self, arr, dtype):
+        import torch
+        import torch.distributed as td
+
+        t = torch.from_numpy(arr)
+        td.all_reduce(t, op=td.ReduceOp.SUM if dtype == _abi.COMM_F64_SUM else td.ReduceOp.MAX, group=self.group)
+
+    def sendrecv(self, send, dst, recv, src):
+        import torch
+        import torch.distributed as td
+
+        reqs = []
+        if dst >= 0:
+            reqs.append(td.isend(torch.from_numpy(send), dst, group=self.group))
+        if src >= 0:
+            reqs.append(td.irecv(torch.from_numpy(recv), src, group=self.group))
+        for r in reqs:
+            r.wait()
+
+    def allgather(self, send, recv):
+        import torch
+        import torch.distributed as td
+
+        world = td.get_world_size(self.group)
+        parts = [torch.from_numpy(recv[k * send.size:(k + 1) * send.size]) for k in range(world)]
+        td.all_gather(parts, torch.from_numpy(send), group=self.group)
+
+    # ctypes entry points (exceptions must not cross into C)
+    def _allreduce(self, user, buf, count, dtype):
+        try:
+            self.allreduce(self._view(buf, count, C.c_double if dtype == _abi.COMM_F64_SUM else C.c_int32), dtype)
+            return 0
+        except Exception as e:  # pragma: no cover - surfaced through the status code
+            self.errors.append(e)
+            return 1
+
+    def _sendrecv(self, user, send, dst, recv, src, count):
+        try:
+            self.sendrecv(self._view(send, count, C.c_double) if dst >= 0 else None, dst,
+                          self._view(recv, count, C.c_double) if src >= 0 else None, src)
+            return 0
+        except Exception as e:  # pragma: no cover
+            self.errors.append(e)
+            return 1
+
+    def _allgather(self, user, send, recv, count):
+        try:
+            import torch.distributed as td
+
+            world = td.get_world_size(self.group)
+            self.allgather(self._view(send, count, C.c_double), self._view(recv, count * world, C.c_double))
+            return 0
+        except Exception as e:  # pragma: no cover
+            self.errors.append(e)
+            return 1
+
+
+def attach_host_transport(ctx, group=None):
+    """Attach a HostTransport over the torch.distributed group to ctx (kept alive on ctx)."""
+    import torch.distributed as td
+
+    tr = HostTransport(group)
+    ctx._check(cq._lib().cqr_attach_host_comm(ctx.h, td.get_rank(group), td.get_world_size(group),
+                                               C.byref(tr.table)))
+    ctx.transport = tr
+    return tr
+
+
 def factor_sharded(ctx, method, a_local, m_global: int, row0: int, cfg: cq.SketchConfig | None = None,
                    opts=None, q_out=None):
     """cqr_factor_dev on this rank's CUDA shard; returns (Q_local, R, report)."""

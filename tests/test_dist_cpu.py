@@ -72,3 +72,53 @@ def test_shard_rows_matches_reference_partition():
         assert spans[0][0] == 0 and sum(r for _, r in spans) == m
         assert all(spans[b][0] + spans[b][1] == spans[b + 1][0] for b in range(p - 1))
         assert [o.block_offset(m, p, b) for b in range(p)] == [s for s, _ in spans]
+
+
+def _transport_worker(rank, world, port, out):
+    """The host transport's C entry points (the function pointers cqr_attach_host_comm
+    stores), called as the engine calls them: pinned-like host buffers, blocking."""
+    import ctypes as C
+
+    from paper_2111_11148_b200 import _abi
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = dist.HostTransport()
+        t = tr.table
+        pd = C.POINTER(C.c_double)
+        ok = 0
+        # all-reduce sum of doubles, in place
+        x = np.arange(5, dtype=np.float64) + 10 * rank
+        assert t.allreduce(None, x.ctypes.data, 5, _abi.COMM_F64_SUM) == 0
+        ok += int(np.array_equal(x, sum(np.arange(5.0) + 10 * b for b in range(world))))
+        # all-reduce max of int32 (the non-finite / shard flags)
+        f = np.array([rank == 1, rank], dtype=np.int32)
+        assert t.allreduce(None, f.ctypes.data, 2, _abi.COMM_I32_MAX) == 0
+        ok += 2 * int(list(f) == [1, world - 1])
+        # send to the next rank, receive from the previous (the Gram chain tail/head), ends have one side
+        s = np.full(7, float(rank + 1))
+        r = np.zeros(7)
+        dst = rank + 1 if rank + 1 < world else -1
+        src = rank - 1 if rank > 0 else -1
+        assert t.sendrecv(None, s.ctypes.data_as(pd) if dst >= 0 else None, dst,
+                          r.ctypes.data_as(pd) if src >= 0 else None, src, 7) == 0
+        ok += 4 * int(src < 0 or np.array_equal(r, np.full(7, float(rank))))
+        # all-gather in rank order
+        g = np.full(3, float(rank))
+        allg = np.empty(3 * world)
+        assert t.allgather(None, g.ctypes.data_as(pd), allg.ctypes.data_as(pd), 3) == 0
+        ok += 8 * int(np.array_equal(allg, np.repeat(np.arange(world, dtype=float), 3)))
+        out[rank] = ok if not tr.errors else -1
+    finally:
+        td.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_transport_callbacks_gloo(world):
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = 30500 + (os.getpid() % 1000) + world
+    mp.start_processes(_transport_worker, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
+    assert dict(out) == {b: 15 for b in range(world)}, dict(out)

@@ -674,3 +674,31 @@ def test_randomized_kernel_sweep():
         a1 = o.gaussian_matrix(l, n, seed + 1)
         assert np.array_equal(G.lu_u_factor(a1), o.lu_u_factor(a1)), (case, l, n)
         assert relf(G.qr_r_factor(a1), o.qr_r_factor(a1)) <= 1e-12, (case, l, n)
+
+
+def test_concurrent_threads_get_their_own_contexts():
+    """concurrent calls on distinct inputs are safe. Each host thread gets its own
+    default context (stream, status word, workspace); results equal the sequential ones bitwise."""
+    import threading
+
+    mats = [o.synthesize(20000 + 1000 * i, 24 + 8 * i, 1e8, 40 + i) for i in range(4)]
+    cfgs = [G.SketchConfig(strategy=G.Strategy.Gaussian, seed=70 + i) for i in range(4)]
+    seq = [G.rlu_cholesky_qr(a, c) for a, c in zip(mats, cfgs)]
+    out = [None] * 4
+    errs = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                out[i] = G.rlu_cholesky_qr(mats[i], cfgs[i])
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    for s, f in zip(seq, out):
+        assert np.array_equal(s.q, f.q) and np.array_equal(s.r, f.r)
