@@ -34,6 +34,8 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s);
 // trisolve_tma.cu: the TMA-staged kernel (16-byte aligned bases, even leading dimensions, np >= 32)
 bool trisolve_tma_eligible(const TrisolveArgs& a, int np);
 cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s);
+// trisolve_rr.cu: register-resident right-looking kernel (np <= 128; same eligibility as the TMA kernel)
+cudaError_t launch_trisolve_rr(const TrisolveArgs& a, int np, cudaStream_t s);
 
 // ---- gram.cu ---------------------------------------------------------------------
 struct GramPlan {

@@ -381,7 +381,15 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   const int nt = np / 8;
   a.bpack = a.pack;
   a.dpack = a.pack + (size_t)nt * (nt - 1) * 32;
-  if (a.variant == 0 && trisolve_tma_eligible(a, np)) {
+  // variant 0: the register-resident right-looking kernel (np <= 128) or the left-looking TMA kernel
+  // (wider); 2: the left-looking TMA kernel at every width; 1: the register kernel (A/B runs)
+  if ((a.variant == 0 || a.variant == 2) && trisolve_tma_eligible(a, np)) {
+    // the right-looking kernel at np <= 64 (c3: 1.032 vs 1.058 ms per call; at np = 128 its 16-row
+    // warps leave the diagonal recurrence on half the lanes: 0.97 vs 0.77 ms, so the left-looking kernel)
+    if (a.variant == 0 && np <= 64) {
+      const cudaError_t e = launch_trisolve_rr(a, np, s);
+      if (e != cudaErrorNotSupported) return e;
+    }
     const cudaError_t e = launch_trisolve_tma(a, np, s);
     if (e != cudaErrorNotSupported) return e;
   }

@@ -6,17 +6,19 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-import bench  # noqa: E402
+import bench  # noqa: E402  (workload tables)
 from paper_2111_11148_b200 import _abi, dist  # noqa: E402
 from paper_2111_11148_b200 import cholqr as cq  # noqa: E402
 
-m = int(os.environ.get("PROF_M", bench.M_PER_GPU))
-n = int(os.environ.get("PROF_N", bench.N))
+m = int(os.environ.get("PROF_M", 1_000_000))
+n = int(os.environ.get("PROF_N", 128))
 methods = os.environ.get("PROF_METHODS", "rlu").split(",")
 dev = torch.device("cuda", 0)
 ctx = dist.make_context(0, 0, 1)
-a = bench.make_input(m, n, 0, 1, dev, float(os.environ.get("PROF_KAPPA", bench.KAPPA)), ctx=ctx)
-cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=2.0, seed=bench._seed_value())
+kap = os.environ.get("PROF_KAPPA", "1e14")
+a = cq.synthesize_dev(m, n, seed=1, sigma=bench.workload_sigma(n, kap if kap == "two-segment" else float(kap)), ctx=ctx)
+cfg = cq.SketchConfig(strategy=cq.Strategy.Gaussian, rate=float(os.environ.get("PROF_RATE", "2.0")),
+                      seed=cq.derive(1, 0x5E7C))
 q = torch.empty_like(a)
 ids = {"rlu": _abi.RLU, "rqr": _abi.RQR_GAUSSIAN, "cholqr2": _abi.CHOLQR2, "scholqr3": _abi.SCHOLQR3,
        "rqr-uniform": _abi.RQR, "cholqr": _abi.CHOLQR}

@@ -1,0 +1,3 @@
+CQR_TRISOLVE_VARIANT=0 python tools/tri_ab.py 4194304 64 > gpurun_out/plain.log 2>&1 && CQR_TRISOLVE_VARIANT=0 python tools/tri_ab.py 1000000 128 >> gpurun_out/plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:trisolve_rr -s 2 -c 1 -o gpurun_out/rr64b python tools/tri_ab.py 4194304 64 > gpurun_out/ncu_rr.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:trisolve_rr -s 2 -c 1 -o gpurun_out/rr128 python tools/tri_ab.py 1000000 128 >> gpurun_out/ncu_rr.log 2>&1; tail -2 gpurun_out/ncu_rr.log; cat gpurun_out/plain.log
