@@ -301,8 +301,10 @@ inline Matrix orthonormalize(const MatrixView& y, Orth orth, uint64_t seed, int 
     }
     case Orth::CholeskyQr2:
       return cholesky_qr2(y, o).q;
+    case Orth::HouseholderQr:  // apps.cpp:171-172: householder_qr_thin(y).q, on the device
+      return detail::run(Method::HouseholderQr, y, {}, detail::options(false, true, {}, workers)).q;
     default:
-      throw std::invalid_argument("orthonormalize: HouseholderQr is the dense baseline, not on the device path");
+      throw std::invalid_argument("orthonormalize: unknown orthogonalizer");
   }
 }
 
@@ -332,6 +334,16 @@ inline Matrix right_trisolve(const Matrix& a, const Matrix& r) {
   Matrix x = a;
   right_trisolve_in_place(x, r);
   return x;
+}
+struct ThinQr {  // kernels.hpp:186-189
+  Matrix q;
+  Matrix r;
+};
+// kernels.hpp:192-209: thin Householder QR with the R diagonal non-negative (Q adjusted), on the device
+inline ThinQr householder_qr_thin(const MatrixView& a) {
+  if (a.rows < a.cols) throw std::invalid_argument("householder_qr_thin: need rows >= cols");
+  QRFactorization f = detail::run(Method::HouseholderQr, a, {}, detail::options(false, false, {}, 1));
+  return ThinQr{std::move(f.q), std::move(f.r)};
 }
 inline Matrix qr_r_factor(const Matrix& a1) {
   if (a1.rows < a1.cols) throw std::invalid_argument("qr_r_factor: need rows >= cols");

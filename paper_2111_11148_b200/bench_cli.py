@@ -68,7 +68,7 @@ def parse_grid(text):  # grids.cpp:28-47
 
 def parse_methods(text):  # grids.cpp:61-82
     if text == "all":
-        return [m for m in range(7) if m != _abi.HOUSEHOLDER]  # the dense baseline is not on the device path
+        return list(range(7))  # grids.cpp:62-66, the HouseholderQr baseline included
     out = []
     for name in text.split(","):
         if name not in METHODS:

@@ -463,8 +463,8 @@ def orth_name(o):
 def orthonormalize(y, orth, seed, call_counter, workers=1, ctx=None):
     """apps.cpp:166-196 orthonormalize: Q of Y with R discarded (r_less). rQR
     draws fresh rows every call: uniform sketch, rate 2, seed
-    derive(seed, 0xA110 + call_counter). Householder QR is the dense baseline,
-    not on the device path (CQR_UNSUPPORTED)."""
+    derive(seed, 0xA110 + call_counter); HouseholderQr is householder_qr_thin
+    (kernels.hpp:192-209) on the device (csrc/householder.cu)."""
     opts = Options(diagnostics=False, r_less=True, workers=workers)
     if orth == Orth.RqrCholeskyQr:
         cfg = SketchConfig(rate=2.0, seed=derive(seed, 0xA110 + int(call_counter)))
@@ -472,7 +472,7 @@ def orthonormalize(y, orth, seed, call_counter, workers=1, ctx=None):
     if orth == Orth.CholeskyQr2:
         return _factor(Method.CholeskyQr2, y, None, _opts(opts), ctx=ctx)[0].q
     if orth == Orth.HouseholderQr:
-        raise NotImplementedError("orthonormalize: HouseholderQr is the dense baseline, not on the device path")
+        return _factor(Method.HouseholderQr, y, None, _opts(opts), ctx=ctx)[0].q
     raise ValueError(f"unknown orthogonalizer {orth}")
 
 
@@ -593,6 +593,13 @@ def right_trisolve(a, r, ctx=None):
     return right_trisolve_in_place(np.array(a, dtype=np.float64, order="C"), r, ctx)
 
 
+def householder_qr_thin(a, ctx=None):
+    """kernels::householder_qr_thin (kernels.hpp:192-209): (Q, R) with R's diagonal
+    non-negative, by the device's tall Householder QR (csrc/householder.cu)."""
+    f, _, _ = _factor(Method.HouseholderQr, a, None, _opts(None), ctx=ctx)
+    return f.q, f.r
+
+
 def qr_r_factor(a1, ctx=None):
     """kernels::qr_r_factor (kernels.hpp:175)."""
     a1 = _host(a1)
@@ -698,9 +705,10 @@ def geometric_sigma(n, kappa):
 
 def synthesize_dev(m, n, kappa=None, seed=0, sigma=None, device=0, m_global=None, row0=0, ctx=None):
     """matgen::synthesize on the device (matgen.cpp:21-46): rows [row0, row0+m) of
-    an m_global x n matrix U diag(sigma) V^T, returned as a CUDA tensor. Same
-    spectrum as the reference's generator; U, V differ from its Householder Q
-    factors by column signs (they are orthonormalised with device CholeskyQR2)."""
+    an m_global x n matrix U diag(sigma) V^T, returned as a CUDA tensor. U and V
+    are random_orthogonal (matgen.cpp:12-19): the thin Householder Q (signs as
+    Householder leaves them) of the reference's Gaussian counter matrices, formed
+    by the device Householder QR -- the reference's A up to rounding."""
     import torch
 
     ctx = ctx or context(device)

@@ -73,7 +73,8 @@ namespace {
 
 enum BufId {
   B_A1 = 0, B_SKPART, B_GPART, B_GTILES, B_G, B_RT, B_RH, B_R, B_RTMP, B_SGN, B_PACK1, B_PACK2, B_WORK,
-  B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X, B_SYN, B_SYNV, B_SHPART, B_SHSLOT, B_SHALL, B_SHTAB, B_SHHT
+  B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X, B_SYN, B_SYNV, B_SHPART, B_SHSLOT, B_SHALL, B_SHTAB, B_SHHT, B_HHW,
+  B_HHPART, B_HHRED, B_HHTAU
 };
 
 struct Fail {
@@ -675,6 +676,88 @@ struct Outcome {
   const double* r_dev = nullptr;
 };
 
+// ---- tall Householder QR (householder.cu) -----------------------------------------------
+// In place on this rank's rows of the m_global x n matrix W: R (n x n, replicated, unnormalised signs)
+// and tau (n); the reflectors stay below W's diagonal. Each column: one reduction pass, summed over
+// ranks (engine collectives), the reflector, one update pass.
+struct HhWs {
+  double *partial, *red, *coef, *tau;
+  int blocks;
+};
+
+HhWs hh_ws(cqr_ctx* c, long long m_local, int n) {
+  HhWs w;
+  w.blocks = cqr::hh_blocks(m_local, c->num_sms);
+  w.partial = dbuf<double>(c, B_HHPART, (size_t)w.blocks * n);
+  w.red = dbuf<double>(c, B_HHRED, (size_t)3 * n);
+  w.coef = w.red + 2 * n;
+  w.tau = dbuf<double>(c, B_HHTAU, (size_t)n);
+  return w;
+}
+
+void hh_factor(cqr_ctx* c, double* W, long long ldw, long long m_local, long long row0, int n, double* R,
+               const HhWs& w) {
+  ck(cudaMemsetAsync(R, 0, sizeof(double) * n * n, c->stream), "memset R");
+  for (int col = 0; col < n; ++col) {
+    LAUNCH(c, cqr::launch_hh_reduce(W, ldw, W, ldw, m_local, row0, col, n, w.blocks, w.partial, w.red, c->stream));
+    allreduce(c, w.red, (size_t)2 * (n - col));
+    LAUNCH(c, cqr::launch_hh_reflect_update(W, ldw, m_local, row0, col, n, w.red, w.coef, R, w.tau, c->num_sms,
+                                            c->stream));
+  }
+}
+
+// Q = H_0 ... H_{n-1} [I; 0] on this rank's rows from the reflectors of hh_factor
+void hh_form_q(cqr_ctx* c, const double* W, long long ldw, double* Q, long long ldq, long long m_local,
+               long long row0, int n, const HhWs& w) {
+  LAUNCH(c, cqr::launch_hh_qinit(Q, ldq, m_local, row0, n, c->num_sms, c->stream));
+  for (int col = n - 1; col >= 0; --col) {
+    LAUNCH(c, cqr::launch_hh_reduce(W, ldw, Q, ldq, m_local, row0, col, n, w.blocks, w.partial, w.red, c->stream));
+    allreduce(c, w.red, (size_t)2 * (n - col));
+    LAUNCH(c, cqr::launch_hh_qstep(W, ldw, Q, ldq, m_local, row0, col, n, w.red, w.tau, w.coef, c->num_sms,
+                                   c->stream));
+  }
+}
+
+// householder_qr_thin (kernels.hpp:192-209) for Method::HouseholderQr (engine.cpp:227-239): Q and R with
+// the R diagonal made non-negative (rows of R, columns of Q flipped).
+Outcome run_householder(Job& j) {
+  cqr_ctx* c = j.c;
+  const int n = j.n;
+  Outcome o;
+  {
+    StageScope t(c, CQR_STAGE_HOUSEHOLDER);
+    double* W = dbuf<double>(c, B_HHW, (size_t)std::max<long long>(j.m_local, 1) * n);
+    wait_all(j);
+    if (j.m_local > 0)
+      ck(cudaMemcpy2DAsync(W, sizeof(double) * n, j.a, sizeof(double) * j.lda, sizeof(double) * n, j.m_local,
+                           cudaMemcpyDeviceToDevice, c->stream),
+         "A copy");
+    HhWs w = hh_ws(c, j.m_local, n);
+    double* r = dbuf<double>(c, B_R, (size_t)n * n);
+    double* sgn = dbuf<double>(c, B_SGN, (size_t)n);
+    hh_factor(c, W, n, j.m_local, j.row0, n, r, w);
+    hh_form_q(c, W, n, j.q, j.ldq, j.m_local, j.row0, n, w);
+    LAUNCH(c, cqr::launch_normalize_sign(r, n, sgn, c->status, c->stream));
+    LAUNCH(c, cqr::launch_col_sign(j.q, j.ldq, j.m_local, n, sgn, c->num_sms, c->stream));
+    if (pipelined(j))  // Q back to the host
+      for (size_t i = 0; i + 1 < j.bounds.size(); ++i) {
+        const long long r0 = j.bounds[i], r1 = j.bounds[i + 1];
+        cudaEvent_t e = c->pipe_ev[j.bounds.size() - 1 + i];
+        ck(cudaEventRecord(e, c->stream), "record");
+        ck(cudaStreamWaitEvent(c->cstream, e, 0), "wait");
+        ck(cudaMemcpy2DAsync(j.q_host + r0 * j.ldq_host, sizeof(double) * j.ldq_host, j.q + r0 * j.ldq,
+                             sizeof(double) * j.ldq, sizeof(double) * n, r1 - r0, cudaMemcpyDeviceToHost, c->cstream),
+           "Q D2H");
+      }
+    o.r_dev = r;
+  }
+  push_stage(o.rep, CQR_STAGE_HOUSEHOLDER);
+  DevStatus s = read_status(c);
+  if (s.code != 0) throw Fail{s.code, s.index, status_msg(s.code)};
+  o.has_r = j.opts.r_less == 0;
+  return o;
+}
+
 // engine.cpp:241-284
 Outcome run_cholqr_family(Job& j) {
   cqr_ctx* c = j.c;
@@ -1021,7 +1104,8 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
         o = run_precond(j);
         break;
       case CQR_HOUSEHOLDER:
-        throw Fail{CQR_UNSUPPORTED, -1, "HouseholderQr (dense baseline) is outside the GPU path"};
+        o = run_householder(j);
+        break;
       default:
         throw Fail{CQR_INVALID_ARGUMENT, -1, "unknown method"};
     }
@@ -1565,53 +1649,41 @@ int cqr_residual_error_dev(cqr_ctx* c, const double* a, int64_t lda, const doubl
   });
 }
 
-// matgen.cpp:21-46 on the device: A = U diag(sigma) V^T with
-// U = orthonormalised gaussian_matrix(m, n, derive(seed, 0)) rows [row0, row0+m_local)
-// (global counters; orthonormalised by device CholeskyQR2, whose R has a positive
-// diagonal, so U matches the reference's Householder Q up to column signs) and
-// V = the same for gaussian_matrix(n, n, derive(seed, 1)). Same spectrum as the
-// reference's synthesize; not bit-identical to it.
+// matgen.cpp:21-46 on the device: A = U diag(sigma) V^T with U = random_orthogonal(m, n,
+// derive(seed, 0)) rows [row0, row0 + m_local) and V = random_orthogonal(n, n, derive(seed, 1)), where
+// random_orthogonal (matgen.cpp:12-19) is the thin Householder Q of gaussian_matrix(rows, cols, seed) with
+// the signs Householder leaves (global counters; the tall Householder's column reductions are summed over
+// the ranks when a communicator is attached). The same matrix as the reference's synthesize up to rounding.
 int cqr_synthesize_dev(cqr_ctx* c, int64_t m_local, int64_t m_global, int64_t row0, int64_t n, const double* sigma,
                        uint64_t seed, double* a, int64_t lda) {
   if (!c || n < 1 || n > 512 || m_global < n || m_local < 0 || row0 + m_local > m_global || lda < n || !sigma)
     return CQR_INVALID_ARGUMENT;
+  if (!attached(c) && (m_local != m_global || row0 != 0)) {
+    c->err = "sharded call without an attached communicator";
+    return CQR_INVALID_ARGUMENT;
+  }
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    double* u = dbuf<double>(c, B_SYN, (size_t)std::max<int64_t>(m_local, 1) * n);
-    double* v = dbuf<double>(c, B_SYNV, (size_t)n * n * 2);
-    // U: Gaussian rows, then CholeskyQR2 (sharded over the communicator when attached)
-    if (m_local > 0) LAUNCH(c, cqr::launch_rng_gaussian(derive(seed, 0), (uint64_t)row0 * n, m_local * n, u, c->stream));
-    cqr_options o = default_opts();
-    o.r_less = 1;
-    Job j{};
-    j.c = c;
-    j.method = CQR_CHOLQR2;
-    j.a = u;
-    j.m_local = m_local;
-    j.m_global = m_global;
-    j.row0 = row0;
-    j.n = (int)n;
-    j.lda = n;
-    j.q = u;
-    j.ldq = n;
-    j.cfg = default_cfg();
-    j.opts = o;
     reset_status(c);
-    run_cholqr_family(j);
-    // V: n x n, replicated on every rank
-    LAUNCH(c, cqr::launch_rng_gaussian(derive(seed, 1), 0, n * n, v, c->stream));
-    Job jv = j;
-    jv.a = v;
-    jv.q = v;
-    jv.m_local = n;
-    jv.m_global = n;
-    jv.row0 = 0;
-    jv.lda = n;
-    jv.ldq = n;
+    const size_t rows = (size_t)std::max<int64_t>(m_local, 1);
+    double* g = dbuf<double>(c, B_SYN, rows * n);    // the Gaussian, then its reflectors
+    double* u = dbuf<double>(c, B_HHW, rows * n);    // U
+    double* v = dbuf<double>(c, B_SYNV, (size_t)n * n * 4);
+    double* gv = v + (size_t)n * n;
+    double* rr = gv + (size_t)n * n;                  // R of the factorizations (not used)
+    // U (matgen.cpp:41): rows [row0, row0 + m_local) of gaussian_matrix(m, n, derive(seed, 0))
+    if (m_local > 0)
+      LAUNCH(c, cqr::launch_rng_gaussian(derive(seed, 0), (uint64_t)row0 * n, m_local * n, g, c->stream));
+    HhWs w = hh_ws(c, m_local, (int)n);
+    hh_factor(c, g, n, m_local, row0, (int)n, rr, w);
+    hh_form_q(c, g, n, u, n, m_local, row0, (int)n, w);
+    // V (matgen.cpp:35): n x n, replicated on every rank
+    LAUNCH(c, cqr::launch_rng_gaussian(derive(seed, 1), 0, n * n, gv, c->stream));
     c->local_only = 1;
-    reset_status(c);
     try {
-      run_cholqr_family(jv);
+      HhWs wv = hh_ws(c, n, (int)n);
+      hh_factor(c, gv, n, n, 0, (int)n, rr, wv);
+      hh_form_q(c, gv, n, v, n, n, 0, (int)n, wv);
     } catch (...) {
       c->local_only = 0;
       throw;
@@ -1619,12 +1691,13 @@ int cqr_synthesize_dev(cqr_ctx* c, int64_t m_local, int64_t m_global, int64_t ro
     c->local_only = 0;
     std::vector<double> hv((size_t)n * n), svt((size_t)n * n);
     copy_sync(c, hv.data(), v, sizeof(double) * n * n, cudaMemcpyDeviceToHost, "V D2H");
-    for (int64_t i = 0; i < n; ++i)
+    for (int64_t i = 0; i < n; ++i)  // svt = diag(sigma) V^T (matgen.cpp:36)
       for (int64_t jj = 0; jj < n; ++jj) svt[(size_t)(i * n + jj)] = sigma[i] * hv[(size_t)(jj * n + i)];
-    double* b = v + (size_t)n * n;
+    double* b = v + (size_t)3 * n * n;
     copy_sync(c, b, svt.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, "SVt H2D");
     if (m_local > 0) LAUNCH(c, cqr::launch_gemm_tall(u, n, b, a, lda, m_local, (int)n, c->num_sms, c->stream));
-    ck(cudaStreamSynchronize(c->stream), "sync");
+    DevStatus s = read_status(c);
+    if (s.code) throw Fail{s.code, s.index, "matgen failed"};
     c->stage_evs.clear();
     c->ev_used = 0;
   });

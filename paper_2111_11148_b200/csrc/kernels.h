@@ -110,6 +110,23 @@ cudaError_t launch_triangular_product(const double* left, const double* right, i
 // is then applied to Q's columns by the final trisolve.
 cudaError_t launch_normalize_sign(double* r, int n, double* sgn, const DevStatus* st, cudaStream_t s);
 
+// ---- householder.cu: tall Householder QR (HouseholderQr method, matgen's random_orthogonal) ----
+int hh_blocks(long long m_local, int num_sms);
+// red[0..w) = block-ordered sums of X(i,c) Y(i,c+t) over rows with global index > c, red[w..2w) = Y(c, c+t)
+// on the rank holding row c (0 elsewhere); partial holds blocks * w doubles, w = n - c
+cudaError_t launch_hh_reduce(const double* X, long long ldx, const double* Y, long long ldy, long long m_local,
+                             long long row0, int c, int n, int blocks, double* partial, double* red, cudaStream_t s);
+// the reflector of column c from the (rank-summed) red, R(c, c..), tau[c]; v stored below the diagonal
+cudaError_t launch_hh_reflect_update(double* W, long long ldw, long long m_local, long long row0, int c, int n,
+                                     double* red, double* coef, double* R, double* tau, int num_sms, cudaStream_t s);
+cudaError_t launch_hh_qinit(double* Q, long long ldq, long long m_local, long long row0, int n, int num_sms,
+                            cudaStream_t s);
+cudaError_t launch_hh_qstep(const double* W, long long ldw, double* Q, long long ldq, long long m_local,
+                            long long row0, int c, int n, const double* red, const double* tau, double* coef,
+                            int num_sms, cudaStream_t s);
+cudaError_t launch_col_sign(double* Q, long long ldq, long long m, int n, const double* sgn, int num_sms,
+                            cudaStream_t s);
+
 // ---- matgen.cu ---------------------------------------------------------------------------
 // C = X * B, X m x n (ldx), B n x n row-major, C m x n (ldc), C != X.
 cudaError_t launch_gemm_tall(const double* x, long long ldx, const double* b, double* c, long long ldc, long long m,

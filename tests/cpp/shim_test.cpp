@@ -1,6 +1,7 @@
 // Exercises include/cholqr_b200.hpp the way the reference's own doctest cases
 // exercise cholqr.hpp (test_cholqr.cpp:26-33, :52-55, :113-121, :258-262).
 // Built and run by tests/test_cpp_shim.py (GPU).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -106,13 +107,17 @@ int main() {
     o.r_less = true;
     CHECK(q1.data == rqr_cholesky_qr(y, cfg, o).q.data);
     CHECK(orthonormalize(y, Orth::CholeskyQr2, 99, 0).data == cholesky_qr2(y, o).q.data);
-    threw = false;
-    try {
-      (void)orthonormalize(y, Orth::HouseholderQr, 99, 0);
-    } catch (const std::invalid_argument&) {
-      threw = true;
-    }
-    CHECK(threw);
+    // HouseholderQr (apps.cpp:171-172) is householder_qr_thin(y).q on the device: orthonormal columns
+    Matrix qh = orthonormalize(y, Orth::HouseholderQr, 99, 0);
+    double orth = 0.0;
+    for (Index i = 0; i < qh.cols; ++i)
+      for (Index j = 0; j < qh.cols; ++j) {
+        double s = 0.0;
+        for (Index k = 0; k < qh.rows; ++k) s += qh(k, i) * qh(k, j);
+        orth = std::max(orth, std::abs(s - (i == j ? 1.0 : 0.0)));
+      }
+    CHECK(orth < 1e-13);
+    CHECK(kernels::householder_qr_thin(y).q.data == qh.data);
   }
   std::printf("shim_test %s (%d failures)\n", fails ? "FAILED" : "ok", fails);
   return fails ? 1 : 0;

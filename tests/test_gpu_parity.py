@@ -511,8 +511,10 @@ def test_orthonormalize_matches_reference_caller(orth):  # apps.cpp:166-196
         else:
             ref = o.factor(_abi.CHOLQR2, y, None, _abi.options(r_less=True)).q
             assert np.array_equal(q, ref)
-    with pytest.raises(NotImplementedError):
-        G.orthonormalize(y, G.Orth.HouseholderQr, seed, 0)
+    # apps.cpp:171-172: householder_qr_thin(y).q, on the device
+    qh = G.orthonormalize(y, G.Orth.HouseholderQr, seed, 0)
+    refq = o.householder_qr_thin(y)[0]
+    assert np.linalg.norm(qh - refq) / math.sqrt(20) <= 1e-12
 
 
 def test_one_rank_nccl_collective_path_is_bit_identical():
