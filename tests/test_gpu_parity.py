@@ -514,7 +514,7 @@ def test_orthonormalize_matches_reference_caller(orth):  # apps.cpp:166-196
     # apps.cpp:171-172: householder_qr_thin(y).q, on the device
     qh = G.orthonormalize(y, G.Orth.HouseholderQr, seed, 0)
     refq = o.householder_qr_thin(y)[0]
-    assert np.linalg.norm(qh - refq) / math.sqrt(20) <= 1e-12
+    assert np.linalg.norm(qh - refq) / math.sqrt(20) <= 4 * 1e6 * U  # Q to O(kappa u), test_gpu_householder.py
 
 
 def test_one_rank_nccl_collective_path_is_bit_identical():
