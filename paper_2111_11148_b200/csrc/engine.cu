@@ -74,7 +74,7 @@ namespace {
 enum BufId {
   B_A1 = 0, B_SKPART, B_GPART, B_GTILES, B_G, B_RT, B_RH, B_R, B_RTMP, B_SGN, B_PACK1, B_PACK2, B_WORK,
   B_IDX, B_HA, B_HQ, B_SCAL, B_DIAG, B_X, B_SYN, B_SYNV, B_SHPART, B_SHSLOT, B_SHALL, B_SHTAB, B_SHHT, B_HHW,
-  B_HHPART, B_HHRED, B_HHTAU
+  B_HHPART, B_HHRED, B_HHTAU, B_SKEXP
 };
 
 struct Fail {
@@ -372,6 +372,35 @@ const int32_t* gram_tiles_dev(cqr_ctx* c, const cqr::GramPlan& p, int slot = 0) 
     c->tiles_key[slot] = key;
   }
   return tiles;
+}
+
+// ---- the Gaussian sketch: the integer tensor-core kernel (sketch_i8.cu) when A is TMA-addressable,
+// else the DMMA kernels (sketch.cu) ------------------------------------------------------------
+struct SketchRun {
+  cqr::SketchPlan p;
+  double* part = nullptr;
+  int* colexp = nullptr;
+};
+
+SketchRun sketch_setup(cqr_ctx* c, const double* a, long long lda, long long m_local, long long m_global,
+                       long long row0, int n, int l, int splits) {
+  SketchRun r;
+  const bool i8 = cqr::sketch_i8_ok(a, lda, m_global, row0, n);
+  r.p = cqr::sketch_plan(m_local, n, l, c->num_sms, cqr::sketch_ws_ok(a, lda, m_global, row0, n), splits);
+  if (i8) cqr::sketch_i8_plan(r.p, m_local, n, l, c->num_sms);
+  r.part = dbuf<double>(c, B_SKPART, std::max<size_t>(r.p.partial_doubles, 1));
+  if (i8) r.colexp = dbuf<int>(c, B_SKEXP, std::max<size_t>(r.p.aux_ints, 1));
+  return r;
+}
+
+cudaError_t sketch_launch(cqr_ctx* c, const SketchRun& r, const double* a, long long lda, long long m_global,
+                          long long row0, uint64_t seed, int vec, int check, int y0 = 0, int y1 = -1) {
+  if (r.p.i8) {
+    ++c->launches;  // the exponent pre-pass + the tensor-core kernel
+    return cqr::launch_sketch_i8(r.p, a, lda, m_global, row0, seed, r.part, r.colexp, c->status, c->stream, y0, y1);
+  }
+  return cqr::launch_sketch_gaussian(r.p, a, lda, m_global, row0, seed, r.part, vec, check, c->status, c->stream, y0,
+                                     y1);
 }
 
 // ---- rank-count-independent sharded Gram (gram_shard.cu) ------------------------------
@@ -834,10 +863,9 @@ Outcome run_precond(Job& j) {
     {
       StageScope t(c, CQR_STAGE_SKETCH);
       if (try_cfg.strategy == CQR_GAUSSIAN) {
-        cqr::SketchPlan sp =
-            cqr::sketch_plan(j.m_local, n, (int)l, c->num_sms, cqr::sketch_ws_ok(j.a, j.lda, m, j.row0, n),
-                             pipelined(j) ? (int)j.bounds.size() - 1 : 1);
-        double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
+        const SketchRun sr = sketch_setup(c, j.a, j.lda, j.m_local, m, j.row0, n, (int)l,
+                                          pipelined(j) ? (int)j.bounds.size() - 1 : 1);
+        const cqr::SketchPlan& sp = sr.p;
         if (j.m_local > 0) {
           const int vec = vec_ok(j.a, j.lda, n) ? 1 : 0, chk = attempt == 0 ? j.check_first : 0;
           if (pipelined(j) && j.waited + 1 < (int)j.bounds.size()) {
@@ -846,17 +874,14 @@ Outcome run_precond(Job& j) {
             for (size_t i = 1; i < j.bounds.size() && y < sp.kchunks; ++i) {
               wait_rows(j, j.bounds[i]);
               const int y1 = (i + 1 == j.bounds.size()) ? sp.kchunks : (int)(j.bounds[i] / sp.rows_per_chunk);
-              if (y1 > y)
-                LAUNCH(c, cqr::launch_sketch_gaussian(sp, j.a, j.lda, m, j.row0, seed, part, vec, chk, c->status,
-                                                      c->stream, y, y1));
+              if (y1 > y) LAUNCH(c, sketch_launch(c, sr, j.a, j.lda, m, j.row0, seed, vec, chk, y, y1));
               y = std::max(y, y1);
             }
           } else {
             wait_all(j);
-            LAUNCH(c, cqr::launch_sketch_gaussian(sp, j.a, j.lda, m, j.row0, seed, part, vec, chk, c->status,
-                                                  c->stream));
+            LAUNCH(c, sketch_launch(c, sr, j.a, j.lda, m, j.row0, seed, vec, chk));
           }
-          LAUNCH(c, cqr::launch_sketch_reduce(sp, part, a1, c->status, c->stream));
+          LAUNCH(c, cqr::launch_sketch_reduce(sp, sr.part, a1, c->status, c->stream));
         } else {
           ck(cudaMemsetAsync(a1, 0, sizeof(double) * l * n, c->stream), "memset");
         }
@@ -1510,13 +1535,10 @@ int cqr_sketch_gaussian_dev(cqr_ctx* c, const double* a, int64_t m_local, int64_
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     reset_status(c);
-    cqr::SketchPlan sp =
-        cqr::sketch_plan(m_local, (int)n, (int)l, c->num_sms, cqr::sketch_ws_ok(a, lda, m_global, row0, (int)n));
-    double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
+    const SketchRun sr = sketch_setup(c, a, lda, m_local, m_global, row0, (int)n, (int)l, 1);
     if (m_local > 0) {
-      LAUNCH(c, cqr::launch_sketch_gaussian(sp, a, lda, m_global, row0, seed, part, vec_ok(a, lda, (int)n) ? 1 : 0,
-                                            0, c->status, c->stream));
-      LAUNCH(c, cqr::launch_sketch_reduce(sp, part, a1_dev, c->status, c->stream));
+      LAUNCH(c, sketch_launch(c, sr, a, lda, m_global, row0, seed, vec_ok(a, lda, (int)n) ? 1 : 0, 0));
+      LAUNCH(c, cqr::launch_sketch_reduce(sr.p, sr.part, a1_dev, c->status, c->stream));
     } else {
       ck(cudaMemsetAsync(a1_dev, 0, sizeof(double) * l * n, c->stream), "memset");
     }
@@ -1536,11 +1558,9 @@ int cqr_sketch_gaussian(cqr_ctx* c, const double* a, int64_t m, int64_t n, int64
                          cudaMemcpyHostToDevice, c->stream),
        "A H2D");
     reset_status(c);
-    cqr::SketchPlan sp = cqr::sketch_plan(m, (int)n, (int)l, c->num_sms, cqr::sketch_ws_ok(da, n, m, 0, (int)n));
-    double* part = dbuf<double>(c, B_SKPART, std::max<size_t>(sp.partial_doubles, 1));
-    LAUNCH(c, cqr::launch_sketch_gaussian(sp, da, n, m, 0, seed, part, vec_ok(da, n, (int)n) ? 1 : 0, 0, c->status,
-                                          c->stream));
-    LAUNCH(c, cqr::launch_sketch_reduce(sp, part, d1, c->status, c->stream));
+    const SketchRun sr = sketch_setup(c, da, n, m, m, 0, (int)n, (int)l, 1);
+    LAUNCH(c, sketch_launch(c, sr, da, n, m, 0, seed, vec_ok(da, n, (int)n) ? 1 : 0, 0));
+    LAUNCH(c, cqr::launch_sketch_reduce(sr.p, sr.part, d1, c->status, c->stream));
     ck(cudaMemcpyAsync(a1, d1, sizeof(double) * l * n, cudaMemcpyDeviceToHost, c->stream), "A1 D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
   });

@@ -1,0 +1,533 @@
+// sketch_i8.cu — the Gaussian sketch A1 = Omega A (sketch.cpp:94-116) as an exact integer product on
+// the 5th-generation tensor cores (tcgen05.mma kind::i8, s32 accumulators in TMEM).
+//
+// FP64 has no tcgen05 kind; DMMA (sketch.cu) tops out at 37 TFLOP/s and shares its pipe with the
+// Box-Muller draws. Here both operands become 56-bit fixed-point integers cut into 7 signed byte digits
+// ("Ozaki" splitting):
+//   Omega(i,k) = N_ik 2^-51,        N_ik = round(w 2^51),          |N| < 2^55 (|w| < 9 for every draw);
+//   A(k,j)     = M_kj 2^(E_j - 54), M_kj = round(a 2^(54 - E_j)),  |M| < 2^54,
+// E_j the exponent bound of column j over the k-chunk (max |a| < 2^E_j), from a pre-pass that also
+// checks finiteness. The digits are balanced: N = sum_s D_s 2^(8(6-s)) with every D_s in [-128, 127],
+// read off the bytes of N + 0x808080808080 (the lower six bytes with their top bit flipped), so the
+// dropped low-order products are zero-mean and do not drift with K. The 28 digit products with
+// s + t <= 6 accumulate per level u = s + t in TMEM -- exactly: |level| <= 7 * 128^2 * K < 2^31 for
+// k-chunks of <= 16384 rows -- and the epilogue recombines sum_u ACC_u 2^(8(6-u)) in 64-bit integers,
+// converts (two roundings) and scales by 2^(E_j - 57). The dropped levels weigh <= 2^-56 of the leading
+// one: as accurate as an FP64 GEMM (tests: <= 1e-13 against the oracle's sequential fma chains). Omega
+// is still the reference's gaussian_at(seed, i*m + k), draw for draw (boxmuller.cuh); it never touches
+// HBM.
+//
+// Warp roles (one CTA per SM, 128 Omega rows x 64 columns of A x one k-chunk):
+//   warp 0      TMEM allocation; lane 0 issues the 10 MMAs of each 32-row step (M=128, N<=256, K=32)
+//               and commits them to the stage's `empty` barrier;
+//   warp 1      lane 0 streams A's FP64 rows (32 x 64 tiles) by TMA into a two-stage ring;
+//   warps 2-9   cut A's tile into the 7 digit planes (K-major core-matrix layout, SWIZZLE_NONE); warps
+//               2-5 then run the epilogue (each warp one TMEM lane quadrant);
+//   warps 6..   draw Omega (Box-Muller pairs, 4 side by side) and cut each draw into its digit planes.
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "boxmuller.cuh"
+#include "common.cuh"
+#include "kernels.h"
+#include "tma.cuh"
+
+namespace cqr {
+
+namespace {
+
+constexpr int kI8Rows = 128;      // Omega rows per CTA (MMA M)
+constexpr int kI8Cols = 64;       // A columns per CTA (MMA N)
+constexpr int kI8K = 32;          // rows of A per step (MMA K for kind::i8)
+constexpr int kI8Stages = 3;      // digit-plane ring
+#ifndef CQR_I8_ASTAGES
+#define CQR_I8_ASTAGES 4
+#endif
+constexpr int kI8AStages = CQR_I8_ASTAGES;  // FP64 A ring
+#ifndef CQR_I8_GEN
+#define CQR_I8_GEN 16
+#endif
+constexpr int kI8Gen = CQR_I8_GEN;  // generator warps
+#ifndef CQR_I8_SLICE
+#define CQR_I8_SLICE 8
+#endif
+constexpr int kI8Slice = CQR_I8_SLICE;  // slicer warps (the first four also run the epilogue)
+constexpr int kI8Warps = 2 + kI8Slice + kI8Gen;
+constexpr long long kI8MaxChunk = 16384;  // rows per k-chunk: 7 * 128^2 * 16384 < 2^31
+constexpr int kDig = 7;                 // byte digits per operand
+constexpr int kOmPlane = kI8Rows * kI8K;  // bytes per Omega digit plane (4 KB)
+constexpr int kAPlane = kI8Cols * kI8K;   // bytes per A digit plane (2 KB)
+constexpr int kStageBytes = kDig * (kOmPlane + kAPlane);
+constexpr int kATile = kI8K * kI8Cols;    // doubles per FP64 A stage
+constexpr size_t kI8Smem = (size_t)kI8Stages * kStageBytes + (size_t)kI8AStages * kATile * 8 + 1024;
+
+__constant__ BmTables c_bm_i8;
+
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t sbo = 256) {
+  // K-major, SWIZZLE_NONE: 8-row x 16-byte core matrices, LBO = 128 B (the two K halves), SBO = the stride
+  // between 8-row groups (256 B when a plane's row groups are consecutive)
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) |
+         ((uint64_t)1 << 46);
+}
+// Omega planes, row-group-major: an 8-row group holds its 256-byte core-matrix pair of every digit plane
+// (1792 B), so the rows one CTA of a cluster draws are ONE contiguous chunk across all planes
+constexpr int kOmGroup = 7 * 256;
+// s32 accumulator, M = 128, N columns, K-major s8 operands
+__host__ __device__ constexpr uint32_t idesc_i8(int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kI8Rows >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// every CTA of the cluster (ctaMask) gets one arrival on its barrier at this smem offset
+__device__ __forceinline__ void umma_commit_cluster(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// shared::cta -> another CTA's shared memory (shared::cluster address), completing on that CTA's barrier
+__device__ __forceinline__ void bulk_copy_cluster(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                                  uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_cluster),
+      "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// byte offset of element (r, k) (k < 32) of an R-row K-major digit plane
+__device__ __forceinline__ int plane_off(int r, int k) {
+  return (r >> 3) * 256 + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
+}
+// the same element in the row-group-major Omega planes (plane p at + p * 256)
+__device__ __forceinline__ int om_off(int r, int k) {
+  return (r >> 3) * kOmGroup + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
+}
+
+// 8 consecutive entries (k = 8o .. 8o+7 of one row) as 64-bit two's complement integers (lo, hi words)
+// -> digit plane s (byte 6 - s) receives the 8 bytes [entry 0 .. entry 7] at plane s + off: an 8x7
+// byte transpose with prmt
+__device__ __forceinline__ void transpose_store(const uint32_t (&lo)[8], const uint32_t (&hi)[8],
+                                                unsigned char* planes, int plane_bytes, int off) {
+#pragma unroll
+  for (int s = 0; s < kDig; ++s) {
+    const int b = 6 - s;
+    const uint32_t* w = b < 4 ? lo : hi;
+    const uint32_t bb = (uint32_t)(b & 3);
+    const uint32_t sel = bb | ((bb + 4) << 4);  // out byte 0 = x.byte bb, out byte 1 = y.byte bb
+    const uint32_t x01 = __byte_perm(w[0], w[1], sel), x23 = __byte_perm(w[2], w[3], sel);
+    const uint32_t x45 = __byte_perm(w[4], w[5], sel), x67 = __byte_perm(w[6], w[7], sel);
+    *reinterpret_cast<uint2*>(planes + s * plane_bytes + off) =
+        make_uint2(__byte_perm(x01, x23, 0x5410u), __byte_perm(x45, x67, 0x5410u));
+  }
+}
+
+// balanced byte digits of v (|v| < 2^55 - 2^48): the bytes of v + 0x808080808080, the lower six with
+// their top bit flipped (byte - 128), the top one as is
+__device__ __forceinline__ void split64(long long v, uint32_t& lo, uint32_t& hi) {
+  const unsigned long long w = (unsigned long long)v + 0x0000808080808080ull;
+  lo = (uint32_t)w ^ 0x80808080u;
+  hi = (uint32_t)(w >> 32) ^ 0x00008080u;
+}
+
+__global__ void __launch_bounds__(kI8Warps * 32, 1)
+    sketch_i8_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global,
+                     long long row0, int l, uint64_t seed, long long rows_per_chunk, const int* __restrict__ colexp,
+                     double* __restrict__ partial, int lp, int np_total, int y0, const DevStatus* st) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ BmTables T;
+  __shared__ __align__(8) uint64_t full[kI8Stages], empty[kI8Stages], afull[kI8AStages], aempty[kI8AStages], done;
+  __shared__ uint32_t tmem_base;
+  __shared__ int sexp[kI8Cols];
+  if (failed(st)) return;
+  unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* sOm = sm;                                    // [stage][plane][4 KB]
+  unsigned char* sAp = sm + kI8Stages * kDig * kOmPlane;      // [stage][plane][2 KB]
+  double* sAf = reinterpret_cast<double*>(sm + kI8Stages * kStageBytes);  // [astage][32 x 64]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s0 = blockIdx.x * kI8Rows;
+  const int ky = blockIdx.y + y0;
+  const int col0 = blockIdx.z * kI8Cols;
+  // the column tiles of one (Omega tile, k-chunk) form a cluster (gridDim.z CTAs): CTA r draws Omega rows
+  // [r 128 / C, (r + 1) 128 / C) once and stores their digits into every CTA's planes
+  const int ncta = (int)gridDim.z, crank = (int)blockIdx.z;
+  const long long k_begin = (long long)ky * rows_per_chunk;
+  const long long k_end = min(m_local, k_begin + rows_per_chunk);
+  const int nsteps = k_end > k_begin ? (int)((k_end - k_begin + kI8K - 1) / kI8K) : 0;
+  {
+    const double* src = reinterpret_cast<const double*>(&c_bm_i8);
+    double* dst = reinterpret_cast<double*>(&T);
+    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += kI8Warps * 32) dst[e] = src[e];
+  }
+  // an all-zero column keeps the initial value: any bound >= its entries works, -1074 keeps the scalings finite
+  if (tid < kI8Cols) sexp[tid] = max(colexp[(long long)ky * np_total + col0 + tid], -1074);
+  if (tid == 0) {
+    for (int s = 0; s < kI8Stages; ++s) {
+      // the local generators and slicers; the partners' Omega rows arrive as bulk-copy bytes (expect_tx)
+      mbar_init(&full[s], kI8Gen * 32 + kI8Slice * 32);
+      mbar_init(&empty[s], ncta);                              // every CTA's MMAs have read the stage
+    }
+    for (int s = 0; s < kI8AStages; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], kI8Slice * 32);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_shared();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();  // the partners' barriers are initialised before anyone arrives on them
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // ---- MMA issuer: per step, D[level s+t] += Omega digit s x A digit t (s + t <= 7)
+    if (lane == 0) {
+      for (int stp = 0; stp < nsteps; ++stp) {
+        const int s = stp % kI8Stages;
+        mbar_wait(&full[s], (stp / kI8Stages) & 1);  // partners' bulk copies included
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t om = smem_u32(sOm + s * kDig * kOmPlane), ap = smem_u32(sAp + s * kDig * kAPlane);
+#ifndef CQR_I8_NOMMA  // probe: the producers' bound (no MMAs)
+        // Omega digit sd against the stacked A digit planes 0 .. 6-sd (consecutive 2 KB planes = one taller
+        // K-major B operand): its N = 64 (7 - sd) output columns land on TMEM levels sd .. 6, i.e. on
+        // columns [64 sd, 448) -- one or two MMAs (N <= 256) per Omega digit, 10 per step
+#pragma unroll
+        for (int sd = 0; sd < kDig; ++sd) {
+          const uint32_t acc = (stp > 0 || sd > 0) ? 1u : 0u;  // sd = 0 writes every level first
+          const uint64_t da = umma_sdesc(om + sd * 256, kOmGroup);
+          const int nt = kDig - sd;                      // A digit planes 0 .. nt-1
+          const int n1 = nt > 4 ? 4 : nt;                // first MMA: up to 4 planes (N <= 256)
+          umma_i8(tmem + 64u * (uint32_t)sd, da, umma_sdesc(ap), idesc_i8(64 * n1), acc);
+          if (nt > n1)
+            umma_i8(tmem + 64u * (uint32_t)(sd + n1), da, umma_sdesc(ap + n1 * kAPlane), idesc_i8(64 * (nt - n1)), acc);
+        }
+#endif
+        // the stage's smem (in every CTA of the cluster) may be rewritten once every CTA's MMAs have read it
+        umma_commit_cluster(&empty[s], (uint16_t)((1u << ncta) - 1u));
+      }
+      umma_commit(&done);
+    }
+  } else if (warp == 1) {
+    // ---- A's FP64 rows by TMA
+    if (lane == 0) {
+      for (int stp = 0; stp < nsteps; ++stp) {
+        const int s = stp % kI8AStages;
+        mbar_wait(&aempty[s], ((stp / kI8AStages) & 1) ^ 1);
+        mbar_expect_tx(&afull[s], kATile * 8);
+        tma_load_2d(sAf + s * kATile, &tma_a, col0, (int)(k_begin + (long long)stp * kI8K), &afull[s]);
+      }
+    }
+  } else if (warp < 2 + kI8Slice) {
+    // ---- A slicers: unit u = (column j, k-octet o), 256 units per step
+    const int st_id = tid - 64;
+    constexpr int SUPT = 256 / (kI8Slice * 32);  // units per thread
+    for (int stp = 0; stp < nsteps; ++stp) {
+      const int s = stp % kI8Stages, sa = stp % kI8AStages;
+      mbar_wait(&afull[sa], (stp / kI8AStages) & 1);
+      mbar_wait(&empty[s], ((stp / kI8Stages) & 1) ^ 1);
+      const long long kb = k_begin + (long long)stp * kI8K;
+      const double* At = sAf + sa * kATile;
+      unsigned char* planes = sAp + s * kDig * kAPlane;
+#ifndef CQR_I8_NOSLICE  // probe: without the A slicing
+#pragma unroll
+      for (int uu = 0; uu < SUPT; ++uu) {
+        const int u = st_id + kI8Slice * 32 * uu;
+        const int j = u & 63, o = u >> 6;
+        // a 2^(54 - E_j) as two exact power-of-two scalings (54 - E_j may exceed the double range)
+        const int sh = 54 - sexp[j], sh1 = sh / 2;
+        const double f1 = ldexp(1.0, sh1), f2 = ldexp(1.0, sh - sh1);
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int k = 8 * o + e;
+          const double v = (kb + k < k_end) ? At[k * kI8Cols + j] : 0.0;  // rows past the chunk: zero
+          split64(__double2ll_rn((v * f1) * f2), lo[e], hi[e]);
+        }
+        transpose_store(lo, hi, planes, kAPlane, plane_off(j, 8 * o));
+      }
+#endif
+      fence_async_shared();  // generic-proxy stores -> visible to the tensor core (async proxy)
+      mbar_arrive(&full[s]);
+      mbar_arrive(&aempty[sa]);
+    }
+  } else {
+    // ---- Omega generators: unit u = (Omega row i, k-octet o) = 4 Box-Muller pairs; this CTA draws the
+    // units [crank UNITS / C, (crank + 1) UNITS / C) of each step for the whole cluster
+    const int gt = tid - 32 * (2 + kI8Slice);
+    constexpr int UNITS = kI8Rows * (kI8K / 8);
+    const int u_lo = crank * UNITS / ncta, u_hi = (crank + 1) * UNITS / ncta;
+    constexpr int UPT = (UNITS + kI8Gen * 32 - 1) / (kI8Gen * 32);  // units per thread per step (at most)
+    uint64_t z[UPT];
+    bool live[UPT];
+#pragma unroll
+    for (int uu = 0; uu < UPT; ++uu) {
+      const int u = min(u_lo + gt + kI8Gen * 32 * uu, UNITS - 1);
+      const int i = u >> 2, o = u & 3;
+      // first counter word of the unit's first pair: c = (s0 + i) m_global + row0 + k (even), pair c/2
+      const unsigned long long c0 =
+          (unsigned long long)(s0 + i) * (unsigned long long)m_global + row0 + k_begin + 8 * o;
+      z[uu] = seed + (2 * (c0 >> 1) + 1) * kGolden;
+      live[uu] = s0 + i < l;
+    }
+    const uint32_t slice = (uint32_t)(kDig * kOmPlane / ncta);  // this CTA's rows of all planes: one chunk
+    for (int stp = 0; stp < nsteps; ++stp) {
+      const int s = stp % kI8Stages;
+      mbar_wait(&empty[s], ((stp / kI8Stages) & 1) ^ 1);  // every CTA's MMAs are done with stage s
+      unsigned char* planes = sOm + s * kDig * kOmPlane;
+#pragma unroll 1
+      for (int uu = 0; uu < UPT; ++uu) {
+        const int u = u_lo + gt + kI8Gen * 32 * uu;
+        if (u >= u_hi) break;
+        const int i = u >> 2, o = u & 3;
+        uint64_t zz[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) zz[q] = z[uu] + (uint64_t)(2 * q) * kGolden;
+        z[uu] += (uint64_t)kI8K * kGolden;
+        double ge[4], go[4];
+#ifdef CQR_I8_NOGEN  // probe: the MMA side's bound (constant draws)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ge[q] = (double)(zz[q] & 255) * 0x1p-6, go[q] = 0.5;
+#else
+        gaussian_pairs_z<4>(T, zz, ge, go);
+#endif
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // round(w 2^51): the scaling is exact, the conversion rounds
+          split64(live[uu] ? __double2ll_rn(ge[q] * 0x1p51) : 0ll, lo[2 * q], hi[2 * q]);
+          split64(live[uu] ? __double2ll_rn(go[q] * 0x1p51) : 0ll, lo[2 * q + 1], hi[2 * q + 1]);
+        }
+        transpose_store(lo, hi, planes, 256, om_off(i, 8 * o));
+      }
+      fence_async_shared();  // the digit stores -> the tensor core's and the bulk copies' (async) view
+      if (ncta > 1) {
+        // all generators' stores are done; lanes 0 .. C-2 of the first generator warp ship this CTA's rows
+        // (one contiguous chunk of whole row groups, all planes) to one partner each
+        asm volatile("bar.sync 1, %0;" ::"n"(kI8Gen * 32) : "memory");
+        if (gt < ncta - 1) {
+          const int r = gt < crank ? gt : gt + 1;
+          const uint32_t dst = mapa_rank(smem_u32(planes), (uint32_t)r);
+          const uint32_t bar = mapa_rank(smem_u32(&full[s]), (uint32_t)r);
+          bulk_copy_cluster(dst + crank * slice, planes + crank * slice, slice, bar);
+        }
+        if (gt == 0)
+          mbar_arrive_expect(&full[s], (uint32_t)(ncta - 1) * slice);  // the partners' chunks to come
+        else
+          mbar_arrive(&full[s]);
+      } else {
+        mbar_arrive(&full[s]);
+      }
+    }
+  }
+
+  // ---- epilogue: warps 2-5 (TMEM lane quadrants 2, 3, 0, 1), row i = 32 * (warp % 4) + lane
+  if (warp >= 2 && warp < 6) {
+    const int quad = warp & 3;
+    const int i = 32 * quad + lane;
+    double* out = partial + ((long long)ky * lp + s0 + i) * np_total + col0;
+    if (nsteps == 0) {  // an empty chunk: no MMA initialised the accumulators
+      for (int j = 0; j < kI8Cols; ++j) out[j] = 0.0;
+    } else {
+    mbar_wait(&done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+    for (int c0 = 0; c0 < kI8Cols; c0 += 8) {
+      long long hi[8], lo[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0;
+#pragma unroll
+      for (int u = 0; u < kDig; ++u) {
+        uint32_t v[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                       "=r"(v[7])
+                     : "r"(tmem + ((uint32_t)(32 * quad) << 16) + 64u * u + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const long long a = (long long)(int)v[j];
+          if (u < 3)
+            hi[j] += a << (8 * (2 - u));
+          else
+            lo[j] += a << (8 * (6 - u));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        // N M ~ sum_u ACC_u 2^(8(12-u)) = 2^48 (hi 2^32 + lo); value = N M 2^-51 2^(E_j - 54)
+        const double v = fma((double)hi[j], 0x1p32, (double)lo[j]);
+        out[c0 + j] = ldexp(v, sexp[c0 + j] - 57);
+      }
+    }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();  // no partner still stores into this CTA's smem or arrives on its barriers
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// exponent bound of each column over each k-chunk (max |a| < 2^E), non-finite entries flagged. Grid
+// (chunks, column blocks, row slices): each block folds its slice with atomicMax (order-independent,
+// so deterministic) into colexp, which the caller initialised to a very small value.
+constexpr int kExpSlices = 8;
+__global__ void sketch_colexp_kernel(const double* __restrict__ a, long long lda, long long m_local, int n,
+                                     long long rows_per_chunk, int np, int y0, int* __restrict__ colexp,
+                                     DevStatus* st) {
+  __shared__ double smax[4][64];
+  const int ky = blockIdx.x + y0;
+  const int jl = threadIdx.x & 63, rl = threadIdx.x >> 6;
+  const int j = blockIdx.y * 64 + jl;
+  const long long c0 = (long long)ky * rows_per_chunk, c1 = min(m_local, c0 + rows_per_chunk);
+  const long long span = (c1 - c0 + kExpSlices - 1) / kExpSlices;
+  const long long k0 = c0 + span * blockIdx.z, k1 = min(c1, k0 + span);
+  double mx = 0.0;
+  bool bad = false;
+  if (j < n) {
+    long long k = k0 + rl;
+    for (; k + 12 < k1; k += 16) {  // four independent loads in flight per thread
+      const double v0 = __ldg(a + k * lda + j), v1 = __ldg(a + (k + 4) * lda + j);
+      const double v2 = __ldg(a + (k + 8) * lda + j), v3 = __ldg(a + (k + 12) * lda + j);
+      bad |= !isfinite(v0) || !isfinite(v1) || !isfinite(v2) || !isfinite(v3);
+      mx = fmax(mx, fmax(fmax(fabs(v0), fabs(v1)), fmax(fabs(v2), fabs(v3))));
+    }
+    for (; k < k1; k += 4) {
+      const double v = __ldg(a + k * lda + j);
+      bad |= !isfinite(v);
+      mx = fmax(mx, fabs(v));
+    }
+  }
+  smax[rl][jl] = mx;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status_invalid(st);
+  __syncthreads();
+  if (rl == 0 && j < np) {
+    const double m4 = fmax(fmax(smax[0][jl], smax[1][jl]), fmax(smax[2][jl], smax[3][jl]));
+    if (m4 > 0.0) {
+      int e;
+      frexp(m4, &e);  // m4 = f 2^e, f in [0.5, 1): m4 < 2^e
+      atomicMax(colexp + (long long)ky * np + j, e);
+    }
+  }
+}
+
+cudaError_t ensure_tables_i8(cudaStream_t s) {
+  static std::mutex mu;
+  static unsigned long long done = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (dev < 64 && (done >> dev) & 1ull) return cudaSuccess;
+  BmTables t;
+  bm_tables_host(&t);
+  e = cudaMemcpyToSymbolAsync(c_bm_i8, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && dev < 64) done |= 1ull << dev;
+  return e;
+}
+
+}  // namespace
+
+bool sketch_i8_ok(const double* a, long long lda, long long m_global, long long row0, int n) {
+  static const bool off = std::getenv("CQR_SKETCH_DMMA") != nullptr;  // A/B: the DMMA kernels
+  if (off || n < 1 || n > 512 || (m_global & 1) || (row0 & 1) || m_global > (1LL << 31) - 64) return false;
+  CUtensorMap probe;
+  return make_tmap_2d(&probe, a, n, std::max<long long>(1, m_global), lda, kI8Cols, kI8K,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+void sketch_i8_plan(SketchPlan& p, long long m_local, int n, int l, int num_sms) {
+  p.i8 = 1;
+  p.ws = 0;
+  p.n = n;
+  p.l = l;
+  p.np = (n + kI8Cols - 1) / kI8Cols * kI8Cols;
+  p.npc = kI8Cols;
+  p.st = kI8Rows;
+  p.m_local = m_local;
+  p.s_tiles = (l + kI8Rows - 1) / kI8Rows;
+  p.lp = p.s_tiles * kI8Rows;
+  const long long per = (long long)p.s_tiles * (p.np / kI8Cols);
+  long long kc = (m_local + kI8MaxChunk - 1) / kI8MaxChunk;
+  if (kc < 1) kc = 1;
+  // whole waves of one CTA per SM where the chunk bound allows
+  const long long waves = (kc * per + num_sms - 1) / num_sms;
+  const long long kc_w = waves * num_sms / per;
+  if (kc_w > kc) kc = kc_w;
+  const long long max_kc = (m_local + kI8K - 1) / kI8K;
+  if (kc > max_kc) kc = max_kc;
+  long long rpc = (m_local + kc - 1) / kc;
+  rpc = (rpc + kI8K - 1) / kI8K * kI8K;
+  if (rpc < kI8K) rpc = kI8K;
+  p.rows_per_chunk = rpc;
+  p.kchunks = (int)((m_local + rpc - 1) / rpc);
+  if (p.kchunks < 1) p.kchunks = 1;
+  p.partial_doubles = (size_t)p.kchunks * p.lp * p.np;
+  p.aux_ints = (size_t)p.kchunks * p.np;
+}
+
+cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
+                             uint64_t seed, double* partial, int* colexp, const DevStatus* st, cudaStream_t s, int y0,
+                             int y1) {
+  if (y1 < 0) y1 = p.kchunks;
+  if (y1 <= y0) return cudaSuccess;
+  cudaError_t e = ensure_tables_i8(s);
+  if (e != cudaSuccess) return e;
+  CUtensorMap tm;
+  if (!make_tmap_2d(&tm, a, p.n, p.m_local, lda, kI8Cols, kI8K, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  e = cudaMemsetAsync(colexp + (size_t)y0 * p.np, 0x80, sizeof(int) * (size_t)(y1 - y0) * p.np, s);  // very small
+  if (e != cudaSuccess) return e;
+  sketch_colexp_kernel<<<dim3((unsigned)(y1 - y0), (unsigned)(p.np / 64), kExpSlices), 256, 0, s>>>(
+      a, lda, p.m_local, p.n, p.rows_per_chunk, p.np, y0, colexp, const_cast<DevStatus*>(st));
+  e = cudaFuncSetAttribute(sketch_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / kI8Cols));
+  cfg.blockDim = dim3(kI8Warps * 32, 1, 1);
+  cfg.dynamicSmemBytes = kI8Smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // the column tiles share their Omega draws
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = (unsigned)(p.np / kI8Cols);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sketch_i8_kernel, tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
+                            (const int*)colexp, partial, p.lp, p.np, y0, st);
+}
+
+}  // namespace cqr

@@ -29,9 +29,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
   return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
-__host__ __device__ constexpr uint32_t idesc_s8(int M, int N) {
+__host__ __device__ constexpr uint32_t idesc_s8(int M, int N, int asg = 1, int bsg = 1) {
   return (2u << 4)                      // D format s32
-         | (1u << 7) | (1u << 10)       // A, B signed 8-bit
+         | ((uint32_t)asg << 7) | ((uint32_t)bsg << 10)  // A, B signed (1) / unsigned (0) 8-bit
          | ((uint32_t)(N >> 3) << 17)   // N / 8
          | ((uint32_t)(M >> 4) << 24);  // M / 16
 }
@@ -44,7 +44,7 @@ __host__ __device__ inline int koff(int r, int k, int R) {
 
 template <int N>
 __global__ void umma_probe(const int8_t* __restrict__ ga, const int8_t* __restrict__ gb, int ktot, int reps,
-                           int* __restrict__ out, long long* cycles) {
+                           int* __restrict__ out, long long* cycles, int asg, int bsg) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar;
@@ -78,7 +78,7 @@ __global__ void umma_probe(const int8_t* __restrict__ ga, const int8_t* __restri
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
-            "l"(da), "l"(db), "r"(idesc_s8(128, N)), "r"(acc));
+            "l"(da), "l"(db), "r"(idesc_s8(128, N, asg, bsg)), "r"(acc));
       }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
   }
@@ -111,7 +111,7 @@ __global__ void umma_probe(const int8_t* __restrict__ ga, const int8_t* __restri
 }
 
 template <int N>
-int run(int ktot, int reps) {
+int run(int ktot, int reps, int asg = 1, int bsg = 1) {
   std::vector<int8_t> A(128 * ktot), B(N * ktot), ha(128 * ktot), hb(N * ktot);
   srand(7 + N);
   for (auto& x : A) x = (int8_t)(rand() % 256 - 128);
@@ -132,7 +132,7 @@ int run(int ktot, int reps) {
   CK(cudaMemcpy(db, hb.data(), hb.size(), cudaMemcpyHostToDevice));
   const size_t smem = (size_t)(128 + N) * ktot + 1024;
   CK(cudaFuncSetAttribute(umma_probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  umma_probe<N><<<1, 128, smem>>>(da, db, ktot, reps, dout, dcyc);
+  umma_probe<N><<<1, 128, smem>>>(da, db, ktot, reps, dout, dcyc, asg, bsg);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<int> out(128 * N);
@@ -143,13 +143,15 @@ int run(int ktot, int reps) {
   for (int i = 0; i < 128; ++i)
     for (int j = 0; j < N; ++j) {
       long long s = 0;
-      for (int k = 0; k < ktot; ++k) s += (long long)A[i * ktot + k] * B[j * ktot + k];
+      for (int k = 0; k < ktot; ++k)
+        s += (long long)(asg ? (int)A[i * ktot + k] : (int)(uint8_t)A[i * ktot + k]) *
+             (bsg ? (int)B[j * ktot + k] : (int)(uint8_t)B[j * ktot + k]);
       s *= reps;
       if ((int)s != out[i * N + j]) ++bad;
     }
   const long long nmma = (long long)reps * (ktot / 32);
-  std::printf("N=%3d ktot=%d reps=%d: mismatches %lld of %d; %lld MMAs in %lld cycles = %.1f cycles/MMA (%.0f MAC/clk)\n",
-              N, ktot, reps, bad, 128 * N, nmma, cyc, (double)cyc / nmma, 128.0 * N * 32 * nmma / cyc);
+  std::printf("a%c b%c N=%3d ktot=%d reps=%d: mismatches %lld of %d; %lld MMAs in %lld cycles = %.1f cycles/MMA (%.0f MAC/clk)\n",
+              asg ? 's' : 'u', bsg ? 's' : 'u', N, ktot, reps, bad, 128 * N, nmma, cyc, (double)cyc / nmma, 128.0 * N * 32 * nmma / cyc);
   cudaFree(da);
   cudaFree(db);
   cudaFree(dout);
@@ -160,6 +162,9 @@ int run(int ktot, int reps) {
 int main() {
   int fails = 0;
   fails += run<64>(256, 1);
+  fails += run<64>(256, 1, 0, 1);
+  fails += run<64>(256, 1, 1, 0);
+  fails += run<64>(256, 1, 0, 0);
   fails += run<128>(256, 1);
   fails += run<64>(256, 200);
   fails += run<128>(256, 200);
