@@ -43,9 +43,12 @@ namespace {
 constexpr int kI8Rows = 128;      // Omega rows per CTA (MMA M)
 constexpr int kI8Cols = 64;       // A columns per CTA (MMA N)
 constexpr int kI8K = 32;          // rows of A per step (MMA K for kind::i8)
-constexpr int kI8Stages = 3;      // digit-plane ring
+#ifndef CQR_I8_STAGES
+#define CQR_I8_STAGES 4
+#endif
+constexpr int kI8Stages = CQR_I8_STAGES;  // digit-plane ring
 #ifndef CQR_I8_ASTAGES
-#define CQR_I8_ASTAGES 4
+#define CQR_I8_ASTAGES 2
 #endif
 constexpr int kI8AStages = CQR_I8_ASTAGES;  // FP64 A ring
 #ifndef CQR_I8_GEN
@@ -53,7 +56,7 @@ constexpr int kI8AStages = CQR_I8_ASTAGES;  // FP64 A ring
 #endif
 constexpr int kI8Gen = CQR_I8_GEN;  // generator warps
 #ifndef CQR_I8_SLICE
-#define CQR_I8_SLICE 8
+#define CQR_I8_SLICE 4
 #endif
 constexpr int kI8Slice = CQR_I8_SLICE;  // slicer warps (the first four also run the epilogue)
 constexpr int kI8Warps = 2 + kI8Slice + kI8Gen;
@@ -157,6 +160,10 @@ __device__ __forceinline__ void split64(long long v, uint32_t& lo, uint32_t& hi)
   hi = (uint32_t)(w >> 32) ^ 0x00008080u;
 }
 
+// Generator teams: with C CTAs sharing an Omega tile each CTA draws 1/C of it per step, too little work to
+// hide one thread's Box-Muller latency; T teams then take every T-th step, so T steps are drawn at once.
+__host__ __device__ constexpr int gen_teams(int ncta) { return ncta >= 4 ? 4 : ncta; }
+
 __global__ void __launch_bounds__(kI8Warps * 32, 1)
     sketch_i8_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global,
                      long long row0, int l, uint64_t seed, long long rows_per_chunk, const int* __restrict__ colexp,
@@ -190,8 +197,8 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
   if (tid < kI8Cols) sexp[tid] = max(colexp[(long long)ky * np_total + col0 + tid], -1074);
   if (tid == 0) {
     for (int s = 0; s < kI8Stages; ++s) {
-      // the local generators and slicers; the partners' Omega rows arrive as bulk-copy bytes (expect_tx)
-      mbar_init(&full[s], kI8Gen * 32 + kI8Slice * 32);
+      // one generator team and the slicers; the partners' Omega rows arrive as bulk-copy bytes (expect_tx)
+      mbar_init(&full[s], kI8Gen * 32 / gen_teams(ncta) + kI8Slice * 32);
       mbar_init(&empty[s], ncta);                              // every CTA's MMAs have read the stage
     }
     for (int s = 0; s < kI8AStages; ++s) {
@@ -286,36 +293,39 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
   } else {
     // ---- Omega generators: unit u = (Omega row i, k-octet o) = 4 Box-Muller pairs; this CTA draws the
     // units [crank UNITS / C, (crank + 1) UNITS / C) of each step for the whole cluster
-    const int gt = tid - 32 * (2 + kI8Slice);
+    const int gt0 = tid - 32 * (2 + kI8Slice);
+    const int teams = gen_teams(ncta), tsize = kI8Gen * 32 / teams;
+    const int team = gt0 / tsize, gt = gt0 - team * tsize;  // this thread's team and rank in it
     constexpr int UNITS = kI8Rows * (kI8K / 8);
     const int u_lo = crank * UNITS / ncta, u_hi = (crank + 1) * UNITS / ncta;
-    constexpr int UPT = (UNITS + kI8Gen * 32 - 1) / (kI8Gen * 32);  // units per thread per step (at most)
+    constexpr int UPT = (UNITS + kI8Gen * 32 - 1) / (kI8Gen * 32) * 4;  // units per thread per step (at most)
+    const int upt = (u_hi - u_lo + tsize - 1) / tsize;
     uint64_t z[UPT];
     bool live[UPT];
 #pragma unroll
     for (int uu = 0; uu < UPT; ++uu) {
-      const int u = min(u_lo + gt + kI8Gen * 32 * uu, UNITS - 1);
+      const int u = min(u_lo + gt + tsize * uu, UNITS - 1);
       const int i = u >> 2, o = u & 3;
-      // first counter word of the unit's first pair: c = (s0 + i) m_global + row0 + k (even), pair c/2
-      const unsigned long long c0 =
-          (unsigned long long)(s0 + i) * (unsigned long long)m_global + row0 + k_begin + 8 * o;
+      // first counter word of the unit's first pair at the team's first step: c = (s0 + i) m_global + row0 + k
+      const unsigned long long c0 = (unsigned long long)(s0 + i) * (unsigned long long)m_global + row0 + k_begin +
+                                    8 * o + (unsigned long long)kI8K * team;
       z[uu] = seed + (2 * (c0 >> 1) + 1) * kGolden;
       live[uu] = s0 + i < l;
     }
     const uint32_t slice = (uint32_t)(kDig * kOmPlane / ncta);  // this CTA's rows of all planes: one chunk
-    for (int stp = 0; stp < nsteps; ++stp) {
+    for (int stp = team; stp < nsteps; stp += teams) {
       const int s = stp % kI8Stages;
       mbar_wait(&empty[s], ((stp / kI8Stages) & 1) ^ 1);  // every CTA's MMAs are done with stage s
       unsigned char* planes = sOm + s * kDig * kOmPlane;
 #pragma unroll 1
-      for (int uu = 0; uu < UPT; ++uu) {
-        const int u = u_lo + gt + kI8Gen * 32 * uu;
+      for (int uu = 0; uu < upt; ++uu) {
+        const int u = u_lo + gt + tsize * uu;
         if (u >= u_hi) break;
         const int i = u >> 2, o = u & 3;
         uint64_t zz[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) zz[q] = z[uu] + (uint64_t)(2 * q) * kGolden;
-        z[uu] += (uint64_t)kI8K * kGolden;
+        z[uu] += (uint64_t)(kI8K * teams) * kGolden;
         double ge[4], go[4];
 #ifdef CQR_I8_NOGEN  // probe: the MMA side's bound (constant draws)
 #pragma unroll
@@ -333,9 +343,9 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
       }
       fence_async_shared();  // the digit stores -> the tensor core's and the bulk copies' (async) view
       if (ncta > 1) {
-        // all generators' stores are done; lanes 0 .. C-2 of the first generator warp ship this CTA's rows
-        // (one contiguous chunk of whole row groups, all planes) to one partner each
-        asm volatile("bar.sync 1, %0;" ::"n"(kI8Gen * 32) : "memory");
+        // the team's stores are done; its lanes 0 .. C-2 ship this CTA's rows (one contiguous chunk of whole
+        // row groups, all planes) to one partner each
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(tsize) : "memory");
         if (gt < ncta - 1) {
           const int r = gt < crank ? gt : gt + 1;
           const uint32_t dst = mapa_rank(smem_u32(planes), (uint32_t)r);
