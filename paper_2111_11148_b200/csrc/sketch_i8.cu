@@ -55,6 +55,9 @@ constexpr int kI8AStages = CQR_I8_ASTAGES;  // FP64 A ring
 #define CQR_I8_GEN 16
 #endif
 constexpr int kI8Gen = CQR_I8_GEN;  // generator warps
+#ifndef CQR_I8_SLEEP_NS
+#define CQR_I8_SLEEP_NS 100
+#endif
 #ifndef CQR_I8_SLICE
 #define CQR_I8_SLICE 4
 #endif
@@ -120,6 +123,15 @@ __device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// a wait that backs off: producers and the epilogue park here for long stretches, and a tight try_wait loop
+// would burn the issue slots the generator warps need
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#ifndef CQR_I8_NOSLEEP
+  while (!mbar_try_wait(bar, parity)) __nanosleep(CQR_I8_SLEEP_NS);
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -252,7 +264,7 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
     if (lane == 0) {
       for (int stp = 0; stp < nsteps; ++stp) {
         const int s = stp % kI8AStages;
-        mbar_wait(&aempty[s], ((stp / kI8AStages) & 1) ^ 1);
+        mbar_wait_sleep(&aempty[s], ((stp / kI8AStages) & 1) ^ 1);
         mbar_expect_tx(&afull[s], kATile * 8);
         tma_load_2d(sAf + s * kATile, &tma_a, col0, (int)(k_begin + (long long)stp * kI8K), &afull[s]);
       }
@@ -263,8 +275,8 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
     constexpr int SUPT = 256 / (kI8Slice * 32);  // units per thread
     for (int stp = 0; stp < nsteps; ++stp) {
       const int s = stp % kI8Stages, sa = stp % kI8AStages;
-      mbar_wait(&afull[sa], (stp / kI8AStages) & 1);
-      mbar_wait(&empty[s], ((stp / kI8Stages) & 1) ^ 1);
+      mbar_wait_sleep(&afull[sa], (stp / kI8AStages) & 1);
+      mbar_wait_sleep(&empty[s], ((stp / kI8Stages) & 1) ^ 1);
       const long long kb = k_begin + (long long)stp * kI8K;
       const double* At = sAf + sa * kATile;
       unsigned char* planes = sAp + s * kDig * kAPlane;
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
     const uint32_t slice = (uint32_t)(kDig * kOmPlane / ncta);  // this CTA's rows of all planes: one chunk
     for (int stp = team; stp < nsteps; stp += teams) {
       const int s = stp % kI8Stages;
-      mbar_wait(&empty[s], ((stp / kI8Stages) & 1) ^ 1);  // every CTA's MMAs are done with stage s
+      mbar_wait_sleep(&empty[s], ((stp / kI8Stages) & 1) ^ 1);  // every CTA's MMAs are done with stage s
       unsigned char* planes = sOm + s * kDig * kOmPlane;
 #pragma unroll 1
       for (int uu = 0; uu < upt; ++uu) {
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
     if (nsteps == 0) {  // an empty chunk: no MMA initialised the accumulators
       for (int j = 0; j < kI8Cols; ++j) out[j] = 0.0;
     } else {
-    mbar_wait(&done, 0);
+    mbar_wait_sleep(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
     for (int c0 = 0; c0 < kI8Cols; c0 += 8) {
