@@ -54,7 +54,6 @@ constexpr int kI8AStages = CQR_I8_ASTAGES;  // FP64 A ring
 #ifndef CQR_I8_GEN
 #define CQR_I8_GEN 16
 #endif
-constexpr int kI8Gen = CQR_I8_GEN;  // generator warps
 #ifndef CQR_I8_SLEEP_NS
 #define CQR_I8_SLEEP_NS 100
 #endif
@@ -62,7 +61,6 @@ constexpr int kI8Gen = CQR_I8_GEN;  // generator warps
 #define CQR_I8_SLICE 4
 #endif
 constexpr int kI8Slice = CQR_I8_SLICE;  // slicer warps (the first four also run the epilogue)
-constexpr int kI8Warps = 2 + kI8Slice + kI8Gen;
 constexpr long long kI8MaxChunk = 16384;  // rows per k-chunk: 7 * 128^2 * 16384 < 2^31
 constexpr int kDig = 7;                 // byte digits per operand
 constexpr int kOmPlane = kI8Rows * kI8K;  // bytes per Omega digit plane (4 KB)
@@ -176,7 +174,10 @@ __device__ __forceinline__ void split64(long long v, uint32_t& lo, uint32_t& hi)
 // hide one thread's Box-Muller latency; T teams then take every T-th step, so T steps are drawn at once.
 __host__ __device__ constexpr int gen_teams(int ncta) { return ncta >= 4 ? 4 : ncta; }
 
-__global__ void __launch_bounds__(kI8Warps * 32, 1)
+// GEN generator warps (16; 12 for clusters of 8 CTAs, where each CTA draws 1/8 of the tile: measured
+// c4 17.0 vs 18.6 ms, every other config within noise or slower)
+template <int GEN>
+__global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
     sketch_i8_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global,
                      long long row0, int l, uint64_t seed, long long rows_per_chunk, const int* __restrict__ colexp,
                      double* __restrict__ partial, int lp, int np_total, int y0, const DevStatus* st) {
@@ -203,14 +204,14 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
   {
     const double* src = reinterpret_cast<const double*>(&c_bm_i8);
     double* dst = reinterpret_cast<double*>(&T);
-    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += kI8Warps * 32) dst[e] = src[e];
+    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += (2 + kI8Slice + GEN) * 32) dst[e] = src[e];
   }
   // an all-zero column keeps the initial value: any bound >= its entries works, -1074 keeps the scalings finite
   if (tid < kI8Cols) sexp[tid] = max(colexp[(long long)ky * np_total + col0 + tid], -1074);
   if (tid == 0) {
     for (int s = 0; s < kI8Stages; ++s) {
       // one generator team and the slicers; the partners' Omega rows arrive as bulk-copy bytes (expect_tx)
-      mbar_init(&full[s], kI8Gen * 32 / gen_teams(ncta) + kI8Slice * 32);
+      mbar_init(&full[s], GEN * 32 / gen_teams(ncta) + kI8Slice * 32);
       mbar_init(&empty[s], ncta);                              // every CTA's MMAs have read the stage
     }
     for (int s = 0; s < kI8AStages; ++s) {
@@ -306,11 +307,11 @@ __global__ void __launch_bounds__(kI8Warps * 32, 1)
     // ---- Omega generators: unit u = (Omega row i, k-octet o) = 4 Box-Muller pairs; this CTA draws the
     // units [crank UNITS / C, (crank + 1) UNITS / C) of each step for the whole cluster
     const int gt0 = tid - 32 * (2 + kI8Slice);
-    const int teams = gen_teams(ncta), tsize = kI8Gen * 32 / teams;
+    const int teams = gen_teams(ncta), tsize = GEN * 32 / teams;
     const int team = gt0 / tsize, gt = gt0 - team * tsize;  // this thread's team and rank in it
     constexpr int UNITS = kI8Rows * (kI8K / 8);
     const int u_lo = crank * UNITS / ncta, u_hi = (crank + 1) * UNITS / ncta;
-    constexpr int UPT = (UNITS + kI8Gen * 32 - 1) / (kI8Gen * 32) * 4;  // units per thread per step (at most)
+    constexpr int UPT = (UNITS + GEN * 32 - 1) / (GEN * 32) * 4;  // units per thread per step (at most)
     const int upt = (u_hi - u_lo + tsize - 1) / tsize;
     uint64_t z[UPT];
     bool live[UPT];
@@ -534,11 +535,14 @@ cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda
   if (e != cudaSuccess) return e;
   sketch_colexp_kernel<<<dim3((unsigned)(y1 - y0), (unsigned)(p.np / 64), kExpSlices), 256, 0, s>>>(
       a, lda, p.m_local, p.n, p.rows_per_chunk, p.np, y0, colexp, const_cast<DevStatus*>(st));
-  e = cudaFuncSetAttribute(sketch_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
+  const int ncta = p.np / kI8Cols;
+  auto kern = ncta >= 8 ? sketch_i8_kernel<12> : sketch_i8_kernel<CQR_I8_GEN>;
+  const int warps = 2 + kI8Slice + (ncta >= 8 ? 12 : CQR_I8_GEN);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / kI8Cols));
-  cfg.blockDim = dim3(kI8Warps * 32, 1, 1);
+  cfg.blockDim = dim3(warps * 32, 1, 1);
   cfg.dynamicSmemBytes = kI8Smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -548,7 +552,7 @@ cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda
   attr[0].val.clusterDim.z = (unsigned)(p.np / kI8Cols);
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, sketch_i8_kernel, tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
+  return cudaLaunchKernelEx(&cfg, kern, tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
                             (const int*)colexp, partial, p.lp, p.np, y0, st);
 }
 
