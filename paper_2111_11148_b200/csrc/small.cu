@@ -1373,6 +1373,130 @@ __global__ void qr_out_kernel(const double* __restrict__ W, int l, int n, double
   r[(long long)i * n + c] = c >= i ? sg * W[(long long)c * l + i] : 0.0;
 }
 
+// Householder R of a sketch that fits in shared memory, one barrier per column: warp w owns the columns
+// c = w (mod NW). The owner of column j has applied reflectors 0 .. j-1 to it by itself, so it forms
+// reflector j (tail norm by a lane-strided sum and shuffles, beta / tau / v as qr_kernel) right after its
+// own update of column j in step j-1 -- before its other columns -- and one barrier publishes v_j; every
+// warp then applies it to its own columns (dot product over the rows, rank-1 update). Same reflector
+// formulas as qr_kernel and the oracle; the reductions are trees (tolerance parity, R <= 1e-13).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) qr_warp_kernel(const double* __restrict__ a1, int l, int n,
+                                                          double* __restrict__ r, DevStatus* st) {
+  extern __shared__ __align__(16) double W[];  // column-major, leading dimension ld = l | 1 (odd: no bank conflicts)
+  __shared__ double s_tau[2];
+  if (failed(st)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ld = l | 1;
+  for (long long e = tid; e < (long long)l * n; e += NW * 32) {
+    const int i = (int)(e / n), c = (int)(e % n);
+    W[(long long)c * ld + i] = __ldg(a1 + e);
+  }
+  __syncthreads();
+  const double tol = 2.2250738585072014e-308 * 2.2250738585072014e-308;  // (smallest normal)^2
+  // reflector j by the owner warp (column j up to date): v below the diagonal, beta on it, tau published
+  auto reflect = [&](int j) {
+    double* col = W + (long long)j * ld;
+    double part = 0.0;
+    for (int i = j + 1 + lane; i < l; i += 32) part = fma(col[i], col[i], part);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const double c0 = col[j];
+    double tau, beta, denom;
+    bool zero;
+    if (part <= tol) {
+      zero = true;
+      tau = 0.0;
+      beta = c0;
+      denom = 1.0;
+    } else {
+      zero = false;
+      beta = sqrt(c0 * c0 + part);
+      if (c0 >= 0.0) beta = -beta;
+      denom = c0 - beta;
+      tau = (beta - c0) / beta;
+    }
+    const double rden = 1.0 / denom;  // v = x / (c0 - beta) as x * RN(1 / (c0 - beta)): within an ulp
+    for (int i = j + 1 + lane; i < l; i += 32) col[i] = zero ? 0.0 : col[i] * rden;
+    __syncwarp();  // every lane has read c0
+    if (lane == 0) {
+      col[j] = beta;
+      s_tau[j & 1] = tau;
+    }
+    __syncwarp();
+  };
+  // H_j applied to column c (c > j): t = tau (W(j, c) + v^T W(j+1.., c)), W(.., c) -= t v
+  auto apply = [&](int j, int c, double tau) {
+    const double* v = W + (long long)j * ld;
+    double* cc = W + (long long)c * ld;
+    double sacc = 0.0;
+    for (int i = j + 1 + lane; i < l; i += 32) sacc = fma(v[i], cc[i], sacc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    const double t = tau * (cc[j] + sacc);
+    __syncwarp();
+    if (lane == 0) cc[j] -= t;
+    for (int i = j + 1 + lane; i < l; i += 32) cc[i] = fma(-t, v[i], cc[i]);
+    __syncwarp();
+  };
+  // the same for columns c, c + S, ..., c + (cnt - 1) S at once (independent chains: ILP), cnt <= 4
+  auto apply4 = [&](int j, int c, int S, int cnt, double tau) {
+    const double* v = W + (long long)j * ld;
+    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = j + 1 + lane; i < l; i += 32) {
+      const double vi = v[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < cnt) sacc[k] = fma(vi, W[(long long)(c + S * k) * ld + i], sacc[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sacc[k] += __shfl_xor_sync(0xffffffffu, sacc[k], o);
+    double t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = k < cnt ? tau * (W[(long long)(c + S * k) * ld + j] + sacc[k]) : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < cnt && lane == k) W[(long long)(c + S * k) * ld + j] -= t[k];
+    for (int i = j + 1 + lane; i < l; i += 32) {
+      const double vi = v[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < cnt) {
+          double* p = W + (long long)(c + S * k) * ld + i;
+          *p = fma(-t[k], vi, *p);
+        }
+    }
+    __syncwarp();
+  };
+  if (warp == 0) reflect(0);
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double tau = s_tau[j & 1];
+    // step j: warp (j + 1) % NW brings column j + 1 up to date and forms reflector j + 1; the other
+    // NW - 1 warps share the columns j + 2 .. n - 1 (W lives in shared memory: any warp may take any column)
+    const int owner = (j + 1) % NW;
+    if (warp == owner) {
+      if (j + 1 < n) {
+        if (tau != 0.0) apply(j, j + 1, tau);
+        reflect(j + 1);
+      }
+    } else if (tau != 0.0) {
+      const int rank = (warp - owner + NW) % NW - 1;  // 0 .. NW - 2
+      for (int c = j + 2 + rank; c < n; c += 4 * (NW - 1))
+        apply4(j, c, NW - 1, min(4, (n - c + NW - 2) / (NW - 1)), tau);
+    }
+    __syncthreads();
+  }
+  // R: the upper triangle, rows with a negative diagonal negated (normalize_r_sign, kernels.hpp:165-168)
+  for (int e = tid; e < n * n; e += NW * 32) {
+    const int i = e / n, c = e % n;
+    const double sg = W[(long long)i * ld + i] < 0.0 ? -1.0 : 1.0;
+    r[e] = c >= i ? sg * W[(long long)c * ld + i] : 0.0;
+  }
+}
+
 cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work, DevStatus* st, cudaStream_t s) {
   if (n > 512) return cudaErrorInvalidValue;
   const size_t bytes = (size_t)l * n * sizeof(double);
@@ -1398,6 +1522,18 @@ cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work,
         cudaFuncSetAttribute(qr_blocked_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
     if (e != cudaSuccess) return e;
     qr_blocked_kernel<false><<<1, kQrT, bsmem, s>>>(a1, l, n, r, work, st);
+    return cudaGetLastError();
+  }
+  static const bool legacy_qr = std::getenv("CQR_QR_LEGACY") != nullptr;  // A/B runs: the one-barrier-per-step kernel off
+  const size_t wbytes = (size_t)(l | 1) * n * sizeof(double);
+  if (!legacy_qr && wbytes <= kSmemCap) {
+#ifndef CQR_QR_WARPS
+#define CQR_QR_WARPS 16
+#endif
+    cudaError_t e =
+        cudaFuncSetAttribute(qr_warp_kernel<CQR_QR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+    if (e != cudaSuccess) return e;
+    qr_warp_kernel<CQR_QR_WARPS><<<1, CQR_QR_WARPS * 32, wbytes, s>>>(a1, l, n, r, st);
     return cudaGetLastError();
   }
   return launch_small(qr_kernel, bytes, s, a1, l, n, r, work, use_smem, st);
