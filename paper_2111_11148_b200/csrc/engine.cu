@@ -240,41 +240,6 @@ cqr_options default_opts() {
   return o;
 }
 
-// kernels.hpp:272-310 one-sided Jacobi singular values (cond_x diagnostics of
-// the n x n R-hat; engine.cpp:94-100).
-bool svd_values(std::vector<double> w, int rows, int c, std::vector<double>& sv) {
-  // w column-major rows x c
-  const double tol = 10.0 * kU * std::sqrt(static_cast<double>(rows));
-  auto dot = [&](int p, int q) {
-    double s = 0.0;
-    for (int i = 0; i < rows; ++i) s = std::fma(w[(size_t)p * rows + i], w[(size_t)q * rows + i], s);
-    return s;
-  };
-  bool conv = c <= 1;
-  for (int sweep = 0; sweep < 100 && !conv; ++sweep) {
-    conv = true;
-    for (int p = 0; p < c - 1; ++p)
-      for (int q = p + 1; q < c; ++q) {
-        const double al = dot(p, p), be = dot(q, q), ga = dot(p, q);
-        if (std::abs(ga) <= tol * std::sqrt(al * be)) continue;
-        conv = false;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = cs * t;
-        for (int i = 0; i < rows; ++i) {
-          const double a = w[(size_t)p * rows + i], b = w[(size_t)q * rows + i];
-          w[(size_t)p * rows + i] = cs * a - sn * b;
-          w[(size_t)q * rows + i] = sn * a + cs * b;
-        }
-      }
-  }
-  if (!conv) return false;
-  sv.resize(c);
-  for (int j = 0; j < c; ++j) sv[j] = std::sqrt(dot(j, j));
-  std::sort(sv.begin(), sv.end(), std::greater<double>());
-  return true;
-}
-
 // ---- stage timing (StageClock, engine.hpp:14-41, with CUDA events) -----------------
 cudaEvent_t next_event(cqr_ctx* c) {
   if (c->ev_used == c->ev_pool.size()) {
@@ -946,18 +911,13 @@ Outcome run_precond(Job& j) {
     Report pass;
     cholesky_pass(j, j.q, j.ldq, pass, rh, 0, 0.0, nullptr, true);
     double cond = 0.0;
-    if (diag) {  // cond(X) = cond(R^) (engine.cpp:94-100), NaN/inf when the pass fails
+    if (diag) {  // cond(X) = cond(R^) (engine.cpp:94-100) by a device Jacobi sweep; inf when the pass fails
       DevStatus s = read_status(c);
       if (s.code == 0) {
-        std::vector<double> hr((size_t)n * n), w((size_t)n * n);
-        copy_sync(c, hr.data(), rh, sizeof(double) * n * n, cudaMemcpyDeviceToHost, "rh D2H");
-        for (int i = 0; i < n; ++i)
-          for (int k = 0; k < n; ++k) w[(size_t)k * n + i] = hr[(size_t)i * n + k];
-        std::vector<double> sv;
-        if (svd_values(w, n, n, sv))
-          cond = sv.back() > 0.0 ? sv.front() / sv.back() : std::numeric_limits<double>::infinity();
-        else
-          cond = std::numeric_limits<double>::quiet_NaN();
+        double* cw = dbuf<double>(c, B_DIAG, (size_t)n * n + 2);
+        LAUNCH(c, cqr::launch_jacobi_cond(rh, n, cw, cw + (size_t)n * n, c->stream));
+        copy_sync(c, c->scal_h, cw + (size_t)n * n, sizeof(double), cudaMemcpyDeviceToHost, "cond D2H");
+        cond = c->scal_h[0];
       } else {
         cond = std::numeric_limits<double>::infinity();
       }

@@ -119,6 +119,9 @@ cudaError_t launch_triangular_product(const double* left, const double* right, i
 // is then applied to Q's columns by the final trisolve.
 cudaError_t launch_normalize_sign(double* r, int n, double* sgn, const DevStatus* st, cudaStream_t s);
 
+// diag.cu: cond(R) by a one-sided Jacobi sweep on the device (out[0]; work holds n x n doubles)
+cudaError_t launch_jacobi_cond(const double* r, int n, double* work, double* out, cudaStream_t s);
+
 // ---- householder.cu: tall Householder QR (HouseholderQr method, matgen's random_orthogonal) ----
 int hh_blocks(long long m_local, int num_sms);
 // red[0..w) = block-ordered sums of X(i,c) Y(i,c+t) over rows with global index > c, red[w..2w) = Y(c, c+t)

@@ -85,3 +85,18 @@ def test_device_diagnostics_match_oracle():
         rg, ro = G.residual_error_dev(ad, qd, f.r), o.residual_error(a, f.q, f.r)
         assert abs(og - oo) <= 1e-12 * oo + 1e-300, (og, oo)
         assert abs(rg - ro) <= 1e-12 * ro + 1e-300, (rg, ro)
+
+
+@pytest.mark.parametrize("m,n,l,kappa,seed", [(20_000, 128, 256, 1e10, 5), (8_000, 256, 300, 1e10, 6),
+                                                (20_000, 128, 256, 10.0, 7), (6_000, 200, 400, 1e3, 8)])
+def test_device_cond_x_matches_oracle(m, n, l, kappa, seed):
+    """engine.cpp:94-100: cond(X) of the preconditioned X on the device (a Jacobi sweep over R^, no host math)
+    against the oracle's qr_r_factor(X) + one-sided Jacobi. X = A R~^{-1} with R~ the Householder R of the
+    sampled rows (a tolerance-class kernel: its reduction order differs from the oracle's), so cond(X) carries
+    an O(kappa(A) u) relative difference (measured 4e-8 at kappa = 1e10); at small kappa the bound is tight."""
+    a = o.synthesize(m, n, kappa, seed)
+    f = G.rqr_cholesky_qr(a, G.SketchConfig(size=l, seed=seed + 1), G.Options(diagnostics=True))
+    ref = o.factor(_abi.RQR, a, _abi.sketch_cfg(size=l, seed=seed + 1), _abi.options(diagnostics=True))
+    c = [s.cond_x for s in f.report.stages if s.cond_x is not None][0]
+    cr = [s.cond_x for s in ref.stages if s.has_cond_x][0]
+    assert abs(c - cr) <= max(1e-12, 10 * kappa * U) * cr, (c, cr)
