@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "trisolve_common.cuh"
 
 namespace cqr {
 
@@ -402,6 +403,16 @@ __device__ long long g_lu_trace[1024];
   {                                          \
     if (threadIdx.x == 0) g_lu_trace[i] = clock64(); \
   }
+// the clock read issues only after v is available (in-order issue behind the compare that reads v)
+__device__ __forceinline__ long long clock_after(double v) {
+  long long t;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.eq.f64 p, %1, 0d7FF1234500000000;\n\tmov.u64 %0, %%clock64;\n\t@p add.s64 %0, %0, 1;\n\t}"
+      : "=l"(t)
+      : "d"(v)
+      : "memory");
+  return t;
+}
 #else
 #define LU_MARK(i) \
   {}
@@ -1224,6 +1235,112 @@ __global__ void __launch_bounds__(256) chol_trail_kernel(double* S, int n, int j
   if (row < n && col + 1 < n) S[(long long)row * n + col + 1] = c1v;
 }
 
+// Register-resident Cholesky for n <= 128 (c1: 128, c3: 64), two barriers per step and a short critical
+// path. S's upper triangle is cut into SEG-column segments of each row; one thread holds one segment in
+// registers (rows packed greedily into warps). Step i: thread t < n - i reads s(i,i) (left in shared
+// memory by row i's lanes), takes d = sqrt(s(i,i)) (kernels.hpp:84-86) and RN(1/d), and divides s(i,i+t)
+// (correctly rounded, as `/`; t = 0 writes d) into the shared row R(i,:); barrier; every row a > i applies
+// s(a,b) = fma(-r(i,a), r(i,b), s(a,b)) to its segment, and row i+1's lanes leave their updated entries in
+// shared memory; barrier. Each entry thus sees the fma chain over i = 0..a-1 in order and one division:
+// the same operations as cholesky_kernel (bitwise). (A dataflow variant -- one pivot warp, mbarriers per
+// row instead of block barriers -- measured slower: 111 vs 89 us at n = 128.)
+template <int SEG>
+__host__ __device__ inline int chol_reg_warps(int n, int warp = -1, int lane = 0, int* my_a = nullptr,
+                                              int* my_sb = nullptr) {
+  const int nseg = (n + SEG - 1) / SEG;
+  int w = 0, pos = 0;
+  for (int a = 0; a < n; ++a) {
+    const int s = nseg - a / SEG;
+    if (pos + s > 32) {
+      ++w;
+      pos = 0;
+    }
+    if (w == warp && lane >= pos && lane < pos + s) {
+      *my_a = a;
+      *my_sb = a / SEG + (lane - pos);
+    }
+    pos += s;
+  }
+  return w + 1;
+}
+constexpr int kChRegMaxN = 128;
+template <int SEG>
+__device__ __forceinline__ int chol_rb(int b) {  // shared slot of column b: segments 2 doubles apart (no bank conflicts)
+  return (b / SEG) * (SEG + 2) + b % SEG;
+}
+template <int SEG>
+__global__ void __launch_bounds__(608) chol_reg_kernel(const double* __restrict__ g, int n, double* __restrict__ r,
+                                                       int shift_mode, double shift_value, double theory_coef,
+                                                       double* shift_out, DevStatus* st) {
+  constexpr int RB = (kChRegMaxN / SEG) * (SEG + 2);
+  __shared__ __align__(16) double rowbuf[2][RB];  // R(i, :), double-buffered
+  __shared__ __align__(16) double und[RB];        // s(i, :) before the division
+  __shared__ double s_sh;
+  if (failed(st)) return;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  int my_a = -1, my_sb = 0;
+  chol_reg_warps<SEG>(n, warp, lane, &my_a, &my_sb);
+  const int c0 = SEG * my_sb, s0 = (SEG + 2) * my_sb;
+  double x[SEG];
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) x[k] = (my_a >= 0 && c0 + k < n) ? g[(long long)my_a * n + c0 + k] : 0.0;
+  for (int i = warp; i < n; i += nt >> 5)  // R's strict lower triangle
+    for (int c = lane; c < i; c += 32) r[(long long)i * n + c] = 0.0;
+  if (tid == 0) {
+    double sh = shift_value;
+    if (shift_mode == 2) {  // theory shift from trace(G) (cholqr.cpp:21-26), as cholesky_kernel
+      double tr = 0.0;
+      for (int j = 0; j < n; ++j) tr += g[(long long)j * n + j];
+      sh = theory_coef * tr;
+    }
+    s_sh = sh;
+    if (shift_mode != 0 && shift_out) *shift_out = sh;
+  }
+  __syncthreads();
+  if (shift_mode != 0 && my_a >= 0 && my_sb == my_a / SEG) {
+    const int o = my_a % SEG;
+#pragma unroll
+    for (int k = 0; k < SEG; ++k)
+      if (k == o) x[k] += s_sh;
+  }
+  if (my_a == 0) {
+#pragma unroll
+    for (int k = 0; k < SEG; k += 2) *reinterpret_cast<double2*>(und + s0 + k) = make_double2(x[k], x[k + 1]);
+  }
+  const int ra_slot = my_a >= 0 ? chol_rb<SEG>(my_a) : 0;
+  for (int i = 0; i < n; ++i) {
+    double* rb = rowbuf[i & 1];
+    __syncthreads();
+    const double sii = und[chol_rb<SEG>(i)];
+    if (!(sii > 0.0)) {  // kernels.hpp:84 (NaN included); every thread sees the same value
+      if (tid == 0) set_status(st, 1 /*CQR_CHOLESKY_BREAKDOWN*/, i);
+      return;
+    }
+    if (tid < n - i) {  // the pivot and the divisions of row i, one entry per thread
+      const double d = sqrt(sii), inv = __drcp_rn(d);
+      const bool safe = fabs(d) >= 0x1p-500 && fabs(d) <= 0x1p+500;
+      const int b = i + tid, slot = chol_rb<SEG>(b);
+      const double q = tid == 0 ? d : tri::fast_div(und[slot], d, inv, safe);
+      rb[slot] = q;
+      r[(long long)i * n + b] = q;
+    }
+    __syncthreads();
+    if (my_a > i) {
+      const double ra = rb[ra_slot];
+#pragma unroll
+      for (int k = 0; k < SEG; k += 2) {
+        const double2 rv = *reinterpret_cast<const double2*>(rb + s0 + k);
+        x[k] = fma(-ra, rv.x, x[k]);
+        x[k + 1] = fma(-ra, rv.y, x[k + 1]);
+      }
+      if (my_a == i + 1) {
+#pragma unroll
+        for (int k = 0; k < SEG; k += 2) *reinterpret_cast<double2*>(und + s0 + k) = make_double2(x[k], x[k + 1]);
+      }
+    }
+  }
+}
+
 __global__ void chol_out_kernel(const double* __restrict__ S, int n, double* __restrict__ r, const DevStatus* st) {
   if (failed(st)) return;
   const int i = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1236,6 +1353,12 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
     const char* v = std::getenv("CQR_CHOL_SPLIT_MIN");
     return v ? std::atoi(v) : 256;
   }();
+  static const bool reg_off = std::getenv("CQR_CHOL_LEGACY") != nullptr;  // A/B runs: the blocked kernels
+  if (!reg_off && n <= 128) {
+    chol_reg_kernel<16><<<1, 32 * chol_reg_warps<16>(n), 0, s>>>(g, n, r, shift_mode, shift_value, theory_coef,
+                                                                 shift_out, st);
+    return cudaGetLastError();
+  }
   if (n >= split_min && n > 64) {
     const size_t smem = (size_t)kChPanel * (n + 1) * sizeof(double);
     cudaError_t e =

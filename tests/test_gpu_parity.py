@@ -159,7 +159,8 @@ def test_gram_known_answers():
     assert G.gram(np.array([[1.0], [2.0], [2.0]]))[0, 0] == 9.0
 
 
-@pytest.mark.parametrize("n,seed", [(1, 1), (2, 2), (30, 3), (64, 4), (128, 5), (129, 6), (256, 7), (300, 8), (512, 9)])
+@pytest.mark.parametrize("n,seed", [(1, 1), (2, 2), (30, 3), (64, 4), (128, 5), (129, 6), (256, 7), (300, 8), (512, 9),
+                                    (7, 10), (16, 11), (17, 12), (33, 13), (95, 14), (100, 15), (112, 16), (127, 17)])
 def test_cholesky_bitwise(n, seed):
     a = o.gaussian_matrix(3 * n + 5, n, seed)
     g = o.gram(a)
@@ -174,6 +175,14 @@ def test_cholesky_known_and_breakdown():
     with pytest.raises(G.CholeskyBreakdown) as eg:
         G.cholesky_upper(g)
     assert eg.value.pivot_index == eo.value.index
+    # a deep breakdown index in the register-resident kernel (n <= 128) and in the blocked one
+    for n in (120, 200):
+        g = o.gram(o.synthesize(4000, n, 1e12, 43))
+        with pytest.raises(o.OracleError) as eo:
+            o.cholesky_upper(g)
+        with pytest.raises(G.CholeskyBreakdown) as eg:
+            G.cholesky_upper(g)
+        assert eg.value.pivot_index == eo.value.index > 10
 
 
 @pytest.mark.parametrize("m,n,seed", [(1, 2, 1), (30, 5, 2), (100, 8, 3), (2000, 9, 4), (3001, 24, 5),
