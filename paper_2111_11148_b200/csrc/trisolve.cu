@@ -385,7 +385,10 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   // (wider); 2: the left-looking TMA kernel at every width; 1: the register kernel (A/B runs)
   if ((a.variant == 0 || a.variant == 2) && trisolve_tma_eligible(a, np)) {
     // the right-looking kernel at np <= 64 (c3: 1.032 vs 1.058 ms per call; at np = 128 its 16-row
-    // warps leave the diagonal recurrence on half the lanes: 0.97 vs 0.77 ms, so the left-looking kernel)
+    // warps leave the diagonal recurrence on half the lanes: 0.97 vs 0.77 ms, so the left-looking kernel;
+    // a variant with warp pairs sharing 32-row groups, each warp owning every other 8-column block and the
+    // blocks handed over by named barriers, was bitwise equal but slower still: 1.22 ms -- the hand-over
+    // serialises the two warps' recurrences and leaves the FP64 pipe idle while a warp waits)
     if (a.variant == 0 && np <= 64) {
       const cudaError_t e = launch_trisolve_rr(a, np, s);
       if (e != cudaErrorNotSupported) return e;
