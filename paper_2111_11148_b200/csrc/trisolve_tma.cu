@@ -17,6 +17,13 @@
 //    64-byte-swizzled staging tile that the diagonal recurrence already uses.
 // A warp owns 32 rows; its TMA traffic is issued by lane 0 and tracked with
 // two mbarriers (loads) and bulk async-groups (stores).
+//  * TMW of the warps (n = 128: 8 of 12, n = 256: 4 of 16; as many as the 512 TMEM
+//    columns hold) keep the left-looking operand in tensor memory instead: each
+//    solved block's A fragments go to the thread's own TMEM lane (tcgen05.st) and
+//    come back with one tcgen05.ld per 16 columns -- no store/read-back round trip
+//    through L2 for those warps. Same values, same DMMA order: bit-identical.
+// Probe builds: -DCQR_TRI_NOLL (no left-looking DMMAs), -DCQR_TRI_NODIAG (no
+// diagonal recurrence) time the kernel's phases (results wrong; timing only).
 
 #include <cudaTypedefs.h>
 
@@ -44,7 +51,40 @@ constexpr int head_doubles() {
   return ((NP / 8) * kDiagStride + (BSMEM ? (NP / 8) * (NP / 8 - 1) * 32 : 0) + 127) / 128 * 128;
 }
 
-template <int NP, int WPC, bool BSMEM>
+// TMEM store of the left-looking operand: thread (gr, q) keeps, in its own TMEM lane, the DMMA A fragments
+// af[g] of every solved k4 step its later passes need (8 32-bit columns per k4: column 8 k4 + 2 g); warp w
+// uses lane quarter w % 4 at column slot w / 4.
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, double (&v)[16]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tm_st16(uint32_t taddr, const double (&v)[8]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    r[2 * i] = (uint32_t)__double2loint(v[i]);
+    r[2 * i + 1] = (uint32_t)__double2hiint(v[i]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+template <int NP, int WPC, bool BSMEM, int TMW = 0>
 __global__ void __launch_bounds__(WPC * 32, 1)
     trisolve_tma_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_ll,
                         const __grid_constant__ CUtensorMap tm_st, long long m, int n,
@@ -78,7 +118,23 @@ __global__ void __launch_bounds__(WPC * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_shared();
   }
+  __shared__ uint32_t tmem_base;
+  if constexpr (TMW > 0) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
   __syncthreads();
+  constexpr int kTmCols = (NT - W) * 16;  // TMEM columns per warp: the blocks later passes read
+  static_assert(TMW == 0 || ((TMW + 3) / 4) * kTmCols <= 512, "TMEM: too many warps for this width");
+  const bool tmw = warp < TMW;
+  uint32_t tm_warp = 0;
+  if constexpr (TMW > 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    tm_warp = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kTmCols);
+  }
 
   // left-looking chunk ch (columns 16ch .. 16ch+15) -> buffer b, four slabs
   auto issue_ll = [&](int ch, int b, int row0) {
@@ -138,7 +194,27 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           acc[g][t][1] = v.y;
         }
       // 2. left-looking: k in [0, c0) ascending, from this warp's stored rows
-      if (P > 0) {
+      if (P > 0 && TMW > 0 && tmw) {
+        const int nch = c0 / 16;
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#pragma unroll 1
+        for (int ch = 0; ch < nch; ++ch) {
+          double af16[16];
+          tm_ld32(tm_warp + 32u * ch, af16);
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const int k4 = 4 * ch + s;
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+              const int JJ = W * P + t;
+              const int bi = (JJ * (JJ - 1) + k4) * 32 + lane;
+              const double bv = BSMEM ? sB[bi] : __ldg(sB + bi);
+#pragma unroll
+              for (int g = 0; g < 4; ++g) dmma(acc[g][t][0], acc[g][t][1], af16[4 * s + g], bv);
+            }
+          }
+        }
+      } else if (P > 0) {
         const int nch = c0 / 16;
         fence_async_shared();
         __syncwarp();
@@ -170,8 +246,12 @@ __global__ void __launch_bounds__(WPC * 32, 1)
               const int JJ = W * P + t;
               const int bi = (JJ * (JJ - 1) + k4) * 32 + lane;
               const double bv = BSMEM ? sB[bi] : __ldg(sB + bi);
+#ifndef CQR_TRI_NOLL  // probe: without the left-looking DMMAs
 #pragma unroll
               for (int g = 0; g < 4; ++g) dmma(acc[g][t][0], acc[g][t][1], af[g], bv);
+#else
+              if (bv == 12345.0) acc[0][t][0] += af[0] + af[1] + af[2] + af[3];
+#endif
             }
           }
           fence_async_shared();
@@ -214,6 +294,12 @@ __global__ void __launch_bounds__(WPC * 32, 1)
             y[2 * u + 1] = v.y;
           }
           bool good = D[80] != 0.0;  // uniform: no zero in the strict upper block, safe divisors
+#ifdef CQR_TRI_NODIAG  // probe: without the diagonal recurrence
+          if (good) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] *= D[64 + j];
+          } else
+#endif
           if (good) {
             bool ok = true;
             const double* Dc = D + kColBase;
@@ -269,6 +355,10 @@ __global__ void __launch_bounds__(WPC * 32, 1)
           for (int kk4 = 0; kk4 < 2; ++kk4) {
             af[g][kk4] = tile[swz64(8 * g + gr, 2 * kk4 + (q >> 1)) + (q & 1)];
           }
+        if (TMW > 0 && tmw && J < NT - W) {
+          const double v8[8] = {af[0][0], af[1][0], af[2][0], af[3][0], af[0][1], af[1][1], af[2][1], af[3][1]};
+          tm_st16(tm_warp + 16u * J, v8);
+        }
         const double* bcol = sB + (2 * J) * 32 + lane;
 #pragma unroll
         for (int t = 1; t < W; ++t) {
@@ -293,6 +383,11 @@ __global__ void __launch_bounds__(WPC * 32, 1)
   }
   if (lane == 0) bulk_wait<0>();
   __syncwarp();
+  if constexpr (TMW > 0) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -307,7 +402,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int NP, int WPC, bool BSMEM>
+template <int NP, int WPC, bool BSMEM, int TMW = 0>
 cudaError_t launch_t(const TrisolveArgs& a, cudaStream_t s) {
   CUtensorMap tin, tll, tst;
   if (!make_tmap_2d(&tin, a.in, a.n, a.m, a.ldi, 8, kRW, CU_TENSOR_MAP_SWIZZLE_NONE) ||
@@ -315,7 +410,7 @@ cudaError_t launch_t(const TrisolveArgs& a, cudaStream_t s) {
       !make_tmap_2d(&tst, a.out, a.n, a.m, a.ldo, 8, kRW, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorNotSupported;
   const size_t smem = (size_t)(head_doubles<NP, BSMEM>() + WPC * kWarpDoubles) * 8 + WPC * 16 + 512;
-  auto k = trisolve_tma_kernel<NP, WPC, BSMEM>;
+  auto k = trisolve_tma_kernel<NP, WPC, BSMEM, TMW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + kRW - 1) / kRW;
@@ -372,6 +467,14 @@ bool trisolve_tma_eligible(const TrisolveArgs& a, int np) {
 #ifndef CQR_TRI512_WPC
 #define CQR_TRI512_WPC 12
 #endif
+// warps whose left-looking operand stays in TMEM (the rest read it back from L2): n = 128, 12 warps:
+// 0/8 TMEM warps 0.777/0.757 ms (all 8 warps TMEM, WPC 8: 0.815); n = 256: 0/4 of 16 warps 2.74/2.60 ms
+#ifndef CQR_TRI128_TMW
+#define CQR_TRI128_TMW 8
+#endif
+#ifndef CQR_TRI256_TMW
+#define CQR_TRI256_TMW 4
+#endif
 #ifndef CQR_TRI64_WPC
 #define CQR_TRI64_WPC 12
 #endif
@@ -379,8 +482,8 @@ cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s) {
   switch (np) {
     case 32: return launch_t<32, 16, true>(a, s);
     case 64: return launch_t<64, CQR_TRI64_WPC, true>(a, s);
-    case 128: return launch_t<128, CQR_TRI128_WPC, CQR_TRI128_BSMEM>(a, s);
-    case 256: return launch_t<256, CQR_TRI256_WPC, false>(a, s);
+    case 128: return launch_t<128, CQR_TRI128_WPC, CQR_TRI128_BSMEM, CQR_TRI128_TMW>(a, s);
+    case 256: return launch_t<256, CQR_TRI256_WPC, false, CQR_TRI256_TMW>(a, s);
     case 512: return launch_t<512, CQR_TRI512_WPC, false>(a, s);
   }
   return cudaErrorInvalidValue;
