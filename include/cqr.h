@@ -172,6 +172,11 @@ typedef struct {
 } cqr_host_comm;
 int cqr_attach_host_comm(cqr_ctx* ctx, int rank, int world, const cqr_host_comm* comm);
 int cqr_stream_handle(cqr_ctx* ctx, void** stream); /* cudaStream_t the context launches on */
+/* Order the context's next launches after all work queued so far on `stream` (a cudaStream_t of the
+ * context's device; NULL = the legacy default stream): an event recorded there and waited on by the
+ * context stream, no host synchronisation. Device-buffer callers whose inputs come from another stream
+ * use this instead of synchronising the producer; every call returns with its own work complete. */
+int cqr_order_after(cqr_ctx* ctx, void* stream);
 
 /* ---- whole factorizations (cholqr.hpp:82-109, parexec.hpp:89-90) ----------- */
 /* Host buffers. Q is m x n (ldq >= n); R is n x n (ldr >= n), untouched when

@@ -185,6 +185,7 @@ def _lib():
             "cqr_attach_comm": (i32, [vp, i32, i32, vp]),
             "cqr_attach_host_comm": (i32, [vp, i32, i32, P(_abi.HostComm)]),
             "cqr_stream_handle": (i32, [vp, P(vp)]),
+            "cqr_order_after": (i32, [vp, vp]),
             "cqr_launch_count": (i64, [vp]),
             "cqr_factor": (i32, [vp, i32, vp, i64, i64, i64, P(_abi.SketchCfg), P(_abi.Options), vp, i64, vp,
                                  i64, P(_abi.Report)]),
@@ -345,16 +346,23 @@ def _stages(rep):
     return out
 
 
-def _check_cuda_matrix(a, what="A"):
+def _check_cuda_matrix(a, what="A", ctx=None):
     """A CUDA tensor the library may read as a row-major float64 matrix with
     leading dimension stride(0); waits for the producer's pending work (the
     library runs on its own non-blocking stream, which is not ordered after
-    torch's streams)."""
+    torch's streams). With `ctx` the wait is stream-ordered (cqr_order_after on
+    torch's current stream) instead of a host synchronisation; ctx=False only
+    validates (the caller has ordered the producer already)."""
     import torch
 
     if a.dtype != torch.float64 or a.dim() != 2 or a.stride(1) != 1 or a.stride(0) < a.shape[1]:
         raise ValueError(f"{what}: expected a CUDA float64 row-major matrix (stride(1) == 1, stride(0) >= cols)")
-    torch.cuda.current_stream(a.device).synchronize()
+    if ctx is False:
+        return
+    if ctx is not None:
+        ctx._check(_lib().cqr_order_after(ctx.h, C.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)), -1)
+    else:
+        torch.cuda.current_stream(a.device).synchronize()
 
 
 def _factor(method, a, cfg: SketchConfig | None, opts_c, ctx=None, precond=None):
@@ -364,12 +372,13 @@ def _factor(method, a, cfg: SketchConfig | None, opts_c, ctx=None, precond=None)
     if _is_torch_cuda(a):
         import torch
 
-        _check_cuda_matrix(a)
+        _check_cuda_matrix(a, "A", False)
         if precond is not None:
             raise ValueError("a custom preconditioner needs host buffers")
         ctx = ctx or context(a.device.index)
         m, n = a.shape
         q = torch.empty((m, n), dtype=torch.float64, device=a.device)
+        _check_cuda_matrix(q, "Q", ctx)  # stream-ordered after torch's pending work on A (and Q's memory)
         r = np.zeros((n, n))
         st = _lib().cqr_factor_dev(ctx.h, method, C.c_void_p(a.data_ptr()), m, m, 0, n, a.stride(0),
                                    C.byref(cfg_c), C.byref(opts_c), C.c_void_p(q.data_ptr()), n, _ptr(r), n,

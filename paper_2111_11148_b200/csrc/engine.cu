@@ -67,6 +67,7 @@ struct cqr_ctx {
   int local_only = 0;  // temporarily treat an attached communicator as absent (replicated small work)
   cudaStream_t cstream = nullptr;  // copy stream of the host-buffer pipeline
   std::vector<cudaEvent_t> pipe_ev;
+  cudaEvent_t order_ev = nullptr;  // cqr_order_after
 };
 
 namespace {
@@ -1167,6 +1168,7 @@ int cqr_destroy(cqr_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->cstream) cudaStreamDestroy(c->cstream);
   for (auto e : c->pipe_ev) cudaEventDestroy(e);
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
   delete c;
   return CQR_OK;
 }
@@ -1222,6 +1224,15 @@ int cqr_stream_handle(cqr_ctx* c, void** stream) {
   if (!c || !stream) return CQR_INVALID_ARGUMENT;
   *stream = (void*)c->stream;
   return CQR_OK;
+}
+
+int cqr_order_after(cqr_ctx* c, void* stream) {
+  if (!c) return CQR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (!c->order_ev) ck(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(c->order_ev, (cudaStream_t)stream), "record");
+    ck(cudaStreamWaitEvent(c->stream, c->order_ev, 0), "wait");
+  });
 }
 
 int64_t cqr_launch_count(const cqr_ctx* c) { return c ? c->launches : 0; }

@@ -161,12 +161,13 @@ def factor_sharded(ctx, method, a_local, m_global: int, row0: int, cfg: cq.Sketc
     if opts is None:
         opts = _abi.options()
     cfg_c = (cfg or cq.SketchConfig())._c()
-    cq._check_cuda_matrix(a_local)  # dtype/layout, and the producer's pending writes have landed
+    cq._check_cuda_matrix(a_local, "A", False)
     m_local, n = a_local.shape
     q = q_out if q_out is not None else torch.empty((m_local, n), dtype=torch.float64, device=a_local.device)
     if q.shape != a_local.shape or q.device != a_local.device:
         raise ValueError("q_out must match the shard's shape and device")
-    cq._check_cuda_matrix(q, "q_out")
+    # the library stream waits for torch's pending work on A and Q (stream-ordered, no host sync)
+    cq._check_cuda_matrix(q, "q_out", ctx)
     r = np.zeros((n, n))
     rep = _abi.Report()
     st = cq._lib().cqr_factor_dev(ctx.h, method, C.c_void_p(a_local.data_ptr()), m_local, m_global, row0, n,

@@ -713,3 +713,27 @@ def test_concurrent_threads_get_their_own_contexts():
     assert not errs
     for s, f in zip(seq, out):
         assert np.array_equal(s.q, f.q) and np.array_equal(s.r, f.r)
+
+
+def test_stream_ordered_inputs():
+    """A written on a torch side stream behind a long-running kernel: the device-buffer calls order the
+    library stream after torch's current stream (cqr_order_after, no host sync) and see the final A."""
+    import torch
+
+    m, n = 50_000, 64
+    ah = o.synthesize(m, n, 1e8, 4)
+    src = torch.as_tensor(ah, device="cuda")
+    ref = G.cholesky_qr2(src.clone())
+    ctx = dist.make_context(0, 0, 1)
+    side = torch.cuda.Stream()
+    for trial in range(3):
+        a = torch.zeros_like(src)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(20_000_000)  # ~10 ms of device time ahead of the copy
+            a.copy_(src)
+            q, r, _ = dist.factor_sharded(ctx, _abi.CHOLQR2, a, m, 0)
+            f = G.cholesky_qr2(a)
+        assert np.array_equal(r, ref.r), trial
+        assert torch.equal(q, ref.q), trial
+        assert np.array_equal(f.r, ref.r) and torch.equal(f.q, ref.q), trial
