@@ -118,4 +118,14 @@ __device__ __forceinline__ void stage_rows(double* s, int lds, const double* g, 
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// The dynamic shared memory cap of a kernel, set once per (device, kernel) to the device's opt-in maximum
+// minus the kernel's static shared memory. The attribute is process-wide per function: setting it to each
+// launch's own size would let a concurrent host thread lower it under another thread's larger launch
+// (cudaErrorInvalidValue). The launch still passes its actual size, which is what occupancy depends on.
+cudaError_t allow_max_smem_impl(const void* kernel);
+template <typename K>
+inline cudaError_t allow_max_smem(K kernel) {
+  return allow_max_smem_impl(reinterpret_cast<const void*>(kernel));
+}
+
 }  // namespace cqr

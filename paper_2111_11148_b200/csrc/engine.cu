@@ -20,6 +20,8 @@
 #include <string>
 #include <unordered_set>
 #include <vector>
+#include <mutex>
+#include <set>
 
 #include "../../include/cqr.h"
 #include "common.cuh"
@@ -345,7 +347,6 @@ const int32_t* gram_tiles_dev(cqr_ctx* c, const cqr::GramPlan& p, int slot = 0) 
 struct SketchRun {
   cqr::SketchPlan p;
   double* part = nullptr;
-  int* colexp = nullptr;
 };
 
 SketchRun sketch_setup(cqr_ctx* c, const double* a, long long lda, long long m_local, long long m_global,
@@ -353,17 +354,15 @@ SketchRun sketch_setup(cqr_ctx* c, const double* a, long long lda, long long m_l
   SketchRun r;
   const bool i8 = cqr::sketch_i8_ok(a, lda, m_global, row0, n);
   r.p = cqr::sketch_plan(m_local, n, l, c->num_sms, cqr::sketch_ws_ok(a, lda, m_global, row0, n), splits);
-  if (i8) cqr::sketch_i8_plan(r.p, m_local, n, l, c->num_sms);
+  if (i8) cqr::sketch_i8_plan(r.p, m_local, n, l, c->num_sms, splits);
   r.part = dbuf<double>(c, B_SKPART, std::max<size_t>(r.p.partial_doubles, 1));
-  if (i8) r.colexp = dbuf<int>(c, B_SKEXP, std::max<size_t>(r.p.aux_ints, 1));
   return r;
 }
 
 cudaError_t sketch_launch(cqr_ctx* c, const SketchRun& r, const double* a, long long lda, long long m_global,
                           long long row0, uint64_t seed, int vec, int check, int y0 = 0, int y1 = -1) {
   if (r.p.i8) {
-    ++c->launches;  // the exponent pre-pass + the tensor-core kernel
-    return cqr::launch_sketch_i8(r.p, a, lda, m_global, row0, seed, r.part, r.colexp, c->status, c->stream, y0, y1);
+    return cqr::launch_sketch_i8(r.p, a, lda, m_global, row0, seed, r.part, c->status, c->stream, y0, y1);
   }
   return cqr::launch_sketch_gaussian(r.p, a, lda, m_global, row0, seed, r.part, vec, check, c->status, c->stream, y0,
                                      y1);
@@ -1113,6 +1112,27 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
 }
 
 }  // namespace
+
+namespace cqr {
+cudaError_t allow_max_smem_impl(const void* kernel) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({dev, kernel})) return cudaSuccess;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.insert({dev, kernel});
+  return e;
+}
+}  // namespace cqr
 
 // =============================== C ABI ===========================================
 extern "C" {

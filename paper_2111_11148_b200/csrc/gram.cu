@@ -374,7 +374,7 @@ cudaError_t launch_leaves_tma(const GramPlan& p, const double* x, long long ldx,
   const int slots = std::max(1, num_sms / p.parts) * p.parts;
   const int grid = (int)std::min<long long>(items, slots);
   auto run = [&](auto kfn, size_t smem) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = allow_max_smem(kfn);
     if (e != cudaSuccess) return e;
     kfn<<<(unsigned)grid, kGtThreads, smem, s>>>(tm, tma3 ? 1 : 0, p.m, p.parts, tiles, partial, leaf0, leaf1,
                                                 const_cast<DevStatus*>(st));
@@ -482,7 +482,7 @@ cudaError_t launch_leaves_t(const GramPlan& p, const double* x, long long ldx, c
   if (leaf1 <= leaf0) return cudaSuccess;
   const size_t smem = (size_t)2 * CH * (NP + 4) * sizeof(double);
   auto k = gram_leaf_kernel<NP, MAXT, CH>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(k);
   if (e != cudaSuccess) return e;
   k<<<(unsigned)((leaf1 - leaf0) * p.parts), kWpc * 32, smem, s>>>(x, ldx, p.m, p.n, p.parts, tiles, partial, vec16,
                                                                      check, leaf0, const_cast<DevStatus*>(st));
@@ -497,7 +497,7 @@ cudaError_t launch_leaves_p(const GramPlan& p, const double* x, long long ldx, c
   if (leaf1 <= leaf0) return cudaSuccess;
   const size_t smem = (size_t)2 * CH * (NP + 4) * sizeof(double);
   auto k = check ? gram_leaf_p_kernel<NP, WPC, MAXT, CH, true> : gram_leaf_p_kernel<NP, WPC, MAXT, CH, false>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(k);
   if (e != cudaSuccess) return e;
   const int grid = std::min(leaf1 - leaf0, num_sms);
   k<<<(unsigned)grid, WPC * 32, smem, s>>>(x, ldx, p.m, p.n, tiles, partial, vec16, leaf0, leaf1,

@@ -66,7 +66,6 @@ cudaError_t launch_mirror_upper(double* g, int n, const DevStatus* st, cudaStrea
 struct SketchPlan {
   int n = 0, np = 0, l = 0, lp = 0, s_tiles = 0, kchunks = 0, ws = 0;  // ws: warp-specialised kernel
   int i8 = 0;            // the integer tensor-core kernel (sketch_i8.cu)
-  size_t aux_ints = 0;   // i8: per-(k-chunk, column) exponent bounds
   int st = 64, npc = 128;  // Omega rows and A columns per CTA
   long long m_local = 0, rows_per_chunk = 0;
   size_t partial_doubles = 0;
@@ -83,9 +82,9 @@ cudaError_t launch_sketch_gaussian(const SketchPlan& p, const double* a, long lo
 // sketch_i8.cu: the sketch as an exact integer product on tcgen05 (kind::i8) -- A needs the TMA
 // alignment of the warp-specialised kernel; sketch_i8_plan turns a plan into the i8 kernel's
 bool sketch_i8_ok(const double* a, long long lda, long long m_global, long long row0, int n);
-void sketch_i8_plan(SketchPlan& p, long long m_local, int n, int l, int num_sms);
+void sketch_i8_plan(SketchPlan& p, long long m_local, int n, int l, int num_sms, int splits = 1);
 cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
-                             uint64_t seed, double* partial, int* colexp, const DevStatus* st, cudaStream_t s,
+                             uint64_t seed, double* partial, const DevStatus* st, cudaStream_t s,
                              int y0 = 0, int y1 = -1);
 // a1[i][c] = sum over k-chunks (ascending) of partial -> l x n (ld = n)
 cudaError_t launch_sketch_reduce(const SketchPlan& p, const double* partial, double* a1, const DevStatus* st,

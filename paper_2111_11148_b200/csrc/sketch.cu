@@ -441,7 +441,7 @@ cudaError_t launch_ws(const SketchPlan& p, const double* a, long long lda, long 
   if (!tma3 && !make_tmap_2d(&tm, a, p.n, p.m_local, lda, BW, kKS, SW)) return cudaErrorInvalidValue;
   auto k = sketch_ws_kernel<NPC, ST>;
   cudaError_t e =
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsShape<NPC, ST>::SMEM);
+      allow_max_smem(k);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NPC));
   k<<<grid, ws_threads<NPC>(), WsShape<NPC, ST>::SMEM, s>>>(tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
@@ -537,7 +537,7 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
   const bool aligned = (m_global % 2 == 0) && (row0 % 2 == 0) && (p.rows_per_chunk % 2 == 0);
   if (!aligned) {
     auto k = sketch_kernel<NP, false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = allow_max_smem(k);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NP));
     k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial,
@@ -545,7 +545,7 @@ cudaError_t launch_sketch_t(const SketchPlan& p, const double* a, long long lda,
     return cudaGetLastError();
   }
   auto k = sketch_kernel<NP, true>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(k);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / NP));
   k<<<grid, kThreads, smem, s>>>(a, lda, p.m_local, m_global, row0, p.n, p.l, seed, p.rows_per_chunk, partial, p.lp,

@@ -28,7 +28,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "boxmuller.cuh"
@@ -174,18 +176,59 @@ __device__ __forceinline__ void split64(long long v, uint32_t& lo, uint32_t& hi)
 // hide one thread's Box-Muller latency; T teams then take every T-th step, so T steps are drawn at once.
 __host__ __device__ constexpr int gen_teams(int ncta) { return ncta >= 4 ? 4 : ncta; }
 
+// Sub-chunks: a CTA's rows [k_begin, k_end) are accumulated in TMEM in sub-chunks of kSubFirst, 4x, 16x ...
+// steps (capped at 512 steps = kI8MaxChunk rows, the s32 exactness bound), each with its own column
+// exponent bounds. The scanner warps find sub-chunk t+1's bounds while sub-chunk t is on the tensor cores
+// (4x its rows in the same time: they read A at ~4x the MMA side's rate, L2-prefetched by TMA), so only the
+// first, short sub-chunk's scan is exposed -- the separate exponent pre-pass over all of A is gone. Between
+// sub-chunks the epilogue warps drain TMEM into the FP64 partial (+=), while the producers run ahead.
+#ifndef CQR_I8_SUBGROW
+#define CQR_I8_SUBGROW 2  // sub-chunk growth 2^CQR_I8_SUBGROW (x2: c1 1.90 ms, x4: 1.84)
+#endif
+#ifndef CQR_I8_SUBFIRST
+#define CQR_I8_SUBFIRST 16
+#endif
+constexpr int kSubFirst = CQR_I8_SUBFIRST;  // steps (32 rows each) of a CTA's first sub-chunk
+constexpr int kI8MaxSteps = (int)(kI8MaxChunk / kI8K);
+__host__ __device__ constexpr int sub_steps(int t) {
+  return t * CQR_I8_SUBGROW >= 5 ? kI8MaxSteps
+                                 : (kSubFirst << (CQR_I8_SUBGROW * t)) < kI8MaxSteps ? (kSubFirst << (CQR_I8_SUBGROW * t))
+                                                                                     : kI8MaxSteps;
+}
+#ifndef CQR_I8_SCAN
+#define CQR_I8_SCAN 4
+#endif
+constexpr int kI8Scan = CQR_I8_SCAN;  // scanner warps (2 or 4; 4: c1 1.84 vs 1.99 ms at x4 growth)
+constexpr int kExpSlots = 4;    // exponent-bound ring (sub-chunks in flight)
+#ifndef CQR_I8_AHEAD
+#define CQR_I8_AHEAD 6
+#endif
+constexpr int kScanAhead = CQR_I8_AHEAD;  // 32-row blocks prefetched into L2 ahead of the scan (0: none)
+
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // GEN generator warps (16; 12 for clusters of 8 CTAs, where each CTA draws 1/8 of the tile: measured
 // c4 17.0 vs 18.6 ms, every other config within noise or slower)
 template <int GEN>
-__global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
-    sketch_i8_kernel(const __grid_constant__ CUtensorMap tma_a, long long m_local, long long m_global,
-                     long long row0, int l, uint64_t seed, long long rows_per_chunk, const int* __restrict__ colexp,
-                     double* __restrict__ partial, int lp, int np_total, int y0, const DevStatus* st) {
+__global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
+    sketch_i8_kernel(const __grid_constant__ CUtensorMap tma_a, const double* __restrict__ a, long long lda,
+                     long long m_local, long long m_global, long long row0, int l, int n, uint64_t seed,
+                     long long rows_per_chunk, double* __restrict__ partial, int lp, int np_total, int y0,
+                     DevStatus* st) {
+  static_assert(kI8Slice == 4, "the four slicer warps are the epilogue (one TMEM lane quadrant each)");
+  constexpr int NTHR = (2 + kI8Slice + GEN + kI8Scan) * 32;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ BmTables T;
-  __shared__ __align__(8) uint64_t full[kI8Stages], empty[kI8Stages], afull[kI8AStages], aempty[kI8AStages], done;
+  __shared__ __align__(8) uint64_t full[kI8Stages], empty[kI8Stages], afull[kI8AStages], aempty[kI8AStages];
+  __shared__ __align__(8) uint64_t subdone, tfree, expfull[kExpSlots];
   __shared__ uint32_t tmem_base;
-  __shared__ int sexp[kI8Cols];
+  __shared__ int sexp[kExpSlots][kI8Cols];
+  __shared__ unsigned sexpw[kI8Scan][kI8Cols];
+  __shared__ int drained;
   if (failed(st)) return;
   unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sOm = sm;                                    // [stage][plane][4 KB]
@@ -204,10 +247,8 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
   {
     const double* src = reinterpret_cast<const double*>(&c_bm_i8);
     double* dst = reinterpret_cast<double*>(&T);
-    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += (2 + kI8Slice + GEN) * 32) dst[e] = src[e];
+    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += NTHR) dst[e] = src[e];
   }
-  // an all-zero column keeps the initial value: any bound >= its entries works, -1074 keeps the scalings finite
-  if (tid < kI8Cols) sexp[tid] = max(colexp[(long long)ky * np_total + col0 + tid], -1074);
   if (tid == 0) {
     for (int s = 0; s < kI8Stages; ++s) {
       // one generator team and the slicers; the partners' Omega rows arrive as bulk-copy bytes (expect_tx)
@@ -218,7 +259,10 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
       mbar_init(&afull[s], 1);
       mbar_init(&aempty[s], kI8Slice * 32);
     }
-    mbar_init(&done, 1);
+    mbar_init(&subdone, 1);
+    mbar_init(&tfree, kI8Slice * 32);
+    for (int s = 0; s < kExpSlots; ++s) mbar_init(&expfull[s], 32);
+    drained = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_shared();
   }
@@ -235,8 +279,11 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
   if (warp == 0) {
     // ---- MMA issuer: per step, D[level s+t] += Omega digit s x A digit t (s + t <= 7)
     if (lane == 0) {
+      int t = 0, t_end = sub_steps(0);  // current sub-chunk and its end step
       for (int stp = 0; stp < nsteps; ++stp) {
         const int s = stp % kI8Stages;
+        const bool first = stp == t_end - sub_steps(t);
+        if (first && t > 0) mbar_wait(&tfree, (t - 1) & 1);  // the epilogue has drained sub-chunk t-1
         mbar_wait(&full[s], (stp / kI8Stages) & 1);  // partners' bulk copies included
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t om = smem_u32(sOm + s * kDig * kOmPlane), ap = smem_u32(sAp + s * kDig * kAPlane);
@@ -246,7 +293,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
         // columns [64 sd, 448) -- one or two MMAs (N <= 256) per Omega digit, 10 per step
 #pragma unroll
         for (int sd = 0; sd < kDig; ++sd) {
-          const uint32_t acc = (stp > 0 || sd > 0) ? 1u : 0u;  // sd = 0 writes every level first
+          const uint32_t acc = (!first || sd > 0) ? 1u : 0u;  // sd = 0 of a sub-chunk's first step writes every level
           const uint64_t da = umma_sdesc(om + sd * 256, kOmGroup);
           const int nt = kDig - sd;                      // A digit planes 0 .. nt-1
           const int n1 = nt > 4 ? 4 : nt;                // first MMA: up to 4 planes (N <= 256)
@@ -257,8 +304,12 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
 #endif
         // the stage's smem (in every CTA of the cluster) may be rewritten once every CTA's MMAs have read it
         umma_commit_cluster(&empty[s], (uint16_t)((1u << ncta) - 1u));
+        if (stp + 1 == t_end || stp + 1 == nsteps) {  // sub-chunk t complete in TMEM -> the epilogue
+          umma_commit(&subdone);
+          ++t;
+          t_end += sub_steps(t);
+        }
       }
-      umma_commit(&done);
     }
   } else if (warp == 1) {
     // ---- A's FP64 rows by TMA
@@ -271,11 +322,28 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
       }
     }
   } else if (warp < 2 + kI8Slice) {
-    // ---- A slicers: unit u = (column j, k-octet o), 256 units per step
+    // ---- A slicers: unit u = (column j, k-octet o), 256 units per step; then (warps 2-5, TMEM lane quadrants
+    // 2, 3, 0, 1) the epilogue of every sub-chunk: row i = 32 (warp % 4) + lane
     const int st_id = tid - 64;
     constexpr int SUPT = 256 / (kI8Slice * 32);  // units per thread
+    const int j = st_id & 63;                    // this thread's column (units st_id + 128 uu)
+    const int quad = warp & 3;
+    const int i = 32 * quad + lane;
+    double* out = partial + ((long long)ky * lp + s0 + i) * np_total + col0;
+    if (nsteps == 0) {  // an empty chunk: no MMA initialised the accumulators
+      for (int c = 0; c < kI8Cols; ++c) out[c] = 0.0;
+    }
+    double f1 = 0.0, f2 = 0.0;
+    int t = 0, t_end = sub_steps(0);
     for (int stp = 0; stp < nsteps; ++stp) {
       const int s = stp % kI8Stages, sa = stp % kI8AStages;
+      if (stp == t_end - sub_steps(t)) {  // a sub-chunk's first step: its exponent bound for column j
+        mbar_wait_sleep(&expfull[t % kExpSlots], (t / kExpSlots) & 1);
+        // a 2^(54 - E_j) as two exact power-of-two scalings (54 - E_j may exceed the double range)
+        const int sh = 54 - sexp[t % kExpSlots][j], sh1 = sh / 2;
+        f1 = ldexp(1.0, sh1);
+        f2 = ldexp(1.0, sh - sh1);
+      }
       mbar_wait_sleep(&afull[sa], (stp / kI8AStages) & 1);
       mbar_wait_sleep(&empty[s], ((stp / kI8Stages) & 1) ^ 1);
       const long long kb = k_begin + (long long)stp * kI8K;
@@ -285,10 +353,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
 #pragma unroll
       for (int uu = 0; uu < SUPT; ++uu) {
         const int u = st_id + kI8Slice * 32 * uu;
-        const int j = u & 63, o = u >> 6;
-        // a 2^(54 - E_j) as two exact power-of-two scalings (54 - E_j may exceed the double range)
-        const int sh = 54 - sexp[j], sh1 = sh / 2;
-        const double f1 = ldexp(1.0, sh1), f2 = ldexp(1.0, sh - sh1);
+        const int o = u >> 6;
         uint32_t lo[8], hi[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -302,8 +367,49 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
       fence_async_shared();  // generic-proxy stores -> visible to the tensor core (async proxy)
       mbar_arrive(&full[s]);
       mbar_arrive(&aempty[sa]);
+      if (stp + 1 == t_end || stp + 1 == nsteps) {
+        // ---- epilogue of sub-chunk t: sum_u ACC_u 2^(8(6-u)) in 64-bit integers, scaled, into the partial
+        mbar_wait_sleep(&subdone, t & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int* E = sexp[t % kExpSlots];
+#pragma unroll 1
+        for (int c0 = 0; c0 < kI8Cols; c0 += 8) {
+          long long hi[8], lo[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) hi[jj] = lo[jj] = 0;
+#pragma unroll
+          for (int u = 0; u < kDig; ++u) {
+            uint32_t v[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                           "=r"(v[7])
+                         : "r"(tmem + ((uint32_t)(32 * quad) << 16) + 64u * u + c0));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const long long a8 = (long long)(int)v[jj];
+              if (u < 3)
+                hi[jj] += a8 << (8 * (2 - u));
+              else
+                lo[jj] += a8 << (8 * (6 - u));
+            }
+          }
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            // N M ~ sum_u ACC_u 2^(8(12-u)) = 2^48 (hi 2^32 + lo); value = N M 2^-51 2^(E_j - 54)
+            const double v = ldexp(fma((double)hi[jj], 0x1p32, (double)lo[jj]), E[c0 + jj] - 57);
+            out[c0 + jj] = t == 0 ? v : out[c0 + jj] + v;
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __threadfence_block();
+        atomicAdd(&drained, 1);  // the exponent slot of sub-chunk t is free again
+        mbar_arrive(&tfree);
+        ++t;
+        t_end += sub_steps(t);
+      }
     }
-  } else {
+  } else if (warp < 2 + kI8Slice + GEN) {
     // ---- Omega generators: unit u = (Omega row i, k-octet o) = 4 Box-Muller pairs; this CTA draws the
     // units [crank UNITS / C, (crank + 1) UNITS / C) of each step for the whole cluster
     const int gt0 = tid - 32 * (2 + kI8Slice);
@@ -373,96 +479,84 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN) * 32, 1)
         mbar_arrive(&full[s]);
       }
     }
-  }
-
-  // ---- epilogue: warps 2-5 (TMEM lane quadrants 2, 3, 0, 1), row i = 32 * (warp % 4) + lane
-  if (warp >= 2 && warp < 6) {
-    const int quad = warp & 3;
-    const int i = 32 * quad + lane;
-    double* out = partial + ((long long)ky * lp + s0 + i) * np_total + col0;
-    if (nsteps == 0) {  // an empty chunk: no MMA initialised the accumulators
-      for (int j = 0; j < kI8Cols; ++j) out[j] = 0.0;
-    } else {
-    mbar_wait_sleep(&done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
+  } else {
+    // ---- exponent scanners: the bound of each column of this CTA over each sub-chunk (max |a| < 2^E, an
+    // all-zero column keeps -1074), ahead of the slicers; non-finite entries set the status (engine.cpp:222).
+    // Scanner w takes the rows k = w (mod kI8Scan) of each group of 16 kI8Scan rows; lane l the columns
+    // col0 + l and col0 + 32 + l. Only the exponent matters (frexp(x) = biased exponent - 1022 for normal
+    // x; 2^-1022 bounds the subnormals), so each load is the 4-byte high word: 32 loads in flight per lane
+    // in 32 registers. Non-finite entries (exponent field 0x7ff) set the status (engine.cpp:222).
+    const int w = warp - (2 + kI8Slice + GEN);
+    const bool ok0 = col0 + lane < n, ok1 = col0 + 32 + lane < n;
+    const unsigned* h0 = reinterpret_cast<const unsigned*>(a + (ok0 ? col0 + lane : 0)) + 1;
+    const unsigned* h1 = reinterpret_cast<const unsigned*>(a + (ok1 ? col0 + 32 + lane : 0)) + 1;
+    const long long ldw = 2 * lda;  // row stride in 32-bit words
+    if (kScanAhead > 0 && w == 0 && lane == 0)
+      for (int b = 0; b < min(kScanAhead, nsteps); ++b) tma_prefetch_2d(&tma_a, col0, (int)(k_begin + 32LL * b));
+    unsigned badbits = 0;
+    int t = 0;
+    for (int b0 = 0; b0 < nsteps; b0 += sub_steps(t), ++t) {
+      const int b1 = min(nsteps, b0 + sub_steps(t));
+      const long long kend = min(k_end, k_begin + 32LL * b1);
+      if (t >= kExpSlots) {  // slot t % 4 is free once the epilogue has drained sub-chunk t - 4
+        while (*(volatile int*)&drained < kI8Slice * 32 * (t - kExpSlots + 1)) __nanosleep(200);
+      }
+      unsigned m0 = 0, m1 = 0;
+#ifdef CQR_I8_NOSCAN  // probe: no scan (bound 2^1: right for |a| < 2 only)
+      m0 = m1 = 0x3ff80000u;
+#else
 #pragma unroll 1
-    for (int c0 = 0; c0 < kI8Cols; c0 += 8) {
-      long long hi[8], lo[8];
+      for (long long k0 = k_begin + 32LL * b0 + w; k0 < kend; k0 += 16 * kI8Scan) {
+        if (kScanAhead > 0 && w == 0 && lane == 0) {
+          const long long bb = (k0 - k_begin) / 32 + kScanAhead;
+          if (bb < nsteps && ((k0 - k_begin) & 31) < kI8Scan) tma_prefetch_2d(&tma_a, col0, (int)(k_begin + 32 * bb));
+        }
+        unsigned x0[16], x1[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0;
+        for (int r = 0; r < 16; ++r) {
+          const long long k = k0 + kI8Scan * r;
+          const unsigned pr = k < kend;
+          x0[r] = x1[r] = 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "@p ld.global.nc.L1::no_allocate.u32 %0, [%2];\n\t@p ld.global.nc.L1::no_allocate.u32 %1, [%3];\n\t}"
+              : "+r"(x0[r]), "+r"(x1[r])
+              : "l"(h0 + k * ldw), "l"(h1 + k * ldw), "r"(pr));
+        }
 #pragma unroll
-      for (int u = 0; u < kDig; ++u) {
-        uint32_t v[8];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                       "=r"(v[7])
-                     : "r"(tmem + ((uint32_t)(32 * quad) << 16) + 64u * u + c0));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const long long a = (long long)(int)v[j];
-          if (u < 3)
-            hi[j] += a << (8 * (2 - u));
-          else
-            lo[j] += a << (8 * (6 - u));
+        for (int r = 0; r < 16; ++r) {
+          const unsigned y0 = x0[r] & 0x7fffffffu, y1 = x1[r] & 0x7fffffffu;
+          badbits |= (y0 + 0x00100000u) | (y1 + 0x00100000u);  // bit 31 set iff the exponent field is 0x7ff
+          m0 = max(m0, y0);
+          m1 = max(m1, y1);
         }
       }
+#endif
+      sexpw[w][lane] = ok0 ? m0 : 0u;
+      sexpw[w][32 + lane] = ok1 ? m1 : 0u;
+      asm volatile("bar.sync %0, %1;" ::"r"(8), "r"(kI8Scan * 32) : "memory");
+      if (w == 0) {
+        int* E = sexp[t % kExpSlots];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        // N M ~ sum_u ACC_u 2^(8(12-u)) = 2^48 (hi 2^32 + lo); value = N M 2^-51 2^(E_j - 54)
-        const double v = fma((double)hi[j], 0x1p32, (double)lo[j]);
-        out[c0 + j] = ldexp(v, sexp[c0 + j] - 57);
+        for (int h = 0; h < 2; ++h) {
+          unsigned mm = 0;
+#pragma unroll
+          for (int ww = 0; ww < kI8Scan; ++ww) mm = max(mm, sexpw[ww][32 * h + lane]);
+          const int be = (int)(mm >> 20);  // biased exponent of the column's largest |a|
+          E[32 * h + lane] = mm == 0 ? -1074 : be == 0 ? -1022 : be - 1022;
+        }
+        mbar_arrive(&expfull[t % kExpSlots]);
       }
+      asm volatile("bar.sync %0, %1;" ::"r"(8), "r"(kI8Scan * 32) : "memory");  // sexpw reusable
     }
-    }
+    const bool bad = (badbits >> 31) != 0;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
   }
+
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   cluster_sync();  // no partner still stores into this CTA's smem or arrives on its barriers
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// exponent bound of each column over each k-chunk (max |a| < 2^E), non-finite entries flagged. Grid
-// (chunks, column blocks, row slices): each block folds its slice with atomicMax (order-independent,
-// so deterministic) into colexp, which the caller initialised to a very small value.
-constexpr int kExpSlices = 8;
-__global__ void sketch_colexp_kernel(const double* __restrict__ a, long long lda, long long m_local, int n,
-                                     long long rows_per_chunk, int np, int y0, int* __restrict__ colexp,
-                                     DevStatus* st) {
-  __shared__ double smax[4][64];
-  const int ky = blockIdx.x + y0;
-  const int jl = threadIdx.x & 63, rl = threadIdx.x >> 6;
-  const int j = blockIdx.y * 64 + jl;
-  const long long c0 = (long long)ky * rows_per_chunk, c1 = min(m_local, c0 + rows_per_chunk);
-  const long long span = (c1 - c0 + kExpSlices - 1) / kExpSlices;
-  const long long k0 = c0 + span * blockIdx.z, k1 = min(c1, k0 + span);
-  double mx = 0.0;
-  bool bad = false;
-  if (j < n) {
-    long long k = k0 + rl;
-    for (; k + 12 < k1; k += 16) {  // four independent loads in flight per thread
-      const double v0 = __ldg(a + k * lda + j), v1 = __ldg(a + (k + 4) * lda + j);
-      const double v2 = __ldg(a + (k + 8) * lda + j), v3 = __ldg(a + (k + 12) * lda + j);
-      bad |= !isfinite(v0) || !isfinite(v1) || !isfinite(v2) || !isfinite(v3);
-      mx = fmax(mx, fmax(fmax(fabs(v0), fabs(v1)), fmax(fabs(v2), fabs(v3))));
-    }
-    for (; k < k1; k += 4) {
-      const double v = __ldg(a + k * lda + j);
-      bad |= !isfinite(v);
-      mx = fmax(mx, fabs(v));
-    }
-  }
-  smax[rl][jl] = mx;
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status_invalid(st);
-  __syncthreads();
-  if (rl == 0 && j < np) {
-    const double m4 = fmax(fmax(smax[0][jl], smax[1][jl]), fmax(smax[2][jl], smax[3][jl]));
-    if (m4 > 0.0) {
-      int e;
-      frexp(m4, &e);  // m4 = f 2^e, f in [0.5, 1): m4 < 2^e
-      atomicMax(colexp + (long long)ky * np + j, e);
-    }
-  }
 }
 
 cudaError_t ensure_tables_i8(cudaStream_t s) {
@@ -491,7 +585,40 @@ bool sketch_i8_ok(const double* a, long long lda, long long m_global, long long 
                       CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
-void sketch_i8_plan(SketchPlan& p, long long m_local, int n, int l, int num_sms) {
+namespace {
+// concurrent clusters of C sketch CTAs on this device (cached per (device, C))
+long long max_active_clusters(int C, int num_sms) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, long long> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return std::max(1, num_sms / C);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find({dev, C});
+  if (it != cache.end()) return it->second;
+  auto kern = C >= 8 ? sketch_i8_kernel<12> : sketch_i8_kernel<CQR_I8_GEN>;
+  const int warps = 2 + kI8Slice + (C >= 8 ? 12 : CQR_I8_GEN) + kI8Scan;
+  long long v = std::max(1, num_sms / C);
+  int nc = 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1, 1, (unsigned)C);
+  cfg.blockDim = dim3(warps * 32, 1, 1);
+  cfg.dynamicSmemBytes = kI8Smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = (unsigned)C;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (allow_max_smem(kern) == cudaSuccess && cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc > 0)
+    v = nc;
+  cudaGetLastError();
+  cache[{dev, C}] = v;
+  return v;
+}
+}  // namespace
+
+void sketch_i8_plan(SketchPlan& p, long long m_local, int n, int l, int num_sms, int splits) {
   p.i8 = 1;
   p.ws = 0;
   p.n = n;
@@ -502,15 +629,21 @@ void sketch_i8_plan(SketchPlan& p, long long m_local, int n, int l, int num_sms)
   p.m_local = m_local;
   p.s_tiles = (l + kI8Rows - 1) / kI8Rows;
   p.lp = p.s_tiles * kI8Rows;
-  const long long per = (long long)p.s_tiles * (p.np / kI8Cols);
-  long long kc = (m_local + kI8MaxChunk - 1) / kI8MaxChunk;
-  if (kc < 1) kc = 1;
-  // whole waves of one CTA per SM where the chunk bound allows
-  const long long waves = (kc * per + num_sms - 1) / num_sms;
-  const long long kc_w = waves * num_sms / per;
-  if (kc_w > kc) kc = kc_w;
+  // the fewest k-chunks whose clusters (s_tiles per k-chunk, C = np / 64 CTAs each) fill whole rounds of
+  // the device's concurrent clusters (cudaOccupancyMaxActiveClusters: clusters of 4 or 8 do not tile all
+  // 148 SMs); every CTA runs its chunk as sub-chunks (sub_steps), so a chunk has no size bound. The host
+  // pipeline launches the chunks in `splits` row ranges: splits x as many.
+  const long long slots = max_active_clusters(p.np / kI8Cols, num_sms);
+  long long g = slots, b = p.s_tiles;
+  while (b) {
+    const long long r = g % b;
+    g = b;
+    b = r;
+  }
+  long long kc = std::max<long long>(1, slots / g) * std::max(1, splits);
   const long long max_kc = (m_local + kI8K - 1) / kI8K;
   if (kc > max_kc) kc = max_kc;
+  if (kc < 1) kc = 1;
   long long rpc = (m_local + kc - 1) / kc;
   rpc = (rpc + kI8K - 1) / kI8K * kI8K;
   if (rpc < kI8K) rpc = kI8K;
@@ -518,12 +651,14 @@ void sketch_i8_plan(SketchPlan& p, long long m_local, int n, int l, int num_sms)
   p.kchunks = (int)((m_local + rpc - 1) / rpc);
   if (p.kchunks < 1) p.kchunks = 1;
   p.partial_doubles = (size_t)p.kchunks * p.lp * p.np;
-  p.aux_ints = (size_t)p.kchunks * p.np;
+  static const bool dbg = std::getenv("CQR_DEBUG_PLAN") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "sketch_i8_plan: m=%lld n=%d l=%d s_tiles=%d C=%d slots=%lld kchunks=%d rows/chunk=%lld\n",
+                 m_local, n, l, p.s_tiles, p.np / kI8Cols, slots, p.kchunks, p.rows_per_chunk);
 }
 
 cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda, long long m_global, long long row0,
-                             uint64_t seed, double* partial, int* colexp, const DevStatus* st, cudaStream_t s, int y0,
-                             int y1) {
+                             uint64_t seed, double* partial, const DevStatus* st, cudaStream_t s, int y0, int y1) {
   if (y1 < 0) y1 = p.kchunks;
   if (y1 <= y0) return cudaSuccess;
   cudaError_t e = ensure_tables_i8(s);
@@ -531,14 +666,10 @@ cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda
   CUtensorMap tm;
   if (!make_tmap_2d(&tm, a, p.n, p.m_local, lda, kI8Cols, kI8K, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
-  e = cudaMemsetAsync(colexp + (size_t)y0 * p.np, 0x80, sizeof(int) * (size_t)(y1 - y0) * p.np, s);  // very small
-  if (e != cudaSuccess) return e;
-  sketch_colexp_kernel<<<dim3((unsigned)(y1 - y0), (unsigned)(p.np / 64), kExpSlices), 256, 0, s>>>(
-      a, lda, p.m_local, p.n, p.rows_per_chunk, p.np, y0, colexp, const_cast<DevStatus*>(st));
   const int ncta = p.np / kI8Cols;
   auto kern = ncta >= 8 ? sketch_i8_kernel<12> : sketch_i8_kernel<CQR_I8_GEN>;
-  const int warps = 2 + kI8Slice + (ncta >= 8 ? 12 : CQR_I8_GEN);
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
+  const int warps = 2 + kI8Slice + (ncta >= 8 ? 12 : CQR_I8_GEN) + kI8Scan;
+  e = allow_max_smem(kern);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / kI8Cols));
@@ -552,8 +683,8 @@ cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda
   attr[0].val.clusterDim.z = (unsigned)(p.np / kI8Cols);
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tm, p.m_local, m_global, row0, p.l, seed, p.rows_per_chunk,
-                            (const int*)colexp, partial, p.lp, p.np, y0, st);
+  return cudaLaunchKernelEx(&cfg, kern, tm, a, lda, p.m_local, m_global, row0, p.l, p.n, seed, p.rows_per_chunk,
+                            partial, p.lp, p.np, y0, const_cast<DevStatus*>(st));
 }
 
 }  // namespace cqr

@@ -719,7 +719,7 @@ cudaError_t launch_lu_split(const double* a1, int l, int n, double* u, double* w
 template <int NW, int PW>
 cudaError_t launch_lu_rot(const double* a1, int l, int n, double* u, double* work, DevStatus* st, cudaStream_t s) {
   const size_t smem = (size_t)l * kLuLdp * sizeof(double) + (size_t)l * sizeof(int);
-  cudaError_t e = cudaFuncSetAttribute(lu_rot_kernel<NW, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(lu_rot_kernel<NW, PW>);
   if (e != cudaSuccess) return e;
   lu_rot_kernel<NW, PW><<<1, NW * 32, smem, s>>>(a1, l, n, u, work, st);
   return cudaGetLastError();
@@ -1189,7 +1189,7 @@ template <typename K, typename... Args>
 cudaError_t launch_small(K kernel, size_t bytes, cudaStream_t s, Args... args) {
   const int use_smem = bytes <= kSmemCap ? 1 : 0;
   const size_t smem = use_smem ? bytes : 0;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+  cudaError_t e = allow_max_smem(kernel);
   if (e != cudaSuccess) return e;
   (void)use_smem;
   kernel<<<1, kT, smem, s>>>(args...);
@@ -1362,7 +1362,7 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
   if (n >= split_min && n > 64) {
     const size_t smem = (size_t)kChPanel * (n + 1) * sizeof(double);
     cudaError_t e =
-        cudaFuncSetAttribute(cholesky_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allow_max_smem(cholesky_blocked_kernel<true>);
     if (e == cudaSuccess) e = cudaMemcpyAsync(work, g, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
     for (int j0 = 0; j0 < n; j0 += kChPanel) {
@@ -1380,7 +1380,7 @@ cudaError_t launch_cholesky(const double* g, int n, double* r, double* work, int
   if (n > 64) {
     const size_t smem = (size_t)kChPanel * (n + 1) * sizeof(double);
     cudaError_t e =
-        cudaFuncSetAttribute(cholesky_blocked_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allow_max_smem(cholesky_blocked_kernel<false>);
     if (e != cudaSuccess) return e;
     cholesky_blocked_kernel<false><<<1, kChThreads, smem, s>>>(g, n, r, work, shift_mode, shift_value, theory_coef, shift_out, st);
     return cudaGetLastError();
@@ -1414,7 +1414,7 @@ cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work,
     // work holds l*n doubles for W, followed by the tall panel when it does not fit
     if (fits) {
       cudaError_t e =
-          cudaFuncSetAttribute(lu_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+          allow_max_smem(lu_blocked_kernel<true>);
       if (e != cudaSuccess) return e;
       lu_blocked_kernel<true><<<1, 512, smem, s>>>(a1, l, n, u, work, nullptr, st);
     } else {
@@ -1424,7 +1424,7 @@ cudaError_t launch_lu_u(const double* a1, int l, int n, double* u, double* work,
   }
   const int rs = (int)std::min<size_t>((size_t)l, kSmemCap / ((size_t)n * sizeof(double)));
   const size_t smem = (size_t)rs * n * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+  cudaError_t e = allow_max_smem(lu_kernel);
   if (e != cudaSuccess) return e;
   lu_kernel<<<1, kT, smem, s>>>(a1, l, n, u, work, rs, st);
   return cudaGetLastError();
@@ -1628,7 +1628,7 @@ cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work,
   static const bool no_split = std::getenv("CQR_QR_NO_SPLIT") != nullptr;  // A/B runs: the one-CTA kernel
   if (!use_smem && bsmem <= 200 * 1024 && !no_split) {  // per-panel launches, trailing update over many SMs
     cudaError_t e =
-        cudaFuncSetAttribute(qr_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+        allow_max_smem(qr_blocked_kernel<true>);
     if (e != cudaSuccess) return e;
     double* Vg = work + (size_t)l * n;  // kQrB x l, then Tg (kQrB x kQrB): qr_work_doubles
     double* Tg = Vg + (size_t)kQrB * l;
@@ -1642,7 +1642,7 @@ cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work,
   }
   if (!use_smem && bsmem <= 200 * 1024) {  // blocked: the panel and V^T A2 in shared memory
     cudaError_t e =
-        cudaFuncSetAttribute(qr_blocked_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+        allow_max_smem(qr_blocked_kernel<false>);
     if (e != cudaSuccess) return e;
     qr_blocked_kernel<false><<<1, kQrT, bsmem, s>>>(a1, l, n, r, work, st);
     return cudaGetLastError();
@@ -1654,7 +1654,7 @@ cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work,
 #define CQR_QR_WARPS 16
 #endif
     cudaError_t e =
-        cudaFuncSetAttribute(qr_warp_kernel<CQR_QR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+        allow_max_smem(qr_warp_kernel<CQR_QR_WARPS>);
     if (e != cudaSuccess) return e;
     qr_warp_kernel<CQR_QR_WARPS><<<1, CQR_QR_WARPS * 32, wbytes, s>>>(a1, l, n, r, st);
     return cudaGetLastError();

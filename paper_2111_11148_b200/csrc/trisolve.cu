@@ -329,7 +329,7 @@ cudaError_t launch_trisolve_sb_t(const TrisolveArgs& a, cudaStream_t s) {
   const size_t smem =
       (size_t)(NT * kDiagStride + (BSMEM ? NT * (NT - 1) * 32 : 0) + WPC * 8 * MG * 8) * sizeof(double);
   auto k = trisolve_sb_kernel<NP, WPC, BSMEM, WIN, MG>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(k);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + 8 * MG - 1) / (8 * MG);
   long long grid = (groups + WPC - 1) / WPC;

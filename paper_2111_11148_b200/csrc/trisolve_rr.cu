@@ -242,7 +242,7 @@ cudaError_t launch_rr(const TrisolveArgs& a, cudaStream_t s) {
       !make_tmap_2d(&tst, a.out, a.n, a.m, a.ldo, 8, RW, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorNotSupported;
   auto k = trisolve_rr_kernel<NP, RW, WPC, BSMEM>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  cudaError_t e = allow_max_smem(k);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + RW - 1) / RW;
   long long grid = (groups + WPC - 1) / WPC;

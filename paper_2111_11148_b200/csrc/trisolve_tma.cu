@@ -411,7 +411,7 @@ cudaError_t launch_t(const TrisolveArgs& a, cudaStream_t s) {
     return cudaErrorNotSupported;
   const size_t smem = (size_t)(head_doubles<NP, BSMEM>() + WPC * kWarpDoubles) * 8 + WPC * 16 + 512;
   auto k = trisolve_tma_kernel<NP, WPC, BSMEM, TMW>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(k);
   if (e != cudaSuccess) return e;
   const long long groups = (a.m + kRW - 1) / kRW;
   long long grid = (groups + WPC - 1) / WPC;
