@@ -112,6 +112,99 @@ __global__ void __launch_bounds__(kWpc * 32) gram_leaf_kernel(const double* __re
   }
 }
 
+// n in (32, 64] (c3): 32 x 32 macro tiles, four warps per leaf -- warp 0 the diagonal tile of columns
+// 0..31 (10 upper 8 x 8 blocks), warp 1 that of 32..63, warps 2 and 3 the two 32 x 16 halves of the
+// off-diagonal tile (8 blocks each): 36 DMMAs per k4 step against 20 fragment loads (the 16 x 16 tiling
+// needs 40 loads for the same 36 DMMAs, and its 10 tiles spread unevenly over 8 warps). Same k order per
+// element as gram_leaf_kernel: bit-identical partials.
+template <int CH>
+__global__ void __launch_bounds__(128) gram_leaf64_kernel(const double* __restrict__ x, long long ldx, long long m,
+                                                          int n, double* __restrict__ partial, int vec16, int check,
+                                                          int leaf0, DevStatus* st) {
+  constexpr int NP = 64, LDX = NP + 4;
+  extern __shared__ __align__(16) double smem[];
+  if (failed(st)) return;
+  const int leaf = blockIdx.x + leaf0;
+  const long long r0 = (long long)leaf * kLeafRows;
+  const int rows = (int)min((long long)kLeafRows, m - r0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, gr = lane >> 2;
+  // this warp's row blocks I in [i0, i0 + 4) and column blocks J in [j0, j0 + nj); diagonal tiles keep I <= J
+  const int i0 = warp == 1 ? 4 : 0;
+  const int j0 = warp == 0 ? 0 : warp == 1 ? 4 : warp == 2 ? 4 : 6;
+  const bool diag = warp < 2;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const double* xg = x + r0 * ldx;
+  const int nch = (rows + CH - 1) / CH;
+  bool bad = false;
+  stage_rows(smem, LDX, xg, ldx, min(CH, rows), CH, n, NP, tid, 128, vec16 != 0);
+  cp_async_commit();
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      const int rr = min(CH, rows - (c + 1) * CH);
+      stage_rows(smem + ((c + 1) & 1) * CH * LDX, LDX, xg + (long long)(c + 1) * CH * ldx, ldx, rr, CH, n, NP, tid,
+                 128, vec16 != 0);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* xb = smem + (c & 1) * CH * LDX;
+#pragma unroll 2
+    for (int k4 = 0; k4 < CH / 4; ++k4) {
+      const double* xr = xb + (4 * k4 + q) * LDX + gr;
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = xr[8 * (i0 + a)];
+      if (diag) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) bad |= nonfinite(av[a]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = a; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], av[a], av[b]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) bv[b] = xr[8 * (j0 + b)];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      }
+    }
+    __syncthreads();
+  }
+  if (check && __any_sync(0xffffffffu, bad) && lane == 0) set_status_invalid(st);
+  double* out = partial + (long long)leaf * NP * NP;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (diag ? b < a : b >= 2) continue;
+      const int i = 8 * (i0 + a) + gr, j = 8 * (diag ? i0 + b : j0 + b) + 2 * q;
+      *reinterpret_cast<double2*>(out + i * NP + j) = make_double2(acc[a][b][0], acc[a][b][1]);
+    }
+}
+
+template <int CH>
+cudaError_t launch_leaves_64(const GramPlan& p, const double* x, long long ldx, double* partial, int vec16, int check,
+                             const DevStatus* st, cudaStream_t s, int leaf0, int leaf1) {
+  if (leaf1 < 0) leaf1 = p.leaves;
+  if (leaf1 <= leaf0) return cudaSuccess;
+  const size_t smem = (size_t)2 * CH * (64 + 4) * sizeof(double);
+  auto k = gram_leaf64_kernel<CH>;
+  cudaError_t e = allow_max_smem(k);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)(leaf1 - leaf0), 128, smem, s>>>(x, ldx, p.m, p.n, partial, vec16, check, leaf0,
+                                                 const_cast<DevStatus*>(st));
+  return cudaGetLastError();
+}
+
 // Persistent variant (the default where the tile count divides evenly over the
 // warps): one CTA per SM walks the leaves blockIdx.x, +gridDim.x, ...; the row
 // chunks of consecutive leaves form one cp.async stream, so the next leaf's
@@ -216,6 +309,9 @@ __global__ void __launch_bounds__(WPC * 32, 1)
 constexpr int kGtMma = 12;
 #ifndef CQR_GRAM_CH256
 #define CQR_GRAM_CH256 32  // rows per ring stage at n in (128, 256] (16 rows: 2.32 vs 2.30 ms)
+#endif
+#ifndef CQR_GRAM_CH64
+#define CQR_GRAM_CH64 32
 #endif
 #ifndef CQR_GRAM_CH128
 #define CQR_GRAM_CH128 64  // rows per ring stage at n in (64, 128] (16/32/64: 0.677/0.636/0.628 ms at c1)
@@ -576,6 +672,9 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
     if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     return cudaErrorInvalidValue;
   }
+  static const bool no64 = std::getenv("CQR_GRAM_NO64") != nullptr;  // A/B: the 16 x 16 tiling at n <= 64
+  if (p.np == 64 && !p.persistent && !no64)
+    return launch_leaves_64<CQR_GRAM_CH64>(p, x, ldx, partial, vec16, check, st, s, leaf0, leaf1);
   if (p.persistent) {
     if (p.np == 128 && p.maxt == 3)
       return launch_leaves_p<128, 12, 3, 32>(p, x, ldx, tiles, partial, vec16, check, st, s, leaf0, leaf1, num_sms);
