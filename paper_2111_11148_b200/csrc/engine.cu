@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -55,6 +56,8 @@ struct cqr_ctx {
   DevStatus* status = nullptr;   // device
   DevStatus* status_h = nullptr;  // pinned host
   double* scal_h = nullptr;       // pinned host scalars
+  double* r_pin = nullptr;        // pinned host R staging (the early R copy)
+  size_t r_pin_n = 0;
   ncclComm_t comm = nullptr;
   cqr_host_comm hcomm{};     // caller-owned host transport (cqr_attach_host_comm)
   bool has_hcomm = false;
@@ -310,6 +313,8 @@ struct Job {
   std::vector<long long> bounds;  // chunk row boundaries, bounds.front() = 0, bounds.back() = m
   int waited = 0;                 // H2D chunks the compute stream already waits on
   int det = 0;  // every rank holds its standard row block: the rank-count-independent Gram (gram_shard.cu)
+  bool want_r = false;     // the caller takes R back to the host
+  bool r_copied = false;   // R already on its way to c->r_pin on the copy stream (overlapping the last solve)
 };
 
 bool pipelined(const Job& j) { return j.a_host != nullptr; }
@@ -937,6 +942,21 @@ Outcome run_precond(Job& j) {
       LAUNCH(c, cqr::launch_pack_r(rh, n, n, pack2, 0, c->status, c->stream, r_less ? nullptr : sgn));
       final_solve(j, j.q, j.ldq, pack2);  // the column signs are folded into the pack
     }
+    if (!r_less && j.want_r) {  // R is final: bring it to pinned host memory while the last solve runs
+      if (c->r_pin_n < (size_t)n * n) {
+        if (c->r_pin) cudaFreeHost(c->r_pin);
+        c->r_pin = nullptr;
+        c->r_pin_n = 0;
+        ck(cudaMallocHost(&c->r_pin, sizeof(double) * n * n), "cudaMallocHost (R staging)");
+        c->r_pin_n = (size_t)n * n;
+      }
+      if (!c->cstream) ck(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking), "copy stream");
+      cudaEvent_t e = next_event(c);
+      ck(cudaEventRecord(e, c->stream), "record");  // after normalize_sign (recover) and the pack
+      ck(cudaStreamWaitEvent(c->cstream, e, 0), "wait R");
+      ck(cudaMemcpyAsync(c->r_pin, r, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->cstream), "R D2H");
+      j.r_copied = true;
+    }
     push_stage(o.rep, CQR_STAGE_TRISOLVE);
     if (!r_less) push_stage(o.rep, CQR_STAGE_RECOVER);
     DevStatus s = read_status(c);
@@ -957,8 +977,7 @@ void fill_report(cqr_ctx* c, cqr_report* rep, const Outcome* o, int status, long
   double ms[CQR_STAGE_COUNT] = {0};
   for (auto& e : c->stage_evs) {
     float t = 0.f;
-    if (cudaEventSynchronize(e.b) == cudaSuccess && cudaEventElapsedTime(&t, e.a, e.b) == cudaSuccess)
-      ms[e.stage] += t;
+    if (cudaEventElapsedTime(&t, e.a, e.b) == cudaSuccess) ms[e.stage] += t;  // the stream is synchronised
   }
   cudaGetLastError();
   c->stage_evs.clear();
@@ -1030,10 +1049,31 @@ void check_finite(cqr_ctx* c, const double* a, long long m, int n, long long lda
   ++c->launches;
 }
 
+// CQR_TRACE=1: host timeline of one call (us since entry) and the device gap before the first stage
+struct CallTrace {
+  bool on = false;
+  std::chrono::steady_clock::time_point t0;
+  cudaEvent_t e0 = nullptr;
+  std::vector<std::pair<const char*, double>> marks;
+  void mark(const char* what) {
+    if (on)
+      marks.push_back({what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count()});
+  }
+};
+
 int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_report* report) {
+  static const bool trace = std::getenv("CQR_TRACE") != nullptr;
+  CallTrace tr;
+  tr.on = trace;
+  if (tr.on) {
+    tr.t0 = std::chrono::steady_clock::now();
+    cudaEventCreate(&tr.e0);
+    cudaEventRecord(tr.e0, c->stream);
+  }
   Outcome o;
   long long index = -1;
   const bool r_less = j.opts.r_less != 0;
+  j.want_r = r_host != nullptr;
   const long long l =
       (j.m_global >= j.n && j.n >= 1) ? resolved_size(j.cfg, j.m_global, j.n) : 0;
   c->stage_evs.clear();
@@ -1094,12 +1134,17 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
       default:
         throw Fail{CQR_INVALID_ARGUMENT, -1, "unknown method"};
     }
-    if (o.has_r && r_host) {
+    tr.mark("attempts done (status read)");
+    if (o.has_r && r_host && j.r_copied) {
+      ck(cudaStreamSynchronize(c->cstream), "sync R");
+      for (int i = 0; i < j.n; ++i) std::memcpy(r_host + (size_t)i * ldr, c->r_pin + (size_t)i * j.n, sizeof(double) * j.n);
+    } else if (o.has_r && r_host) {
       ck(cudaMemcpy2DAsync(r_host, sizeof(double) * ldr, o.r_dev, sizeof(double) * j.n, sizeof(double) * j.n, j.n,
                            cudaMemcpyDeviceToHost, c->stream),
          "R D2H");
       ck(cudaStreamSynchronize(c->stream), "sync");
     }
+    tr.mark("R D2H");
   } catch (const Fail& e) {
     st = e.code;
     index = e.index;
@@ -1108,6 +1153,19 @@ int factor_dev_impl(cqr_ctx* c, Job& j, double* r_host, long long ldr, cqr_repor
     cudaGetLastError();
   }
   fill_report(c, report, st == CQR_OK ? &o : nullptr, st, index, r_less, j.method, j.n, l, j.opts.workers);
+  tr.mark("report");
+  if (tr.on) {
+    float gap = 0.f, span = 0.f;
+    if (!c->stage_evs.empty()) {
+      cudaEventElapsedTime(&gap, tr.e0, c->stage_evs.front().a);
+      cudaEventElapsedTime(&span, c->stage_evs.front().a, c->stage_evs.back().b);
+    }
+    std::fprintf(stderr, "CQR_TRACE device: entry->first stage %.1f us, first->last stage %.1f us; host:", gap * 1e3,
+                 span * 1e3);
+    for (auto& m : tr.marks) std::fprintf(stderr, " %s %.1f", m.first, m.second);
+    std::fprintf(stderr, "\n");
+    cudaEventDestroy(tr.e0);
+  }
   return st;
 }
 
@@ -1184,6 +1242,7 @@ int cqr_destroy(cqr_ctx* c) {
   if (c->status) cudaFree(c->status);
   if (c->status_h) cudaFreeHost(c->status_h);
   if (c->scal_h) cudaFreeHost(c->scal_h);
+  if (c->r_pin) cudaFreeHost(c->r_pin);
   if (c->stage_h) cudaFreeHost(c->stage_h);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->cstream) cudaStreamDestroy(c->cstream);

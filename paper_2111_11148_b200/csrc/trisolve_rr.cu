@@ -260,13 +260,16 @@ cudaError_t launch_rr(const TrisolveArgs& a, cudaStream_t s) {
 #ifndef CQR_RR128_BSMEM
 #define CQR_RR128_BSMEM true
 #endif
+#ifndef CQR_RR64_RW
+#define CQR_RR64_RW 32
+#endif
 #ifndef CQR_RR64_WPC
 #define CQR_RR64_WPC 8  // 226 registers, no spills (10 warps: 168 registers with spills, 1.32 vs 1.03 ms at c3)
 #endif
 cudaError_t launch_trisolve_rr(const TrisolveArgs& a, int np, cudaStream_t s) {
   switch (np) {
     case 32: return launch_rr<32, 32, 12, true>(a, s);
-    case 64: return launch_rr<64, 32, CQR_RR64_WPC, true>(a, s);
+    case 64: return launch_rr<64, CQR_RR64_RW, CQR_RR64_WPC, true>(a, s);
     case 128: return launch_rr<128, 16, CQR_RR128_WPC, CQR_RR128_BSMEM>(a, s);
   }
   return cudaErrorNotSupported;
