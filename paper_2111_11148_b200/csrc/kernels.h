@@ -31,6 +31,8 @@ struct TrisolveArgs {
   int variant = 0;  // 0: the TMA kernel when eligible, else the register kernel; nonzero: the register kernel
 };
 cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s);
+// panel.cu: X[:, c0:c0+128] <- A[:, c0:c0+128] - X[:, 0:c0] R[0:c0, c0:c0+128] (k-ordered DMMA chains)
+cudaError_t launch_panel_update(const TrisolveArgs& a, int c0, cudaStream_t s);
 // trisolve_tma.cu: the TMA-staged kernel (16-byte aligned bases, even leading dimensions, np >= 32)
 bool trisolve_tma_eligible(const TrisolveArgs& a, int np);
 cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s);

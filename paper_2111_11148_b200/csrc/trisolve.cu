@@ -21,6 +21,8 @@
 //
 // Per row: HBM 8n bytes read + 8n written; n^2 flops (n(n-1)/2 fma + n div).
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "trisolve_common.cuh"
@@ -91,7 +93,7 @@ __global__ void pack_r_kernel(const double* __restrict__ r, int ldr, int n, int 
     }
   }
   // diagonal check, lowest failing index (kernels.hpp:106-107 / engine.cpp:118-127)
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; bad_min && j < n; j += gridDim.x * blockDim.x) {
     const double dj = r[(long long)j * ldr + j];
     if (dj == 0.0 || (degenerate && !isfinite(dj))) atomicMin(bad_min, j);
   }
@@ -352,10 +354,22 @@ int trisolve_np(int n) {
   return 512;
 }
 
+// The wide solve in 128-column panels (panel.cu): n a multiple of 128, at least 384 (m = 1e6: n = 512
+// 9.98 -> 9.09 ms; n = 256 2.61 -> 2.64 ms, so the one-pass kernel stays there).
+static bool panel_path(int n) {
+  static const bool off = std::getenv("CQR_TRISOLVE_NO_PANELS") != nullptr;  // A/B: the one-pass kernel
+  return !off && n >= 384 && n % 128 == 0 && n <= 512;
+}
+constexpr size_t kSubPack = 16 * 15 * 32 + 16 * kDiagStride + 128;  // one 128-column diagonal block's pack
+
+static size_t full_pack_doubles(int np) {
+  const int nt = np / 8;
+  return ((size_t)nt * (nt - 1) * 32 + (size_t)nt * kDiagStride + 8 + 127) / 128 * 128;
+}
+
 size_t trisolve_pack_doubles(int n) {
   const int np = trisolve_np(n);
-  const int nt = np / 8;
-  return (size_t)nt * (nt - 1) * 32 + (size_t)nt * kDiagStride + 8;
+  return full_pack_doubles(np) + (panel_path(n) ? (size_t)(n / 128) * kSubPack : 0);
 }
 
 cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int degenerate, DevStatus* st,
@@ -373,6 +387,13 @@ cudaError_t launch_pack_r(const double* r, int ldr, int n, double* pack, int deg
   if (e != cudaSuccess) return e;
   pack_r_kernel<<<grid, 256, 0, s>>>(r, ldr, n, np, bpack, dpack, bad, degenerate, sgn, st);
   pack_status_kernel<<<1, 1, 0, s>>>(bad, n, st);
+  if (panel_path(n)) {  // the diagonal 128 x 128 blocks, each packed as an n = 128 problem
+    for (int p = 0; p < n / 128; ++p) {
+      double* sp = pack + full_pack_doubles(np) + (size_t)p * kSubPack;
+      pack_r_kernel<<<64, 256, 0, s>>>(r + (size_t)128 * p * ldr + 128 * p, ldr, 128, 128, sp, sp + 16 * 15 * 32,
+                                       nullptr, degenerate, sgn ? sgn + 128 * p : nullptr, st);
+    }
+  }
   return cudaGetLastError();
 }
 
@@ -383,6 +404,36 @@ cudaError_t launch_trisolve(TrisolveArgs a, cudaStream_t s) {
   a.dpack = a.pack + (size_t)nt * (nt - 1) * 32;
   // variant 0: the register-resident right-looking kernel (np <= 128) or the left-looking TMA kernel
   // (wider); 2: the left-looking TMA kernel at every width; 1: the register kernel (A/B runs)
+  if (a.variant == 0 && panel_path(a.n) && trisolve_tma_eligible(a, np)) {
+    // 128-column panels: the GEMM update of panel p by panels 0 .. p-1, then the n = 128 solve in place
+    bool ok = true;
+    for (int p = 0; p < a.n / 128 && ok; ++p) {
+      if (p > 0) {
+        const cudaError_t e = launch_panel_update(a, 128 * p, s);
+        if (e == cudaErrorNotSupported) {
+          ok = false;
+          break;
+        }
+        if (e != cudaSuccess) return e;
+      }
+      TrisolveArgs b = a;
+      b.in = p == 0 ? a.in : a.out + 128 * p;
+      b.ldi = p == 0 ? a.ldi : a.ldo;
+      b.out = a.out + 128 * p;
+      b.n = 128;
+      b.pack = a.pack + full_pack_doubles(np) + (size_t)p * kSubPack;
+      b.bpack = b.pack;
+      b.dpack = b.pack + 16 * 15 * 32;
+      if (!trisolve_tma_eligible(b, 128)) {
+        ok = false;
+        break;
+      }
+      const cudaError_t e = launch_trisolve_tma(b, 128, s);
+      if (e != cudaSuccess) return e;
+    }
+    if (ok) return cudaSuccess;
+    // (only reachable before the first launch: the eligibility of the views matches the whole matrix's)
+  }
   if ((a.variant == 0 || a.variant == 2) && trisolve_tma_eligible(a, np)) {
     // the right-looking kernel at np <= 64 (c3: 1.032 vs 1.058 ms per call; at np = 128 its 16-row
     // warps leave the diagonal recurrence on half the lanes: 0.97 vs 0.77 ms, so the left-looking kernel;

@@ -187,7 +187,9 @@ def test_cholesky_known_and_breakdown():
 
 @pytest.mark.parametrize("m,n,seed", [(1, 2, 1), (30, 5, 2), (100, 8, 3), (2000, 9, 4), (3001, 24, 5),
                                       (10000, 64, 6), (4099, 128, 7), (1000, 100, 8), (700, 256, 9),
-                                      (300, 300, 10), (200, 512, 11)])
+                                      (300, 300, 10), (200, 512, 11),
+                                      # the 128-column panel path (GEMM update + n = 128 panel solves)
+                                      (20003, 256, 12), (5003, 512, 13), (1, 384, 14), (3000, 384, 15)])
 def test_trisolve_bitwise(m, n, seed):
     a = o.gaussian_matrix(m, n, seed)
     r = o.qr_r_factor(o.gaussian_matrix(2 * n + 3, n, seed + 100))
