@@ -174,7 +174,18 @@ __device__ __forceinline__ void split64(long long v, uint32_t& lo, uint32_t& hi)
 
 // Generator teams: with C CTAs sharing an Omega tile each CTA draws 1/C of it per step, too little work to
 // hide one thread's Box-Muller latency; T teams then take every T-th step, so T steps are drawn at once.
-__host__ __device__ constexpr int gen_teams(int ncta) { return ncta >= 4 ? 4 : ncta; }
+#ifndef CQR_I8_TEAMS2
+#define CQR_I8_TEAMS2 4  // clusters of 2 (c1): 2/4 teams 1.89/1.80 ms
+#endif
+#ifndef CQR_I8_TEAMS4
+#define CQR_I8_TEAMS4 4  // clusters of 4/8 (c2/c4): 2 teams 24.6/16.8 ms vs 4 teams 24.0/16.4 (<= 7: bar ids 1..7)
+#endif
+#ifndef CQR_I8_TEAMS1
+#define CQR_I8_TEAMS1 1
+#endif
+__host__ __device__ constexpr int gen_teams(int ncta) {
+  return ncta >= 4 ? CQR_I8_TEAMS4 : ncta == 2 ? CQR_I8_TEAMS2 : CQR_I8_TEAMS1;
+}
 
 // Sub-chunks: a CTA's rows [k_begin, k_end) are accumulated in TMEM in sub-chunks of kSubFirst, 4x, 16x ...
 // steps (capped at 512 steps = kI8MaxChunk rows, the s32 exactness bound), each with its own column
