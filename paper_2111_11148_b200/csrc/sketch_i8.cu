@@ -45,14 +45,33 @@ namespace {
 constexpr int kI8Rows = 128;      // Omega rows per CTA (MMA M)
 constexpr int kI8Cols = 64;       // A columns per CTA (MMA N)
 constexpr int kI8K = 32;          // rows of A per step (MMA K for kind::i8)
-#ifndef CQR_I8_STAGES
-#define CQR_I8_STAGES 4
+// ring depths per cluster size C (digit-plane stages S, FP64 A stages AS; S >= generator teams, smem
+// S 42 KB + AS 16 KB <= 218 KB): C = 1 (c3) S 3 AS 4: 2.65 vs 2.70 ms (S 4 AS 2); C = 2 (c1) S 4 AS 3: 1.77 vs 1.80;
+// C = 4, 8 (c2, c4) S 4 AS 3: 23.79 / 16.32 vs 23.98 / 16.40 ms (AS 2)
+#ifndef CQR_I8_S1
+#define CQR_I8_S1 3
 #endif
-constexpr int kI8Stages = CQR_I8_STAGES;  // digit-plane ring
-#ifndef CQR_I8_ASTAGES
-#define CQR_I8_ASTAGES 2
+#ifndef CQR_I8_AS1
+#define CQR_I8_AS1 4
 #endif
-constexpr int kI8AStages = CQR_I8_ASTAGES;  // FP64 A ring
+#ifndef CQR_I8_S2
+#define CQR_I8_S2 4
+#endif
+#ifndef CQR_I8_AS2
+#define CQR_I8_AS2 3
+#endif
+#ifndef CQR_I8_S4
+#define CQR_I8_S4 4
+#endif
+#ifndef CQR_I8_AS4
+#define CQR_I8_AS4 3
+#endif
+#ifndef CQR_I8_S8
+#define CQR_I8_S8 4
+#endif
+#ifndef CQR_I8_AS8
+#define CQR_I8_AS8 3
+#endif
 #ifndef CQR_I8_GEN
 #define CQR_I8_GEN 16
 #endif
@@ -69,7 +88,9 @@ constexpr int kOmPlane = kI8Rows * kI8K;  // bytes per Omega digit plane (4 KB)
 constexpr int kAPlane = kI8Cols * kI8K;   // bytes per A digit plane (2 KB)
 constexpr int kStageBytes = kDig * (kOmPlane + kAPlane);
 constexpr int kATile = kI8K * kI8Cols;    // doubles per FP64 A stage
-constexpr size_t kI8Smem = (size_t)kI8Stages * kStageBytes + (size_t)kI8AStages * kATile * 8 + 1024;
+__host__ __device__ constexpr size_t i8_smem(int stages, int astages) {
+  return (size_t)stages * kStageBytes + (size_t)astages * kATile * 8 + 1024;
+}
 
 __constant__ BmTables c_bm_i8;
 
@@ -224,7 +245,7 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
 
 // GEN generator warps (16; 12 for clusters of 8 CTAs, where each CTA draws 1/8 of the tile: measured
 // c4 17.0 vs 18.6 ms, every other config within noise or slower)
-template <int GEN>
+template <int GEN, int kI8Stages, int kI8AStages>
 __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
     sketch_i8_kernel(const __grid_constant__ CUtensorMap tma_a, const double* __restrict__ a, long long lda,
                      long long m_local, long long m_global, long long row0, int l, int n, uint64_t seed,
@@ -597,6 +618,28 @@ bool sketch_i8_ok(const double* a, long long lda, long long m_global, long long 
 }
 
 namespace {
+// the kernel instance, block size and dynamic smem for clusters of C CTAs
+struct I8Launch {
+  void (*kern)(CUtensorMap, const double*, long long, long long, long long, long long, int, int, uint64_t, long long,
+               double*, int, int, int, DevStatus*);
+  int warps;
+  size_t smem;
+};
+I8Launch i8_launch(int C) {
+  if (C >= 8)
+    return {sketch_i8_kernel<12, CQR_I8_S8, CQR_I8_AS8>, 2 + kI8Slice + 12 + kI8Scan, i8_smem(CQR_I8_S8, CQR_I8_AS8)};
+  if (C >= 4)
+    return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S4, CQR_I8_AS4>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
+            i8_smem(CQR_I8_S4, CQR_I8_AS4)};
+  if (C >= 2)
+    return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S2, CQR_I8_AS2>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
+            i8_smem(CQR_I8_S2, CQR_I8_AS2)};
+  return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S1, CQR_I8_AS1>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
+          i8_smem(CQR_I8_S1, CQR_I8_AS1)};
+}
+}  // namespace
+
+namespace {
 // concurrent clusters of C sketch CTAs on this device (cached per (device, C))
 long long max_active_clusters(int C, int num_sms) {
   static std::mutex mu;
@@ -606,14 +649,15 @@ long long max_active_clusters(int C, int num_sms) {
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find({dev, C});
   if (it != cache.end()) return it->second;
-  auto kern = C >= 8 ? sketch_i8_kernel<12> : sketch_i8_kernel<CQR_I8_GEN>;
-  const int warps = 2 + kI8Slice + (C >= 8 ? 12 : CQR_I8_GEN) + kI8Scan;
+  const I8Launch L = i8_launch(C);
+  auto kern = L.kern;
+  const int warps = L.warps;
   long long v = std::max(1, num_sms / C);
   int nc = 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(1, 1, (unsigned)C);
   cfg.blockDim = dim3(warps * 32, 1, 1);
-  cfg.dynamicSmemBytes = kI8Smem;
+  cfg.dynamicSmemBytes = L.smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
@@ -678,14 +722,15 @@ cudaError_t launch_sketch_i8(const SketchPlan& p, const double* a, long long lda
   if (!make_tmap_2d(&tm, a, p.n, p.m_local, lda, kI8Cols, kI8K, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   const int ncta = p.np / kI8Cols;
-  auto kern = ncta >= 8 ? sketch_i8_kernel<12> : sketch_i8_kernel<CQR_I8_GEN>;
-  const int warps = 2 + kI8Slice + (ncta >= 8 ? 12 : CQR_I8_GEN) + kI8Scan;
+  const I8Launch L = i8_launch(ncta);
+  auto kern = L.kern;
+  const int warps = L.warps;
   e = allow_max_smem(kern);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.s_tiles, (unsigned)(y1 - y0), (unsigned)(p.np / kI8Cols));
   cfg.blockDim = dim3(warps * 32, 1, 1);
-  cfg.dynamicSmemBytes = kI8Smem;
+  cfg.dynamicSmemBytes = L.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;  // the column tiles share their Omega draws
