@@ -259,14 +259,15 @@ cudaEvent_t next_event(cqr_ctx* c) {
 struct StageScope {
   cqr_ctx* c;
   StageEv ev;
-  StageScope(cqr_ctx* c_, int stage) : c(c_) {
+  cudaStream_t strm;
+  StageScope(cqr_ctx* c_, int stage, cudaStream_t on = nullptr) : c(c_), strm(on ? on : c_->stream) {
     ev.stage = stage;
     ev.a = next_event(c);
     ev.b = next_event(c);
-    ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
+    ck(cudaEventRecord(ev.a, strm), "cudaEventRecord");
   }
   ~StageScope() {
-    cudaEventRecord(ev.b, c->stream);
+    cudaEventRecord(ev.b, strm);
     c->stage_evs.push_back(ev);
   }
 };
@@ -931,10 +932,16 @@ Outcome run_precond(Job& j) {
     for (auto& s : pass.stages) o.rep.stages.push_back(s);
     double* r = dbuf<double>(c, B_R, (size_t)n * n);
     double* sgn = dbuf<double>(c, B_SGN, (size_t)n);
+    cudaEvent_t ev_r = nullptr;
     if (!r_less) {
+      // (a side stream for this step measured no better: the last solve's persistent CTAs hold every SM)
       StageScope t(c, CQR_STAGE_RECOVER);
       LAUNCH(c, cqr::launch_triangular_product(rh, rt, n, r, c->status, c->stream));
       LAUNCH(c, cqr::launch_normalize_sign(r, n, sgn, c->status, c->stream));
+    }
+    if (!r_less && j.want_r) {
+      ev_r = next_event(c);
+      ck(cudaEventRecord(ev_r, c->stream), "record R");  // R is final: its copy overlaps the last solve
     }
     double* pack2 = dbuf<double>(c, B_PACK2, cqr::trisolve_pack_doubles(n));
     {
@@ -951,9 +958,7 @@ Outcome run_precond(Job& j) {
         c->r_pin_n = (size_t)n * n;
       }
       if (!c->cstream) ck(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking), "copy stream");
-      cudaEvent_t e = next_event(c);
-      ck(cudaEventRecord(e, c->stream), "record");  // after normalize_sign (recover) and the pack
-      ck(cudaStreamWaitEvent(c->cstream, e, 0), "wait R");
+      ck(cudaStreamWaitEvent(c->cstream, ev_r, 0), "wait R");
       ck(cudaMemcpyAsync(c->r_pin, r, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->cstream), "R D2H");
       j.r_copied = true;
     }
