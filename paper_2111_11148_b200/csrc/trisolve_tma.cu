@@ -477,13 +477,16 @@ bool trisolve_tma_eligible(const TrisolveArgs& a, int np) {
 #ifndef CQR_TRI256_TMW
 #define CQR_TRI256_TMW 4
 #endif
+#ifndef CQR_TRI64_TMW
+#define CQR_TRI64_TMW 0
+#endif
 #ifndef CQR_TRI64_WPC
 #define CQR_TRI64_WPC 12
 #endif
 cudaError_t launch_trisolve_tma(const TrisolveArgs& a, int np, cudaStream_t s) {
   switch (np) {
     case 32: return launch_t<32, 16, true>(a, s);
-    case 64: return launch_t<64, CQR_TRI64_WPC, true>(a, s);
+    case 64: return launch_t<64, CQR_TRI64_WPC, true, CQR_TRI64_TMW>(a, s);
     case 128: return launch_t<128, CQR_TRI128_WPC, CQR_TRI128_BSMEM, CQR_TRI128_TMW>(a, s);
     case 256: return launch_t<256, CQR_TRI256_WPC, false, CQR_TRI256_TMW>(a, s);
     case 512: return launch_t<512, CQR_TRI512_WPC, false>(a, s);
