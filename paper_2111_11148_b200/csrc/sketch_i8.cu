@@ -251,7 +251,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
                      long long m_local, long long m_global, long long row0, int l, int n, uint64_t seed,
                      long long rows_per_chunk, double* __restrict__ partial, int lp, int np_total, int y0,
                      DevStatus* st) {
-  static_assert(kI8Slice == 4, "the four slicer warps are the epilogue (one TMEM lane quadrant each)");
+  static_assert(kI8Slice == 4 || kI8Slice == 8, "warps 2-5 (the first four slicers) are the epilogue");
   constexpr int NTHR = (2 + kI8Slice + GEN + kI8Scan) * 32;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ BmTables T;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
       mbar_init(&aempty[s], kI8Slice * 32);
     }
     mbar_init(&subdone, 1);
-    mbar_init(&tfree, kI8Slice * 32);
+    mbar_init(&tfree, 4 * 32);  // the four epilogue warps
     for (int s = 0; s < kExpSlots; ++s) mbar_init(&expfull[s], 32);
     drained = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -361,8 +361,9 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
     const int j = st_id & 63;                    // this thread's column (units st_id + 128 uu)
     const int quad = warp & 3;
     const int i = 32 * quad + lane;
+    const bool epi = warp < 6;  // warps 2-5: TMEM lane quadrants 2, 3, 0, 1
     double* out = partial + ((long long)ky * lp + s0 + i) * np_total + col0;
-    if (nsteps == 0) {  // an empty chunk: no MMA initialised the accumulators
+    if (nsteps == 0 && epi) {  // an empty chunk: no MMA initialised the accumulators
       for (int c = 0; c < kI8Cols; ++c) out[c] = 0.0;
     }
     double f1 = 0.0, f2 = 0.0;
@@ -399,7 +400,10 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
       fence_async_shared();  // generic-proxy stores -> visible to the tensor core (async proxy)
       mbar_arrive(&full[s]);
       mbar_arrive(&aempty[sa]);
-      if (stp + 1 == t_end || stp + 1 == nsteps) {
+      if ((stp + 1 == t_end || stp + 1 == nsteps) && !epi) {
+        ++t;
+        t_end += sub_steps(t);
+      } else if (stp + 1 == t_end || stp + 1 == nsteps) {
         // ---- epilogue of sub-chunk t: sum_u ACC_u 2^(8(6-u)) in 64-bit integers, scaled, into the partial
         mbar_wait_sleep(&subdone, t & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -531,7 +535,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
       const int b1 = min(nsteps, b0 + sub_steps(t));
       const long long kend = min(k_end, k_begin + 32LL * b1);
       if (t >= kExpSlots) {  // slot t % 4 is free once the epilogue has drained sub-chunk t - 4
-        while (*(volatile int*)&drained < kI8Slice * 32 * (t - kExpSlots + 1)) __nanosleep(200);
+        while (*(volatile int*)&drained < 4 * 32 * (t - kExpSlots + 1)) __nanosleep(200);
       }
       unsigned m0 = 0, m1 = 0;
 #ifdef CQR_I8_NOSCAN  // probe: no scan (bound 2^1: right for |a| < 2 only)
