@@ -931,6 +931,19 @@ constexpr int kQrT = 512;
 // global memory (Vg: kQrB columns of ld l, Tg: kQrB x kQrB); qr_trail_kernel applies A2 -= V (T^T
 // (V^T A2)) with one CTA per 8-column strip and qr_out_kernel writes the sign-normalised R. Same
 // operations in the same order per element as the one-CTA kernel.
+// W (column-major, ld l) = A1 (l x n, row-major), 32 x 32 tiles through shared memory over many CTAs
+__global__ void transpose_kernel(const double* __restrict__ a, int l, int n, double* __restrict__ w,
+                                 const DevStatus* st) {
+  __shared__ double t[32][33];
+  if (failed(st)) return;
+  const int i0 = blockIdx.y * 32, c0 = blockIdx.x * 32, tx = threadIdx.x, ty = threadIdx.y;
+  for (int u = ty; u < 32; u += 8)
+    if (i0 + u < l && c0 + tx < n) t[u][tx] = a[(long long)(i0 + u) * n + c0 + tx];
+  __syncthreads();
+  for (int u = ty; u < 32; u += 8)
+    if (c0 + u < n && i0 + tx < l) w[(long long)(c0 + u) * l + i0 + tx] = t[tx][u];
+}
+
 template <bool SPLIT = false>
 __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restrict__ a1, int l, int n,
                                                          double* __restrict__ r, double* W, DevStatus* st,
@@ -947,7 +960,7 @@ __global__ void __launch_bounds__(kQrT) qr_blocked_kernel(const double* __restri
   double* Pn = smem;                 // kQrB columns of (l - j0) rows
   double* Ys = smem + kQrB * ldr;    // kQrB x n (row stride n + 4): V^T A2, then T^T V^T A2
   const int ldy = n + 4;
-  if (!SPLIT || j0s == 0) {
+  if (!SPLIT) {  // (SPLIT: transpose_kernel has written W)
     for (long long e = tid; e < (long long)l * n; e += nt) {
       const int i = (int)(e / n), c = (int)(e % n);
       W[(long long)c * l + i] = a1[e];
@@ -1632,6 +1645,7 @@ cudaError_t launch_qr_r(const double* a1, int l, int n, double* r, double* work,
     if (e != cudaSuccess) return e;
     double* Vg = work + (size_t)l * n;  // kQrB x l, then Tg (kQrB x kQrB): qr_work_doubles
     double* Tg = Vg + (size_t)kQrB * l;
+    transpose_kernel<<<dim3((n + 31) / 32, (l + 31) / 32), dim3(32, 8), 0, s>>>(a1, l, n, work, st);
     for (int j0 = 0; j0 < n; j0 += kQrB) {
       qr_blocked_kernel<true><<<1, kQrT, bsmem, s>>>(a1, l, n, r, work, st, j0, Vg, Tg);
       const int b = min(kQrB, n - j0), c1 = j0 + b;
