@@ -296,6 +296,17 @@ def test_sketch_gaussian_tolerance(m, n, l, seed):
                                                  seed).a1)  # deterministic
 
 
+def test_sketch_gaussian_long_subchunks():
+    """A k-chunk long enough for every sub-chunk size of the int8 kernel (16, 64, 256, then 512-step sub-chunks
+    at the exactness cap, and a short last one): 4.2e6 rows over 148 one-CTA chunks, ~28k rows each."""
+    m, n, l, seed = 4_200_000, 40, 80, 17
+    a = o.gaussian_matrix(m, n, seed + 1)
+    a[123_457, 7] = 1e3   # one large entry deep inside a chunk: its sub-chunk's exponent bound, not the others'
+    ref = o.sketch_gaussian(a, l, seed)
+    got = G.sketch_gaussian(a, G.SketchConfig(strategy=G.Strategy.Gaussian, size=l), seed).a1
+    assert relf(got, ref) <= 1e-13
+
+
 def test_uniform_gather_bitwise():
     a = o.gaussian_matrix(1000, 10, 2)
     for wr in (False, True):
