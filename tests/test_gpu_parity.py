@@ -447,6 +447,11 @@ def test_r_less_and_non_finite():
     for meth in (_abi.CHOLQR2, _abi.SCHOLQR3, _abi.RQR_GAUSSIAN, _abi.RLU, _abi.RQR):
         with pytest.raises(ValueError):
             G._factor(meth, c, G.SketchConfig(seed=3), _abi.options())
+    # the int8 sketch's scanner warps check every sub-chunk: a NaN late in a long k-chunk
+    d = o.gaussian_matrix(900_000, 24, 5)
+    d[899_000, 20] = np.nan
+    with pytest.raises(ValueError):
+        G._factor(_abi.RQR_GAUSSIAN, d, G.SketchConfig(seed=3), _abi.options())
 
 
 def test_invalid_arguments_match_reference():
