@@ -310,6 +310,14 @@ constexpr int kGtMma = 12;
 #ifndef CQR_GRAM_CH256
 #define CQR_GRAM_CH256 32  // rows per ring stage at n in (128, 256] (16 rows: 2.32 vs 2.30 ms)
 #endif
+#ifndef CQR_GRAM256_PARTS
+#define CQR_GRAM256_PARTS 3
+#define CQR_GRAM256_MAXT 4
+#endif
+#ifndef CQR_GRAM512_PARTS
+#define CQR_GRAM512_PARTS 11
+#define CQR_GRAM512_MAXT 4
+#endif
 #ifndef CQR_GRAM_CH64
 #define CQR_GRAM_CH64 32
 #endif
@@ -623,7 +631,7 @@ GramPlan gram_plan(long long m, int n, bool tma_ok) {
     p.tma = 1;
     p.persistent = 1;
     p.wpc = kGtMma;
-    p.parts = p.np == 128 ? 1 : p.np == 256 ? 3 : 11;  // 36 / 136 / 528 macros: 3, 4, 4 per warp (13 warps: 128 regs)
+    p.parts = p.np == 128 ? 1 : p.np == 256 ? CQR_GRAM256_PARTS : CQR_GRAM512_PARTS;  // 36 / 136 / 528 macros: 3, 4, 4 per warp (13 warps: 128 regs)
     p.maxt = (macros + p.wpc * p.parts - 1) / (p.wpc * p.parts);
     p.ch = p.np == 512 ? 16 : p.np == 128 ? CQR_GRAM_CH128 : CQR_GRAM_CH256;
   } else if (p.np == 128 && !legacy) {  // persistent: the 36 macro tiles divide evenly over 12 warps (measured: n = 64 is faster per leaf)
@@ -668,8 +676,8 @@ cudaError_t launch_gram_leaves(const GramPlan& p, const double* x, long long ldx
       return launch_leaves_tma<128, 1, CQR_GRAM_CH128>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     if (p.np == 128)
       return launch_leaves_tma<128, 3, CQR_GRAM_CH128>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
-    if (p.np == 256) return launch_leaves_tma<256, 4, CQR_GRAM_CH256>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
-    if (p.np == 512) return launch_leaves_tma<512, 4, 16>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 256) return launch_leaves_tma<256, CQR_GRAM256_MAXT, CQR_GRAM_CH256>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
+    if (p.np == 512) return launch_leaves_tma<512, CQR_GRAM512_MAXT, 16>(p, x, ldx, tiles, partial, check, st, s, leaf0, leaf1, num_sms);
     return cudaErrorInvalidValue;
   }
   static const bool no64 = std::getenv("CQR_GRAM_NO64") != nullptr;  // A/B: the 16 x 16 tiling at n <= 64
