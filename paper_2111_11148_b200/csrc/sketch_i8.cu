@@ -75,6 +75,9 @@ constexpr int kI8K = 32;          // rows of A per step (MMA K for kind::i8)
 #ifndef CQR_I8_GEN
 #define CQR_I8_GEN 16
 #endif
+#ifndef CQR_I8_GEN8
+#define CQR_I8_GEN8 12  // generator warps for clusters of 8 (c4: 12 vs 16 warps 17.0 vs 18.6 ms)
+#endif
 #ifndef CQR_I8_SLEEP_NS
 #define CQR_I8_SLEEP_NS 100
 #endif
@@ -631,7 +634,8 @@ struct I8Launch {
 };
 I8Launch i8_launch(int C) {
   if (C >= 8)
-    return {sketch_i8_kernel<12, CQR_I8_S8, CQR_I8_AS8>, 2 + kI8Slice + 12 + kI8Scan, i8_smem(CQR_I8_S8, CQR_I8_AS8)};
+    return {sketch_i8_kernel<CQR_I8_GEN8, CQR_I8_S8, CQR_I8_AS8>, 2 + kI8Slice + CQR_I8_GEN8 + kI8Scan,
+            i8_smem(CQR_I8_S8, CQR_I8_AS8)};
   if (C >= 4)
     return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S4, CQR_I8_AS4>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
             i8_smem(CQR_I8_S4, CQR_I8_AS4)};
