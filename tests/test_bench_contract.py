@@ -39,7 +39,11 @@ def test_our_arm_line():
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     assert d["dtype"] == "f64" and d["higher_is_better"] is True
     r = d["roofline"]
-    assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] <= 1 and r["peak"] > 0
+    assert r["bound"] in ("hbm", "tensor") and r["frac"] > 0 and r["peak"] > 0
+    # The sketch's FP64-equivalent rate is counted against the FP64 (DMMA) roof north_star names, but the exact
+    # product runs on the int8 tensor cores: it may pass the DMMA peak, and then the line must also carry the
+    # roof of the unit it really runs on, which bounds it.
+    assert r["frac"] <= 1 or 0 < r["int8_emulation"]["frac"] <= 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
