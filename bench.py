@@ -203,8 +203,10 @@ def shard(m_global, world, rank):
     return lo, hi - lo
 
 
-def workload_shape(name, world, rank):
+def workload_shape(name, world, rank, rows_override=None):
     mname, rows, weak, n, l, kap, desc = WORKLOADS[name]
+    if rows_override:
+        rows, desc = rows_override, desc + f" [--rows {rows_override}: a flow check, not the workload]"
     m_global = rows * world if weak else rows
     row0, m_local = shard(m_global, world, rank)
     return mname, m_global, row0, m_local, n, l, kap, desc, weak
@@ -234,12 +236,24 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    host_tr = args.transport == "host" and world > 1
+    if host_tr:
+        # ranks share the visible GPUs round-robin; the exchange steps go through pinned host buffers
+        # and gloo (dist.HostTransport). No kernel waits on another rank, so this is safe on one GPU;
+        # it validates the N-rank flow, its timings are not scaling numbers.
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        td.init_process_group("nccl", device_id=dev)
-    ctx = dist.make_context(local, rank, world)
-    mname, m_global, row0, m_local, n, l_req, kap, wdesc, weak = workload_shape(args.workload, world, rank)
+    rdev = torch.device("cpu") if host_tr else dev  # where the max-over-ranks scalars live
+    if host_tr:
+        td.init_process_group("gloo")
+        ctx = cq.Context(local)
+        dist.attach_host_transport(ctx)
+    else:
+        if world > 1:
+            td.init_process_group("nccl", device_id=dev)
+        ctx = dist.make_context(local, rank, world)
+    mname, m_global, row0, m_local, n, l_req, kap, wdesc, weak = workload_shape(args.workload, world, rank, args.rows)
     method = {v: k for k, v in _abi.METHOD_NAMES.items()}[mname]
     a = cq.synthesize_dev(m_local, n, seed=SEED, sigma=workload_sigma(n, kap), m_global=m_global, row0=row0,
                           ctx=ctx)
@@ -277,7 +291,7 @@ def run_ours(args):
     if world > 1:
         td.barrier()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    t = torch.tensor([ms], device=rdev, dtype=torch.float64)
     if world > 1:
         td.all_reduce(t, op=td.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
@@ -312,7 +326,7 @@ def run_ours(args):
     for _ in range(ke):
         e2e_step()
     torch.cuda.synchronize(dev)
-    te = torch.tensor([(time.perf_counter() - t0) / ke], device=dev, dtype=torch.float64)
+    te = torch.tensor([(time.perf_counter() - t0) / ke], device=rdev, dtype=torch.float64)
     if world > 1:
         td.all_reduce(te, op=td.ReduceOp.MAX)
     te = float(te.item())
@@ -371,7 +385,7 @@ def run_ours(args):
 
     comparison = None
     if args.workload == "c1" and not args.no_compare:
-        comparison = compare_methods(ctx, a, m_global, row0, n, args, stream, dev, world)
+        comparison = compare_methods(ctx, a, m_global, row0, n, args, stream, dev, world, rdev)
 
     cpu = None
     if not args.no_cpu:
@@ -387,7 +401,9 @@ def run_ours(args):
             "config": {"workload": wdesc, "method": mname, "sketch": "gaussian", "m_global": m_global,
                        "m_per_gpu": m_local if weak else None, "n": n, "l": l, "kappa": kap,
                        "l2": f"inputs larger than L2 ({8 * m_local * n / 1e9:.2f} GB per GPU vs 126 MB L2), no flush",
-                       "parallelism": f"row-block dp{world}" + ("" if weak else " (strong: fixed m, ceil(b*m/p) blocks)")},
+                       "parallelism": f"row-block dp{world}" + ("" if weak else " (strong: fixed m, ceil(b*m/p) blocks)"),
+                       "transport": ("host (gloo + pinned staging; ranks may share a GPU: a flow check, not a "
+                                     "scaling number)" if host_tr else "nccl" if world > 1 else None)},
             "stage_ms": stage_avg, "clocks": clk.summary(), "gpu_launches": launches,
             "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu, "e2e": e2e,
             "comparison": comparison,
@@ -398,7 +414,7 @@ def run_ours(args):
         td.destroy_process_group()
 
 
-def compare_methods(ctx, a, m_global, row0, n, args, stream, dev, world):
+def compare_methods(ctx, a, m_global, row0, n, args, stream, dev, world, rdev=None):
     """BASELINE.json configs[1]: CholeskyQR2 and shifted CholeskyQR3 (fixed shift 1e-15,
     experiments.hpp:52) on the same A. CholeskyQR2 breaks down at cond 1e14 (its time is
     the time to the breakdown verdict)."""
@@ -433,7 +449,7 @@ def compare_methods(ctx, a, m_global, row0, n, args, stream, dev, world):
             one()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        t = torch.tensor([e0.elapsed_time(e1) / k], device=dev, dtype=torch.float64)
+        t = torch.tensor([e0.elapsed_time(e1) / k], device=rdev or dev, dtype=torch.float64)
         if world > 1:
             td.all_reduce(t, op=td.ReduceOp.MAX)
         ms = float(t.item())
@@ -536,6 +552,9 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-compare", action="store_true", help="skip the CholeskyQR2 / sCholeskyQR3 arms (c1)")
     ap.add_argument("--dry-run", action="store_true", help="print the multi-GPU launch command and exit")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="N > 1: NCCL (one rank per GPU) or the host transport over gloo (ranks may share a GPU)")
+    ap.add_argument("--rows", type=int, default=None, help="override the workload's row count (flow checks only)")
     ap.add_argument("--workload", default="c1", choices=sorted(WORKLOADS),
                     help="BASELINE.json config (c1, the benchmark line, by default)")
     args = ap.parse_args(argv)

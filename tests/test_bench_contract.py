@@ -51,6 +51,28 @@ def test_our_arm_line():
     assert d["check"]["orth"] < 1e-10
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload,rows", [("c2", 300_001), ("c1", 150_000)])
+def test_n_rank_flow_on_one_gpu(workload, rows):
+    """bench.py --gpus 2 end to end (launcher, shards, sharded factorization and e2e, max over ranks, one
+    line from rank 0) with the ranks sharing this GPU over the host transport; NCCL needs one GPU per rank."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--transport", "host",
+                          "--workload", workload, "--rows", str(rows), "--steps", "2", "--warmup", "3", "--no-cpu"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= d.keys() and d["n_gpus"] == 2 and d["value"] > 0
+    weak = workload == "c1"
+    assert d["scaling"] == ("weak" if weak else "strong")
+    assert d["config"]["m_global"] == (2 * rows if weak else rows)
+    assert d["check"]["orth"] < 1e-10 and d["check"]["res"] < 1e-12
+    assert d["e2e"]["value"] > 0 and "cqr_factor_sharded" in d["e2e"]["api"]
+    assert d["config"]["transport"].startswith("host")
+
+
 def test_multi_gpu_launcher_dry_run():
     """--gpus N without WORLD_SIZE re-launches under torch.distributed.run, one rank per GPU."""
     env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
