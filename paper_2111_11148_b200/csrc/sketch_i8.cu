@@ -48,8 +48,14 @@ constexpr int kI8K = 32;          // rows of A per step (MMA K for kind::i8)
 // ring depths per cluster size C (digit-plane stages S, FP64 A stages AS; S >= generator teams, smem
 // S 42 KB + AS 16 KB <= 218 KB): C = 1 (c3) S 3 AS 4: 2.65 vs 2.70 ms (S 4 AS 2); C = 2 (c1) S 4 AS 3: 1.77 vs 1.80;
 // C = 4, 8 (c2, c4) S 4 AS 3: 23.79 / 16.32 vs 23.98 / 16.40 ms (AS 2)
+// r04: the Omega planes (28 KB per stage) and A's digit planes (14 KB) are separate rings of S and P stages: a
+// generator team owns every teams-th step, and with S = teams its next step had to wait for the MMAs of its
+// previous one (ncu: 35% of the generators' samples at c1 sat in that wait); S > teams gives a step of slack.
 #ifndef CQR_I8_S1
 #define CQR_I8_S1 3
+#endif
+#ifndef CQR_I8_P1
+#define CQR_I8_P1 3
 #endif
 #ifndef CQR_I8_AS1
 #define CQR_I8_AS1 4
@@ -57,17 +63,26 @@ constexpr int kI8K = 32;          // rows of A per step (MMA K for kind::i8)
 #ifndef CQR_I8_S2
 #define CQR_I8_S2 4
 #endif
+#ifndef CQR_I8_P2
+#define CQR_I8_P2 4
+#endif
 #ifndef CQR_I8_AS2
 #define CQR_I8_AS2 3
 #endif
 #ifndef CQR_I8_S4
 #define CQR_I8_S4 4
 #endif
+#ifndef CQR_I8_P4
+#define CQR_I8_P4 4
+#endif
 #ifndef CQR_I8_AS4
 #define CQR_I8_AS4 3
 #endif
 #ifndef CQR_I8_S8
 #define CQR_I8_S8 4
+#endif
+#ifndef CQR_I8_P8
+#define CQR_I8_P8 4
 #endif
 #ifndef CQR_I8_AS8
 #define CQR_I8_AS8 3
@@ -89,10 +104,11 @@ constexpr long long kI8MaxChunk = 16384;  // rows per k-chunk: 7 * 128^2 * 16384
 constexpr int kDig = 7;                 // byte digits per operand
 constexpr int kOmPlane = kI8Rows * kI8K;  // bytes per Omega digit plane (4 KB)
 constexpr int kAPlane = kI8Cols * kI8K;   // bytes per A digit plane (2 KB)
-constexpr int kStageBytes = kDig * (kOmPlane + kAPlane);
+constexpr int kOmStage = kDig * kOmPlane;  // 28 KB
+constexpr int kApStage = kDig * kAPlane;   // 14 KB
 constexpr int kATile = kI8K * kI8Cols;    // doubles per FP64 A stage
-__host__ __device__ constexpr size_t i8_smem(int stages, int astages) {
-  return (size_t)stages * kStageBytes + (size_t)astages * kATile * 8 + 1024;
+__host__ __device__ constexpr size_t i8_smem(int stages, int pstages, int astages) {
+  return (size_t)stages * kOmStage + (size_t)pstages * kApStage + (size_t)astages * kATile * 8 + 1024;
 }
 
 __constant__ BmTables c_bm_i8;
@@ -248,7 +264,7 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
 
 // GEN generator warps (16; 12 for clusters of 8 CTAs, where each CTA draws 1/8 of the tile: measured
 // c4 17.0 vs 18.6 ms, every other config within noise or slower)
-template <int GEN, int kI8Stages, int kI8AStages>
+template <int GEN, int kI8Stages, int kI8PStages, int kI8AStages>
 __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
     sketch_i8_kernel(const __grid_constant__ CUtensorMap tma_a, const double* __restrict__ a, long long lda,
                      long long m_local, long long m_global, long long row0, int l, int n, uint64_t seed,
@@ -259,6 +275,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ BmTables T;
   __shared__ __align__(8) uint64_t full[kI8Stages], empty[kI8Stages], afull[kI8AStages], aempty[kI8AStages];
+  __shared__ __align__(8) uint64_t pfull[kI8PStages], pempty[kI8PStages];
   __shared__ __align__(8) uint64_t subdone, tfree, expfull[kExpSlots];
   __shared__ uint32_t tmem_base;
   __shared__ int sexp[kExpSlots][kI8Cols];
@@ -267,8 +284,8 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
   if (failed(st)) return;
   unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sOm = sm;                                    // [stage][plane][4 KB]
-  unsigned char* sAp = sm + kI8Stages * kDig * kOmPlane;      // [stage][plane][2 KB]
-  double* sAf = reinterpret_cast<double*>(sm + kI8Stages * kStageBytes);  // [astage][32 x 64]
+  unsigned char* sAp = sm + kI8Stages * kOmStage;             // [pstage][plane][2 KB]
+  double* sAf = reinterpret_cast<double*>(sm + kI8Stages * kOmStage + kI8PStages * kApStage);  // [astage][32 x 64]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s0 = blockIdx.x * kI8Rows;
   const int ky = blockIdx.y + y0;
@@ -286,9 +303,13 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
   }
   if (tid == 0) {
     for (int s = 0; s < kI8Stages; ++s) {
-      // one generator team and the slicers; the partners' Omega rows arrive as bulk-copy bytes (expect_tx)
-      mbar_init(&full[s], GEN * 32 / gen_teams(ncta) + kI8Slice * 32);
+      // one generator team; the partners' Omega rows arrive as bulk-copy bytes (expect_tx)
+      mbar_init(&full[s], GEN * 32 / gen_teams(ncta));
       mbar_init(&empty[s], ncta);                              // every CTA's MMAs have read the stage
+    }
+    for (int s = 0; s < kI8PStages; ++s) {
+      mbar_init(&pfull[s], kI8Slice * 32);  // the slicers
+      mbar_init(&pempty[s], 1);             // this CTA's MMAs have read A's digit planes
     }
     for (int s = 0; s < kI8AStages; ++s) {
       mbar_init(&afull[s], 1);
@@ -316,12 +337,13 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
     if (lane == 0) {
       int t = 0, t_end = sub_steps(0);  // current sub-chunk and its end step
       for (int stp = 0; stp < nsteps; ++stp) {
-        const int s = stp % kI8Stages;
+        const int s = stp % kI8Stages, sp = stp % kI8PStages;
         const bool first = stp == t_end - sub_steps(t);
         if (first && t > 0) mbar_wait(&tfree, (t - 1) & 1);  // the epilogue has drained sub-chunk t-1
+        mbar_wait(&pfull[sp], (stp / kI8PStages) & 1);
         mbar_wait(&full[s], (stp / kI8Stages) & 1);  // partners' bulk copies included
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t om = smem_u32(sOm + s * kDig * kOmPlane), ap = smem_u32(sAp + s * kDig * kAPlane);
+        const uint32_t om = smem_u32(sOm + s * kOmStage), ap = smem_u32(sAp + sp * kApStage);
 #ifndef CQR_I8_NOMMA  // probe: the producers' bound (no MMAs)
         // Omega digit sd against the stacked A digit planes 0 .. 6-sd (consecutive 2 KB planes = one taller
         // K-major B operand): its N = 64 (7 - sd) output columns land on TMEM levels sd .. 6, i.e. on
@@ -339,6 +361,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
 #endif
         // the stage's smem (in every CTA of the cluster) may be rewritten once every CTA's MMAs have read it
         umma_commit_cluster(&empty[s], (uint16_t)((1u << ncta) - 1u));
+        umma_commit(&pempty[sp]);
         if (stp + 1 == t_end || stp + 1 == nsteps) {  // sub-chunk t complete in TMEM -> the epilogue
           umma_commit(&subdone);
           ++t;
@@ -372,7 +395,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
     double f1 = 0.0, f2 = 0.0;
     int t = 0, t_end = sub_steps(0);
     for (int stp = 0; stp < nsteps; ++stp) {
-      const int s = stp % kI8Stages, sa = stp % kI8AStages;
+      const int s = stp % kI8PStages, sa = stp % kI8AStages;
       if (stp == t_end - sub_steps(t)) {  // a sub-chunk's first step: its exponent bound for column j
         mbar_wait_sleep(&expfull[t % kExpSlots], (t / kExpSlots) & 1);
         // a 2^(54 - E_j) as two exact power-of-two scalings (54 - E_j may exceed the double range)
@@ -381,10 +404,10 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
         f2 = ldexp(1.0, sh - sh1);
       }
       mbar_wait_sleep(&afull[sa], (stp / kI8AStages) & 1);
-      mbar_wait_sleep(&empty[s], ((stp / kI8Stages) & 1) ^ 1);
+      mbar_wait_sleep(&pempty[s], ((stp / kI8PStages) & 1) ^ 1);
       const long long kb = k_begin + (long long)stp * kI8K;
       const double* At = sAf + sa * kATile;
-      unsigned char* planes = sAp + s * kDig * kAPlane;
+      unsigned char* planes = sAp + s * kApStage;
 #ifndef CQR_I8_NOSLICE  // probe: without the A slicing
 #pragma unroll
       for (int uu = 0; uu < SUPT; ++uu) {
@@ -401,7 +424,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
       }
 #endif
       fence_async_shared();  // generic-proxy stores -> visible to the tensor core (async proxy)
-      mbar_arrive(&full[s]);
+      mbar_arrive(&pfull[s]);
       mbar_arrive(&aempty[sa]);
       if ((stp + 1 == t_end || stp + 1 == nsteps) && !epi) {
         ++t;
@@ -474,7 +497,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
     for (int stp = team; stp < nsteps; stp += teams) {
       const int s = stp % kI8Stages;
       mbar_wait_sleep(&empty[s], ((stp / kI8Stages) & 1) ^ 1);  // every CTA's MMAs are done with stage s
-      unsigned char* planes = sOm + s * kDig * kOmPlane;
+      unsigned char* planes = sOm + s * kOmStage;
 #pragma unroll 1
       for (int uu = 0; uu < upt; ++uu) {
         const int u = u_lo + gt + tsize * uu;
@@ -634,16 +657,16 @@ struct I8Launch {
 };
 I8Launch i8_launch(int C) {
   if (C >= 8)
-    return {sketch_i8_kernel<CQR_I8_GEN8, CQR_I8_S8, CQR_I8_AS8>, 2 + kI8Slice + CQR_I8_GEN8 + kI8Scan,
-            i8_smem(CQR_I8_S8, CQR_I8_AS8)};
+    return {sketch_i8_kernel<CQR_I8_GEN8, CQR_I8_S8, CQR_I8_P8, CQR_I8_AS8>, 2 + kI8Slice + CQR_I8_GEN8 + kI8Scan,
+            i8_smem(CQR_I8_S8, CQR_I8_P8, CQR_I8_AS8)};
   if (C >= 4)
-    return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S4, CQR_I8_AS4>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
-            i8_smem(CQR_I8_S4, CQR_I8_AS4)};
+    return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S4, CQR_I8_P4, CQR_I8_AS4>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
+            i8_smem(CQR_I8_S4, CQR_I8_P4, CQR_I8_AS4)};
   if (C >= 2)
-    return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S2, CQR_I8_AS2>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
-            i8_smem(CQR_I8_S2, CQR_I8_AS2)};
-  return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S1, CQR_I8_AS1>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
-          i8_smem(CQR_I8_S1, CQR_I8_AS1)};
+    return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S2, CQR_I8_P2, CQR_I8_AS2>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
+            i8_smem(CQR_I8_S2, CQR_I8_P2, CQR_I8_AS2)};
+  return {sketch_i8_kernel<CQR_I8_GEN, CQR_I8_S1, CQR_I8_P1, CQR_I8_AS1>, 2 + kI8Slice + CQR_I8_GEN + kI8Scan,
+          i8_smem(CQR_I8_S1, CQR_I8_P1, CQR_I8_AS1)};
 }
 }  // namespace
 
