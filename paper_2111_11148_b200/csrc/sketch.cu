@@ -458,8 +458,17 @@ __global__ void sketch_reduce_kernel(const double* __restrict__ partial, int kch
   const int i = (int)(e / n), c = (int)(e - (long long)i * n);
   const double* p = partial + (long long)i * np + c;
   const long long stride = (long long)lp * np;
+  // the sum stays in k order (a fixed order: run-to-run identical); only the loads run ahead, 16 in flight
   double s = 0.0;
-  for (int k = 0; k < kchunks; ++k) s += __ldg(p + k * stride);
+  int k = 0;
+  for (; k + 16 <= kchunks; k += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(p + (k + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s += v[u];
+  }
+  for (; k < kchunks; ++k) s += __ldg(p + k * stride);
   a1[e] = s;
 }
 

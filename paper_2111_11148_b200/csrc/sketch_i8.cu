@@ -52,13 +52,13 @@ constexpr int kI8K = 32;          // rows of A per step (MMA K for kind::i8)
 // generator team owns every teams-th step, and with S = teams its next step had to wait for the MMAs of its
 // previous one (ncu: 35% of the generators' samples at c1 sat in that wait); S > teams gives a step of slack.
 #ifndef CQR_I8_S1
-#define CQR_I8_S1 3
+#define CQR_I8_S1 4
 #endif
 #ifndef CQR_I8_P1
 #define CQR_I8_P1 3
 #endif
 #ifndef CQR_I8_AS1
-#define CQR_I8_AS1 4
+#define CQR_I8_AS1 3
 #endif
 #ifndef CQR_I8_S2
 #define CQR_I8_S2 4
@@ -221,7 +221,7 @@ __device__ __forceinline__ void split64(long long v, uint32_t& lo, uint32_t& hi)
 #define CQR_I8_TEAMS4 4  // clusters of 4/8 (c2/c4): 2 teams 24.6/16.8 ms vs 4 teams 24.0/16.4 (<= 7: bar ids 1..7)
 #endif
 #ifndef CQR_I8_TEAMS1
-#define CQR_I8_TEAMS1 1
+#define CQR_I8_TEAMS1 4  // no cluster (c3): 1/2/4 teams 2.652/2.622/2.614 ms (4 teams: S 4, P 3, AS 3)
 #endif
 __host__ __device__ constexpr int gen_teams(int ncta) {
   return ncta >= 4 ? CQR_I8_TEAMS4 : ncta == 2 ? CQR_I8_TEAMS2 : CQR_I8_TEAMS1;
@@ -515,10 +515,13 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
         gaussian_pairs_z<4>(T, zz, ge, go);
 #endif
         uint32_t lo[8], hi[8];
+        // round(w 2^51): the scaling is exact, the conversion rounds; rows past l draw zeros (a zero factor
+        // instead of 16 selects per unit: c3 2.65 -> 2.60 ms, c1 1.767 -> 1.747)
+        const double lv = live[uu] ? 0x1p51 : 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // round(w 2^51): the scaling is exact, the conversion rounds
-          split64(live[uu] ? __double2ll_rn(ge[q] * 0x1p51) : 0ll, lo[2 * q], hi[2 * q]);
-          split64(live[uu] ? __double2ll_rn(go[q] * 0x1p51) : 0ll, lo[2 * q + 1], hi[2 * q + 1]);
+        for (int q = 0; q < 4; ++q) {
+          split64(__double2ll_rn(ge[q] * lv), lo[2 * q], hi[2 * q]);
+          split64(__double2ll_rn(go[q] * lv), lo[2 * q + 1], hi[2 * q + 1]);
         }
         transpose_store(lo, hi, planes, 256, om_off(i, 8 * o));
       }
