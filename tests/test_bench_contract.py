@@ -46,6 +46,7 @@ def test_our_arm_line():
     assert r["frac"] <= 1 or 0 < r["int8_emulation"]["frac"] <= 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["two_in_flight"]["value"] > 0  # the extra: two blocking calls in flight from two host threads
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
     assert set(d["stage_roofline"]) >= {"sketch", "gram", "trisolve"}
     assert d["check"]["orth"] < 1e-10
