@@ -111,7 +111,7 @@ __host__ __device__ constexpr size_t i8_smem(int stages, int pstages, int astage
   return (size_t)stages * kOmStage + (size_t)pstages * kApStage + (size_t)astages * kATile * 8 + 1024;
 }
 
-__constant__ BmTables c_bm_i8;
+__constant__ BmTablesX c_bm_i8;  // full-circle sine table: no quadrant arithmetic in the draws
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t sbo = 256) {
   // K-major, SWIZZLE_NONE: 8-row x 16-byte core matrices, LBO = 128 B (the two K halves), SBO = the stride
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
   static_assert(kI8Slice == 4 || kI8Slice == 8, "warps 2-5 (the first four slicers) are the epilogue");
   constexpr int NTHR = (2 + kI8Slice + GEN + kI8Scan) * 32;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ BmTables T;
+  __shared__ BmTablesX T;
   __shared__ __align__(8) uint64_t full[kI8Stages], empty[kI8Stages], afull[kI8AStages], aempty[kI8AStages];
   __shared__ __align__(8) uint64_t pfull[kI8PStages], pempty[kI8PStages];
   __shared__ __align__(8) uint64_t subdone, tfree, expfull[kExpSlots];
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
   {
     const double* src = reinterpret_cast<const double*>(&c_bm_i8);
     double* dst = reinterpret_cast<double*>(&T);
-    for (int e = tid; e < (int)(sizeof(BmTables) / sizeof(double)); e += NTHR) dst[e] = src[e];
+    for (int e = tid; e < (int)(sizeof(BmTablesX) / sizeof(double)); e += NTHR) dst[e] = src[e];
   }
   if (tid == 0) {
     for (int s = 0; s < kI8Stages; ++s) {
@@ -634,7 +634,9 @@ cudaError_t ensure_tables_i8(cudaStream_t s) {
   if (dev < 64 && (done >> dev) & 1ull) return cudaSuccess;
   BmTables t;
   bm_tables_host(&t);
-  e = cudaMemcpyToSymbolAsync(c_bm_i8, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
+  static BmTablesX x;  // static: the async copy reads it until the synchronize below (under the mutex)
+  bm_tables_expand(t, &x);
+  e = cudaMemcpyToSymbolAsync(c_bm_i8, &x, sizeof(x), 0, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && dev < 64) done |= 1ull << dev;
   return e;
