@@ -375,8 +375,12 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
       for (int stp = 0; stp < nsteps; ++stp) {
         const int s = stp % kI8AStages;
         mbar_wait_sleep(&aempty[s], ((stp / kI8AStages) & 1) ^ 1);
+#ifdef CQR_I8_NOTMA  // probe: no A loads
+        mbar_arrive(&afull[s]);
+#else
         mbar_expect_tx(&afull[s], kATile * 8);
         tma_load_2d(sAf + s * kATile, &tma_a, col0, (int)(k_begin + (long long)stp * kI8K), &afull[s]);
+#endif
       }
     }
   } else if (warp < 2 + kI8Slice) {
@@ -523,9 +527,13 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
           split64(__double2ll_rn(ge[q] * lv), lo[2 * q], hi[2 * q]);
           split64(__double2ll_rn(go[q] * lv), lo[2 * q + 1], hi[2 * q + 1]);
         }
+#ifndef CQR_I8_NOGENSTORE  // probe: no Omega digit stores
         transpose_store(lo, hi, planes, 256, om_off(i, 8 * o));
+#endif
       }
+#ifndef CQR_I8_NOGENFENCE  // probe: no proxy fence after the digit stores
       fence_async_shared();  // the digit stores -> the tensor core's and the bulk copies' (async) view
+#endif
       if (ncta > 1) {
         // the team's stores are done; its lanes 0 .. C-2 ship this CTA's rows (one contiguous chunk of whole
         // row groups, all planes) to one partner each
