@@ -93,9 +93,11 @@ __device__ __forceinline__ double rsqrt_approx(double x) {
 // Box-Muller on raw counter bits: b1 -> u1 = ((b1 >> 11) + 1) 2^-53, b2 -> u2 =
 // (b2 >> 11) 2^-53; g_even = r cos(a), g_odd = r sin(a). The pairs are independent;
 // every step is issued for all P of them before the next one (P-way ILP).
-template <int P, class TT>
+// SCALED: the outputs times `scale`, a power of two (or zero) folded into the radius -- exact, so
+// g * scale is bit for bit the scaled draw (one multiply per pair instead of one per draw).
+template <int P, class TT, bool SCALED = false>
 __device__ __forceinline__ void box_muller_bits(const TT& T, const uint64_t (&b1)[P], const uint64_t (&b2)[P],
-                                                double (&g_even)[P], double (&g_odd)[P]) {
+                                                double (&g_even)[P], double (&g_odd)[P], double scale = 1.0) {
   double n1[P], a[P], fk[P];
   int k[P];
   CQR_BM_EACH {
@@ -162,7 +164,7 @@ __device__ __forceinline__ void box_muller_bits(const TT& T, const uint64_t (&b1
     double s = x[j] * y[j];
     const double hy = __longlong_as_double(__double_as_longlong(y[j]) - (1ll << 52));  // y / 2, y normal
     s = fma(hy, fma(-s, s, x[j]), s);
-    const double rad = __double_as_longlong(x[j]) > 0 ? s : 0.0;
+    const double rad = __double_as_longlong(x[j]) > 0 ? (SCALED ? s * scale : s) : 0.0;
     const double sn = fma(d[j] * d2[j], sp[j], d[j]);
     const double cs = fma(cp[j], d2[j], kBmK[14]);
     double S, C;
@@ -193,6 +195,17 @@ __device__ __forceinline__ void gaussian_pairs_z(const TT& T, const uint64_t (&z
     b2[j] = mix64(z[j] + 0x9E3779B97F4A7C15ull);
   }
   box_muller_bits<P, TT>(T, b1, b2, g_even, g_odd);
+}
+// the same draws times `scale` (a power of two or zero)
+template <int P, class TT>
+__device__ __forceinline__ void gaussian_pairs_z_scaled(const TT& T, const uint64_t (&z)[P], double scale,
+                                                        double (&g_even)[P], double (&g_odd)[P]) {
+  uint64_t b1[P], b2[P];
+  CQR_BM_EACH {
+    b1[j] = mix64(z[j]);
+    b2[j] = mix64(z[j] + 0x9E3779B97F4A7C15ull);
+  }
+  box_muller_bits<P, TT, true>(T, b1, b2, g_even, g_odd, scale);
 }
 #undef CQR_BM_EACH
 

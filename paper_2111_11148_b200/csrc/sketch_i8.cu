@@ -511,21 +511,22 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) zz[q] = z[uu] + (uint64_t)(2 * q) * kGolden;
         z[uu] += (uint64_t)(kI8K * teams) * kGolden;
+        // round(w 2^51): the scaling is exact (folded into the Box-Muller radius: one multiply per pair), the
+        // conversion rounds; rows past l draw zeros (a zero factor instead of 16 selects per unit: c3 2.65 ->
+        // 2.60 ms, c1 1.767 -> 1.747)
+        const double lv = live[uu] ? 0x1p51 : 0.0;
         double ge[4], go[4];
 #ifdef CQR_I8_NOGEN  // probe: the MMA side's bound (constant draws)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ge[q] = (double)(zz[q] & 255) * 0x1p-6, go[q] = 0.5;
+        for (int q = 0; q < 4; ++q) ge[q] = (double)(zz[q] & 255) * 0x1p45 * (lv != 0.0), go[q] = 0x1p50;
 #else
-        gaussian_pairs_z<4>(T, zz, ge, go);
+        gaussian_pairs_z_scaled<4>(T, zz, lv, ge, go);
 #endif
         uint32_t lo[8], hi[8];
-        // round(w 2^51): the scaling is exact, the conversion rounds; rows past l draw zeros (a zero factor
-        // instead of 16 selects per unit: c3 2.65 -> 2.60 ms, c1 1.767 -> 1.747)
-        const double lv = live[uu] ? 0x1p51 : 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          split64(__double2ll_rn(ge[q] * lv), lo[2 * q], hi[2 * q]);
-          split64(__double2ll_rn(go[q] * lv), lo[2 * q + 1], hi[2 * q + 1]);
+          split64(__double2ll_rn(ge[q]), lo[2 * q], hi[2 * q]);
+          split64(__double2ll_rn(go[q]), lo[2 * q + 1], hi[2 * q + 1]);
         }
 #ifndef CQR_I8_NOGENSTORE  // probe: no Omega digit stores
         transpose_store(lo, hi, planes, 256, om_off(i, 8 * o));
