@@ -188,19 +188,29 @@ __device__ __forceinline__ int om_off(int r, int k) {
 
 // 8 consecutive entries (k = 8o .. 8o+7 of one row) as 64-bit two's complement integers (lo, hi words)
 // -> digit plane s (byte 6 - s) receives the 8 bytes [entry 0 .. entry 7] at plane s + off: an 8x7
-// byte transpose with prmt
+// byte transpose as four 4x4 byte transposes (two prmt stages each: 30 prmt, 3 per stored word pair;
+// a per-plane gather took 42)
+__device__ __forceinline__ void transpose4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&t)[4],
+                                           bool need3) {
+  const uint32_t a0 = __byte_perm(w0, w1, 0x5140u), a2 = __byte_perm(w2, w3, 0x5140u);  // bytes 0, 1 of each pair
+  const uint32_t a1 = __byte_perm(w0, w1, 0x7362u), a3 = __byte_perm(w2, w3, 0x7362u);  // bytes 2, 3
+  t[0] = __byte_perm(a0, a2, 0x5410u);  // byte 0 of w0..w3
+  t[1] = __byte_perm(a0, a2, 0x7632u);  // byte 1
+  t[2] = __byte_perm(a1, a3, 0x5410u);  // byte 2
+  t[3] = need3 ? __byte_perm(a1, a3, 0x7632u) : 0u;  // byte 3 (byte 7 of an entry is not a digit)
+}
 __device__ __forceinline__ void transpose_store(const uint32_t (&lo)[8], const uint32_t (&hi)[8],
                                                 unsigned char* planes, int plane_bytes, int off) {
+  uint32_t la[4], lb[4], ha[4], hb[4];  // bytes 0-3 (lo) and 4-7 (hi) of entries 0-3 (a) and 4-7 (b)
+  transpose4(lo[0], lo[1], lo[2], lo[3], la, true);
+  transpose4(lo[4], lo[5], lo[6], lo[7], lb, true);
+  transpose4(hi[0], hi[1], hi[2], hi[3], ha, false);
+  transpose4(hi[4], hi[5], hi[6], hi[7], hb, false);
 #pragma unroll
   for (int s = 0; s < kDig; ++s) {
     const int b = 6 - s;
-    const uint32_t* w = b < 4 ? lo : hi;
-    const uint32_t bb = (uint32_t)(b & 3);
-    const uint32_t sel = bb | ((bb + 4) << 4);  // out byte 0 = x.byte bb, out byte 1 = y.byte bb
-    const uint32_t x01 = __byte_perm(w[0], w[1], sel), x23 = __byte_perm(w[2], w[3], sel);
-    const uint32_t x45 = __byte_perm(w[4], w[5], sel), x67 = __byte_perm(w[6], w[7], sel);
     *reinterpret_cast<uint2*>(planes + s * plane_bytes + off) =
-        make_uint2(__byte_perm(x01, x23, 0x5410u), __byte_perm(x45, x67, 0x5410u));
+        b < 4 ? make_uint2(la[b], lb[b]) : make_uint2(ha[b - 4], hb[b - 4]);
   }
 }
 
