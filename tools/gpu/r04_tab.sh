@@ -1,3 +1,3 @@
 # full-circle sine table in the i8 sketch generator: timing at the four configs + the sketch / config parity tests
 for cfg in "1000000 128 256" "4000000 256 512" "4194304 64 128" "1000000 512 768"; do timeout 120 python tools/sk_time.py $cfg; done 2>&1 | grep "sketch\|rror" | tee gpurun_out/r04_tab.txt
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py -m gpu -q -k "sketch or config_shape or gaussian" 2>&1 | tail -3 | tee -a gpurun_out/r04_tab.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py -m gpu -q -k "sketch or config_shape or gaussian or box_muller or rng" 2>&1 | tail -3 | tee -a gpurun_out/r04_tab.txt
