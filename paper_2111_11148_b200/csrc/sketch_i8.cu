@@ -621,13 +621,14 @@ __global__ void __launch_bounds__((2 + kI8Slice + GEN + kI8Scan) * 32, 1)
         }
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-          const unsigned y0 = x0[r] & 0x7fffffffu, y1 = x1[r] & 0x7fffffffu;
-          badbits |= (y0 + 0x00100000u) | (y1 + 0x00100000u);  // bit 31 set iff the exponent field is 0x7ff
-          m0 = max(m0, y0);
-          m1 = max(m1, y1);
+          m0 = max(m0, x0[r] & 0x7fffffffu);
+          m1 = max(m1, x1[r] & 0x7fffffffu);
         }
       }
 #endif
+      // non-finite entries: the running maximum reaches the exponent field 0x7ff iff some entry does (bit 31 of
+      // the sum), so one check per sub-chunk replaces one per entry
+      badbits |= (m0 + 0x00100000u) | (m1 + 0x00100000u);
       sexpw[w][lane] = ok0 ? m0 : 0u;
       sexpw[w][32 + lane] = ok1 ? m1 : 0u;
       asm volatile("bar.sync %0, %1;" ::"r"(8), "r"(kI8Scan * 32) : "memory");
