@@ -95,18 +95,19 @@ __device__ __forceinline__ double rsqrt_approx(double x) {
 // every step is issued for all P of them before the next one (P-way ILP).
 // SCALED: the outputs times `scale`, a power of two (or zero) folded into the radius -- exact, so
 // g * scale is bit for bit the scaled draw (one multiply per pair instead of one per draw).
+// The core works on the 53-bit words m1 = b1 >> 11, m2 = b2 >> 11 (the only bits of the draws it uses).
 template <int P, class TT, bool SCALED = false>
-__device__ __forceinline__ void box_muller_bits(const TT& T, const uint64_t (&b1)[P], const uint64_t (&b2)[P],
-                                                double (&g_even)[P], double (&g_odd)[P], double scale = 1.0) {
+__device__ __forceinline__ void box_muller_top53(const TT& T, const uint64_t (&m1)[P], const uint64_t (&m2)[P],
+                                                 double (&g_even)[P], double (&g_odd)[P], double scale = 1.0) {
   double n1[P], a[P], fk[P];
   int k[P];
   CQR_BM_EACH {
     // u1 = N1 * 2^-53 with N1 = (b1 >> 11) + 1 in [1, 2^53]: the scaling is folded into the
     // exponent below (N1's double has u1's mantissa bits, its exponent is 53 higher)
-    n1[j] = (double)((b1[j] >> 11) + 1);
+    n1[j] = (double)(m1[j] + 1);
     // a = RN(2 pi) * u2 with u2 = N2 * 2^-53: the power-of-two scaling commutes with the
     // rounding (a is 0 or >= 2^-51), so one multiply by RN(2 pi) * 2^-53 gives the same a
-    const uint64_t n2 = b2[j] >> 11;
+    const uint64_t n2 = m2[j];
     a[j] = (double)n2 * kBmK[15];
     // table point k = round(256 u2) in [0, 256] (k = 256 reduces with 2 pi and reads entry 0)
     const int kk = (int)((n2 + (1ull << 44)) >> 45);
@@ -174,6 +175,21 @@ __device__ __forceinline__ void box_muller_bits(const TT& T, const uint64_t (&b1
   }
 }
 
+template <int P, class TT, bool SCALED = false>
+__device__ __forceinline__ void box_muller_bits(const TT& T, const uint64_t (&b1)[P], const uint64_t (&b2)[P],
+                                                double (&g_even)[P], double (&g_odd)[P], double scale = 1.0) {
+  uint64_t m1[P], m2[P];
+  CQR_BM_EACH m1[j] = b1[j] >> 11, m2[j] = b2[j] >> 11;
+  box_muller_top53<P, TT, SCALED>(T, m1, m2, g_even, g_odd, scale);
+}
+// mix64(z) >> 11 without forming mix64's last xor-shift: (z ^ (z >> 31)) >> 11 = (z >> 11) ^ (z >> 42), and
+// z >> 42 has no high word (two instructions fewer per hash)
+__device__ __forceinline__ uint64_t mix64_top53(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return (z >> 11) ^ (z >> 42);
+}
+
 // Both outputs of Box-Muller pairs p[0..P) (counters 2p -> cos, 2p+1 -> sin; rng.hpp:47-55).
 template <int P>
 __device__ __forceinline__ void gaussian_pairs_fast(const BmTables& T, uint64_t seed, const uint64_t (&p)[P],
@@ -200,12 +216,12 @@ __device__ __forceinline__ void gaussian_pairs_z(const TT& T, const uint64_t (&z
 template <int P, class TT>
 __device__ __forceinline__ void gaussian_pairs_z_scaled(const TT& T, const uint64_t (&z)[P], double scale,
                                                         double (&g_even)[P], double (&g_odd)[P]) {
-  uint64_t b1[P], b2[P];
+  uint64_t m1[P], m2[P];
   CQR_BM_EACH {
-    b1[j] = mix64(z[j]);
-    b2[j] = mix64(z[j] + 0x9E3779B97F4A7C15ull);
+    m1[j] = mix64_top53(z[j]);
+    m2[j] = mix64_top53(z[j] + 0x9E3779B97F4A7C15ull);
   }
-  box_muller_bits<P, TT, true>(T, b1, b2, g_even, g_odd, scale);
+  box_muller_top53<P, TT, true>(T, m1, m2, g_even, g_odd, scale);
 }
 #undef CQR_BM_EACH
 
