@@ -6,8 +6,8 @@
 // ("Ozaki" splitting):
 //   Omega(i,k) = N_ik 2^-51,        N_ik = round(w 2^51),          |N| < 2^55 (|w| < 9 for every draw);
 //   A(k,j)     = M_kj 2^(E_j - 54), M_kj = round(a 2^(54 - E_j)),  |M| < 2^54,
-// E_j the exponent bound of column j over the k-chunk (max |a| < 2^E_j), from a pre-pass that also
-// checks finiteness. The digits are balanced: N = sum_s D_s 2^(8(6-s)) with every D_s in [-128, 127],
+// E_j the exponent bound of column j over the current sub-chunk of the CTA's rows (max |a| < 2^E_j), found by
+// scanner warps of this kernel one sub-chunk ahead (they also check finiteness). The digits are balanced: N = sum_s D_s 2^(8(6-s)) with every D_s in [-128, 127],
 // read off the bytes of N + 0x808080808080 (the lower six bytes with their top bit flipped), so the
 // dropped low-order products are zero-mean and do not drift with K. The 28 digit products with
 // s + t <= 6 accumulate per level u = s + t in TMEM -- exactly: |level| <= 7 * 128^2 * K < 2^31 for
@@ -19,11 +19,17 @@
 //
 // Warp roles (one CTA per SM, 128 Omega rows x 64 columns of A x one k-chunk):
 //   warp 0      TMEM allocation; lane 0 issues the 10 MMAs of each 32-row step (M=128, N<=256, K=32)
-//               and commits them to the stage's `empty` barrier;
-//   warp 1      lane 0 streams A's FP64 rows (32 x 64 tiles) by TMA into a two-stage ring;
-//   warps 2-9   cut A's tile into the 7 digit planes (K-major core-matrix layout, SWIZZLE_NONE); warps
-//               2-5 then run the epilogue (each warp one TMEM lane quadrant);
-//   warps 6..   draw Omega (Box-Muller pairs, 4 side by side) and cut each draw into its digit planes.
+//               and commits them to the stages' `empty` barriers (Omega planes and A planes are two rings);
+//   warp 1      lane 0 streams A's FP64 rows (32 x 64 tiles) by TMA into its own ring;
+//   warps 2-5   cut A's tile into the 7 digit planes (K-major core-matrix layout, SWIZZLE_NONE: one exact
+//               scaling, conversion, four 4x4 byte transposes per 8 entries) and run the epilogue of every
+//               sub-chunk (each warp one TMEM lane quadrant);
+//   next 16     (12 for clusters of 8) draw Omega (Box-Muller pairs, 4 side by side, in teams that take
+//               alternate steps) and cut each draw into its digit planes; with a cluster each CTA draws its
+//               share of the rows and ships it to the partners by bulk copies;
+//   last 4      scan the next sub-chunk's column exponent bounds (and finiteness) from A's high words.
+// The kernel is bound by the SM's issue rate for this mix (profiles/r04_sketch_probes.txt): its time follows the
+// generators' and slicers' instruction counts, hence the care for every prmt and xor below.
 
 #include <cudaTypedefs.h>
 
