@@ -137,17 +137,20 @@ class ClockSampler:
             idx = int(ent)
         return nv, nv.nvmlDeviceGetHandleByIndex(idx)
 
-    def _poll_nvml(self, nv, h):
-        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+    def _sample_nvml(self):
+        nv, h = self.nv, self.h
         bits = [(nv.nvmlClocksEventReasonHwSlowdown, 0), (nv.nvmlClocksEventReasonHwThermalSlowdown, 1),
                 (nv.nvmlClocksEventReasonSwThermalSlowdown, 2), (nv.nvmlClocksEventReasonSwPowerCap, 3)]
+        try:
+            sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((sm, self.mx, [self.NAMES[i] for b, i in bits if mask & b]))
+        except Exception:
+            pass
+
+    def _poll_nvml(self):
         while not self.stop.is_set():
-            try:
-                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((sm, mx, [self.NAMES[i] for b, i in bits if mask & b]))
-            except Exception:
-                pass
+            self._sample_nvml()
             self.stop.wait(0.005)
 
     def _read_smi(self):
@@ -159,9 +162,16 @@ class ClockSampler:
 
     def __enter__(self):
         try:
-            nv, h = self._nvml_handle()
+            # the slow first NVML calls happen here, not in the sampling thread (a 50 ms region once ended before
+            # the thread's first sample); the first sample is taken right after the warm-up steps, the last one
+            # right after the region's last step, so there are always at least two
+            self.nv, self.h = self._nvml_handle()
+            self.mx = float(self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self._sample_nvml()
+            if not self.rows:
+                raise RuntimeError("nvml sample failed")
             self.src = "nvml"
-            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
             self.t.start()
             return self
         except Exception:
@@ -187,6 +197,7 @@ class ClockSampler:
                 self.proc.kill()
         elif self.src == "nvml":
             self.t.join(timeout=1)
+            self._sample_nvml()
 
     def summary(self):
         if not self.rows:
